@@ -508,3 +508,8 @@ uint32_t orc_crc32(const uint8_t* data, uint64_t n) { /* crc32.hpp:12-43 */
     for (uint64_t i = 0; i < n; ++i) state = table[(state ^ data[i]) & 0xFFu] ^ (state >> 8);
     return state ^ 0xFFFFFFFFu;
 }
+
+/* Vectorised form of orc_lossy_roundtrip for the exhaustive parity sweep. */
+void orc_lossy_roundtrip_many(const uint16_t* bits, const uint8_t* scales, uint64_t n, int k, uint16_t* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = orc_lossy_roundtrip(bits[i], scales[i], k);
+}

@@ -106,6 +106,8 @@ int orc_decompress_lossy(const uint8_t* stream, uint64_t stream_len,
                          uint64_t n, uint16_t* out);
 /* Element-wise lossy round trip of one value (oracles.hpp:129-153 / tensorstore.hpp:179-198, :229-236). */
 uint16_t orc_lossy_roundtrip(uint16_t bits, uint8_t scale_byte, int k);
+void orc_lossy_roundtrip_many(const uint16_t* bits, const uint8_t* scales, uint64_t n, int k,
+                              uint16_t* out);
 /* footprint().total() (tensorstore.hpp:242-283) */
 uint64_t orc_footprint_total(uint64_t stream_len, uint64_t mantissa_bytes,
                              uint64_t scale_bytes, uint64_t ndim);

@@ -91,6 +91,7 @@ class Oracle:
         self._crc = fn("crc32", _u32, [_vp, _u64])
         if lib == "port":
             self._lossy_rt = fn("lossy_roundtrip", C.c_uint16, [C.c_uint16, C.c_uint8, _int])
+            self._lossy_rt_many = fn("lossy_roundtrip_many", None, [_vp, _vp, _u64, _int, _vp])
             self._round = fn("round_mantissa", _int, [_int, _int, _vp, _vp])
             self._pack = fn("pack_signed_mantissas", _int, [_vp, _vp, _u64, _int, _vp])
             self._unpack = fn("unpack_signed_mantissas", _int, [_vp, _u64, _int, _u64, _vp, _vp])
@@ -212,6 +213,13 @@ class Oracle:
     # port-only helpers
     def lossy_roundtrip(self, bits: int, scale: int, k: int) -> int:
         return int(self._lossy_rt(bits, scale, k))
+
+    def lossy_roundtrip_many(self, bits, scales, k: int) -> np.ndarray:
+        b = np.ascontiguousarray(bits, dtype=np.uint16)
+        s = np.ascontiguousarray(scales, dtype=np.uint8)
+        out = np.zeros(max(b.size, 1), np.uint16)
+        self._lossy_rt_many(_p(b), _p(s), b.size, k, _p(out))
+        return out[: b.size]
 
     def round_mantissa(self, m: int, k: int):
         a, b = C.c_int(), C.c_int()

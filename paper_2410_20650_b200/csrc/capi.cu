@@ -1,0 +1,909 @@
+// capi.cu -- the C ABI (include/nzgpu.h): blob management, compress /
+// decompress pipelines, grouped decode plans and the host tier that the
+// drop-in C++ API (include/neuzip/*.hpp) calls.
+//
+// No CPU fallback: every data-path function runs the CUDA kernels and
+// returns NZGPU_NO_DEVICE when no GPU is present.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/nzgpu.h"
+#include "nzgpu_internal.cuh"
+
+namespace nzgpu {
+// kernels (split_table.cu, encode.cu, lossy.cu, decode.cu)
+__global__ void split_hist_kernel(const uint16_t*, uint64_t, uint8_t*, uint8_t*, unsigned long long*);
+__global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
+__global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
+                                   uint32_t*);
+__global__ void ans_encode_kernel(const uint8_t*, uint64_t, uint32_t, uint32_t, const EncSym*, uint8_t*, uint64_t,
+                                  uint32_t*, uint2*, uint32_t*);
+__global__ void stream_scan_kernel(const uint32_t*, uint64_t, uint64_t, uint32_t, uint4*, uint8_t*,
+                                   unsigned long long*);
+__global__ void stream_copy_kernel(const uint8_t*, uint64_t, const uint4*, uint8_t*);
+__global__ void lossy_normalize_kernel(const uint16_t*, uint64_t, int, uint32_t, uint8_t*, uint8_t*, uint8_t*,
+                                       uint32_t*);
+__global__ void pack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*, uint64_t);
+__global__ void lossy_roundtrip_kernel(const uint16_t*, const uint8_t*, uint64_t, int, uint16_t*);
+__global__ void seq_decode_kernel(const uint8_t*, const uint4*, const uint64_t*, uint32_t, uint64_t, const uint32_t*,
+                                  uint32_t, uint32_t, uint2*, uint8_t*, uint32_t*);
+__global__ void merge_plane_kernel(const uint8_t*, const uint8_t*, const uint8_t*, uint64_t, int, uint32_t,
+                                   uint16_t*);
+cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int ndesc, const uint64_t* prefix,
+                          const DecodeDesc& one, uint64_t tiles, uint32_t win_cap, cudaStream_t s);
+cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
+uint32_t decode_smem_for(int log2k, uint32_t win_cap);
+}  // namespace nzgpu
+
+using namespace nzgpu;
+
+namespace {
+
+constexpr int kDecodeThreads = 128;
+constexpr uint32_t kIndexMagic = 0x58495A4Eu;  // "NZIX"
+constexpr uint32_t kIndexVersion = 1;
+constexpr uint32_t kFlagIrregular = 2u;
+
+struct IndexHeader {
+    uint32_t magic;
+    uint32_t version;
+    uint32_t chunk_syms;
+    uint32_t interval;
+    uint64_t n;
+    uint64_t nchunks;
+    uint64_t nsub;
+    uint64_t stream_len;
+};
+static_assert(sizeof(IndexHeader) == 48, "index header layout");
+
+thread_local char g_msg[512] = "";
+
+int fail_cuda(cudaError_t e, const char* what) {
+    std::snprintf(g_msg, sizeof(g_msg), "%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? NZGPU_OUT_OF_MEMORY
+           : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? NZGPU_NO_DEVICE
+                                                                            : NZGPU_CUDA_ERROR;
+}
+
+#define CK(call)                                           \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return fail_cuda(e_, #call); \
+    } while (0)
+
+int status_from_bits(uint32_t bits) {
+    if (!bits) return NZGPU_OK;
+    if (bits & kErrNonFinite) return NZGPU_NONFINITE;
+    if (bits & kErrZeroFreq) return NZGPU_INVALID_ARGUMENT;
+    if (bits & kErrTable) return NZGPU_FORMAT_TABLE;
+    if (bits & kErrTruncated) return NZGPU_FORMAT_TRUNCATED;
+    if (bits & kErrDesync) return NZGPU_FORMAT_DESYNC;
+    return NZGPU_FORMAT_LENGTH;
+}
+
+int log2_of(uint32_t k) {
+    switch (k) {
+        case 64: return 6;
+        case 128: return 7;
+        case 256: return 8;
+        default: return -1;
+    }
+}
+
+bool valid_precision(int p) { return p == 7 || p == 0 || p == 1 || p == 3; }
+
+uint64_t mant_bytes(uint64_t n, int p) { return (n * (uint64_t)(p + 1) + 7) / 8; }
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+int device_ready() {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        std::snprintf(g_msg, sizeof(g_msg), "no CUDA device: %s",
+                      e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+        cudaGetLastError();
+        return NZGPU_NO_DEVICE;
+    }
+    return NZGPU_OK;
+}
+
+// One device allocation carved into 256-byte aligned sections.
+struct Carve {
+    uint64_t size = 0;
+    uint64_t take(uint64_t bytes) {
+        const uint64_t off = size;
+        size = align_up(size + bytes, 256);
+        return off;
+    }
+};
+
+unsigned grid_for(uint64_t work, unsigned threads, unsigned cap = 148 * 16) {
+    const uint64_t g = (work + threads - 1) / threads;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ blob --
+struct nzgpu_blob_s {
+    uint64_t n = 0;
+    int precision = 7;
+    uint32_t block = 0;
+    uint32_t chunk_syms = kDefaultChunk;
+    uint32_t interval = 128;
+    int log2k = 7;
+    uint64_t nchunks = 0;
+    uint64_t nsub = 0;
+    uint32_t flags = 0;
+    uint32_t single_symbol = 0;
+    uint32_t max_window = 0;
+    // main allocation
+    void* base = nullptr;
+    uint16_t* freqs = nullptr;
+    uint32_t* lut = nullptr;
+    uint8_t* mant = nullptr;
+    uint64_t mant_len = 0;
+    uint8_t* scales = nullptr;
+    uint64_t scales_len = 0;
+    uint4* chunk_info = nullptr;
+    uint64_t* chunk_sym0 = nullptr;  // irregular framing only
+    uint2* ckpt = nullptr;
+    uint32_t* err = nullptr;
+    uint32_t* scratch_u32 = nullptr;  // 4 words: table info[3] + window
+    // stream allocation
+    uint8_t* stream = nullptr;
+    uint64_t stream_len = 0;
+
+    ~nzgpu_blob_s() {
+        if (base) cudaFree(base);
+        if (stream) cudaFree(stream);
+    }
+
+    DecodeDesc desc(uint16_t* out) const {
+        DecodeDesc d{};
+        d.stream = stream;
+        d.mant = mant;
+        d.scales = scales;
+        d.ckpt = ckpt;
+        d.chunk_info = chunk_info;
+        d.lut = lut;
+        d.out = out;
+        d.err = err;
+        d.n = n;
+        d.chunk_syms = chunk_syms;
+        d.flags = flags & kFlagSingleSymbol;
+        d.single_symbol = single_symbol;
+        d.precision = precision;
+        d.block_size = block ? block : 1;
+        return d;
+    }
+    uint64_t tiles() const { return ceil_div(nsub, kDecodeThreads); }
+};
+
+namespace {
+
+// Allocate the main section block of a blob (everything but the stream).
+int blob_alloc(nzgpu_blob_s* b, bool irregular) {
+    Carve cv;
+    const uint64_t o_freqs = cv.take(512);
+    const uint64_t o_lut = cv.take(16384);
+    const uint64_t o_mant = cv.take(std::max<uint64_t>(b->mant_len, 1) + 16);
+    const uint64_t o_scales = cv.take(std::max<uint64_t>(b->scales_len, 1));
+    const uint64_t o_info = cv.take(std::max<uint64_t>(b->nchunks, 1) * sizeof(uint4));
+    const uint64_t o_sym0 = cv.take(irregular ? std::max<uint64_t>(b->nchunks, 1) * 8 : 8);
+    const uint64_t o_ckpt = cv.take(std::max<uint64_t>(b->nsub, 1) * sizeof(uint2) + 16);
+    const uint64_t o_err = cv.take(64);
+    CK(cudaMalloc(&b->base, cv.size));
+    uint8_t* p = static_cast<uint8_t*>(b->base);
+    b->freqs = reinterpret_cast<uint16_t*>(p + o_freqs);
+    b->lut = reinterpret_cast<uint32_t*>(p + o_lut);
+    b->mant = p + o_mant;
+    b->scales = p + o_scales;
+    b->chunk_info = reinterpret_cast<uint4*>(p + o_info);
+    b->chunk_sym0 = reinterpret_cast<uint64_t*>(p + o_sym0);
+    b->ckpt = reinterpret_cast<uint2*>(p + o_ckpt);
+    b->err = reinterpret_cast<uint32_t*>(p + o_err);
+    b->scratch_u32 = b->err + 4;
+    return NZGPU_OK;
+}
+
+int sync_status(cudaStream_t s, uint32_t* d_err, bool clear) {
+    CK(cudaStreamSynchronize(s));
+    uint32_t bits = 0;
+    CK(cudaMemcpy(&bits, d_err, 4, cudaMemcpyDeviceToHost));
+    if (clear && bits) CK(cudaMemset(d_err, 0, 4));
+    return status_from_bits(bits);
+}
+
+// Host walk of the serialized framing (deserialize_stream, ans.hpp:318-347).
+int walk_stream(const uint8_t* s, uint64_t len, std::vector<uint4>& info, uint64_t& total) {
+    if (len < 4) return NZGPU_FORMAT_TRUNCATED;
+    auto le32 = [&](uint64_t p) {
+        return (uint32_t)s[p] | ((uint32_t)s[p + 1] << 8) | ((uint32_t)s[p + 2] << 16) | ((uint32_t)s[p + 3] << 24);
+    };
+    const uint32_t cnt = le32(0);
+    uint64_t pos = 4;
+    total = 0;
+    info.clear();
+    info.reserve(std::min<uint64_t>(cnt, len / 8 + 1));
+    for (uint32_t c = 0; c < cnt; ++c) {
+        if (len - pos < 8) return NZGPU_FORMAT_TRUNCATED;  // "ans stream: truncated framing"
+        const uint32_t nsym = le32(pos), plen = le32(pos + 4);
+        pos += 8;
+        if (len - pos < plen) return NZGPU_FORMAT_TRUNCATED;
+        info.push_back(make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), plen, nsym));
+        pos += plen;
+        total += nsym;
+    }
+    if (pos != len) return NZGPU_FORMAT_LENGTH;  // "ans stream: trailing bytes"
+    return NZGPU_OK;
+}
+
+// Exponent-table upload + validation (deserialize_table, ans.hpp:120-130)
+// + packed decode LUT; reads back flags.
+int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
+    CK(cudaMemcpyAsync(b->freqs, h_freqs, 512, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(b->scratch_u32, 0, 16, s));
+    build_table_kernel<<<1, 256, 0, s>>>(nullptr, b->freqs, nullptr, nullptr, b->lut, b->scratch_u32);
+    CK(cudaGetLastError());
+    uint32_t info[3];
+    CK(cudaMemcpyAsync(info, b->scratch_u32, 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info[2]) return status_from_bits(info[2]);
+    b->flags |= info[0] & kFlagSingleSymbol;
+    b->single_symbol = info[1];
+    return NZGPU_OK;
+}
+
+int compute_window(nzgpu_blob_s* b, cudaStream_t s) {
+    b->max_window = 0;
+    if ((b->flags & kFlagIrregular) || b->nsub == 0 || (b->flags & kFlagSingleSymbol)) return NZGPU_OK;
+    CK(cudaMemsetAsync(b->scratch_u32 + 3, 0, 4, s));
+    CK(launch_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 3, s));
+    CK(cudaMemcpyAsync(&b->max_window, b->scratch_u32 + 3, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return NZGPU_OK;
+}
+
+int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
+    if (b->n == 0) return NZGPU_OK;
+    if (b->flags & kFlagIrregular) {
+        // Sequential decode of every chunk, then a separate merge.
+        uint8_t* exps = nullptr;
+        CK(cudaMallocAsync(&exps, b->n, s));
+        seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
+            b->stream, b->chunk_info, b->chunk_sym0, 0u, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k,
+            nullptr, exps, b->err);
+        merge_plane_kernel<<<grid_for(b->n, 256), 256, 0, s>>>(exps, b->mant, b->scales, b->n, b->precision,
+                                                                b->block ? b->block : 1, d_out);
+        CK(cudaGetLastError());
+        CK(cudaFreeAsync(exps, s));
+        return NZGPU_OK;
+    }
+    CK(launch_decode(b->log2k, b->precision, nullptr, 0, nullptr, b->desc(d_out), b->tiles(), b->max_window, s));
+    return NZGPU_OK;
+}
+
+// Fill a blob from host sections (reference formats).
+int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, cudaStream_t s) {
+    if (!t || !valid_precision(t->precision)) return NZGPU_INVALID_ARGUMENT;
+    if (interval == 0) interval = NZGPU_DEFAULT_INTERVAL;
+    if (log2_of(interval) < 0) return NZGPU_INVALID_ARGUMENT;
+    if (!t->freqs || (!t->stream && t->stream_len)) return NZGPU_INVALID_ARGUMENT;
+    std::vector<uint4> info;
+    uint64_t total = 0;
+    int rc = walk_stream(t->stream, t->stream_len, info, total);
+    if (rc) return rc;
+    {  // table sum check first (deserialize_table precedes decode)
+        uint32_t sum = 0;
+        for (int i = 0; i < 256; ++i) sum += t->freqs[i];
+        if (sum != kProbScale) return NZGPU_FORMAT_TABLE;
+    }
+    if (total != t->n) return NZGPU_FORMAT_LENGTH;  // tensorstore.hpp:115-117, :218-220
+    if (t->mantissa_len != mant_bytes(t->n, t->precision) || (t->n && !t->mantissas)) {
+        // lossless: FormatError (tensorstore.hpp:115-117); lossy: unpack's
+        // invalid_argument (bitfloat.hpp:151-153).
+        return t->precision == 7 ? NZGPU_FORMAT_LENGTH : NZGPU_INVALID_ARGUMENT;
+    }
+    if (t->precision != 7) {
+        if (t->block_size == 0) return NZGPU_INVALID_ARGUMENT;
+        if (t->scales_len != ceil_div(t->n, t->block_size) || (t->scales_len && !t->scales))
+            return NZGPU_FORMAT_LENGTH;  // tensorstore.hpp:223-227
+    }
+    b->n = t->n;
+    b->precision = t->precision;
+    b->block = t->precision == 7 ? 0 : t->block_size;
+    b->interval = interval;
+    b->log2k = log2_of(interval);
+    b->nchunks = info.size();
+    b->nsub = ceil_div(t->n, interval);
+    b->mant_len = t->mantissa_len;
+    b->scales_len = t->precision == 7 ? 0 : t->scales_len;
+    b->stream_len = t->stream_len;
+    // Uniform framing (every chunk but the last holds S symbols, S % K == 0)
+    // enables the tiled decoder; anything else decodes sequentially.
+    bool uniform = !info.empty();
+    const uint32_t S = info.empty() ? kDefaultChunk : info[0].w;
+    if (uniform && (S == 0 || S % interval)) uniform = false;
+    for (size_t c = 0; uniform && c < info.size(); ++c) {
+        if (c + 1 < info.size() ? info[c].w != S : (info[c].w == 0 || info[c].w > S)) uniform = false;
+    }
+    b->chunk_syms = S;
+    b->flags = uniform || t->n == 0 ? 0u : kFlagIrregular;
+    rc = blob_alloc(b, !uniform);
+    if (rc) return rc;
+    CK(cudaMalloc(&b->stream, align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32));
+    CK(cudaMemsetAsync(b->err, 0, 64, s));
+    if (t->stream_len) CK(cudaMemcpyAsync(b->stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
+    if (t->mantissa_len) CK(cudaMemcpyAsync(b->mant, t->mantissas, t->mantissa_len, cudaMemcpyHostToDevice, s));
+    if (b->scales_len) CK(cudaMemcpyAsync(b->scales, t->scales, b->scales_len, cudaMemcpyHostToDevice, s));
+    if (!info.empty())
+        CK(cudaMemcpyAsync(b->chunk_info, info.data(), info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    if (!uniform && !info.empty()) {
+        std::vector<uint64_t> sym0(info.size());
+        uint64_t acc = 0;
+        for (size_t c = 0; c < info.size(); ++c) {
+            sym0[c] = acc;
+            acc += info[c].w;
+        }
+        CK(cudaMemcpyAsync(b->chunk_sym0, sym0.data(), sym0.size() * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // sym0 is a stack vector
+    }
+    rc = install_table(b, t->freqs, s);
+    if (rc) return rc;
+    if (!uniform || t->n == 0) return NZGPU_OK;
+    bool have_index = false;
+    if (t->index && t->index_len >= sizeof(IndexHeader)) {
+        IndexHeader h;
+        std::memcpy(&h, t->index, sizeof(h));
+        have_index = h.magic == kIndexMagic && h.version == kIndexVersion && h.chunk_syms == S &&
+                     h.interval == interval && h.n == t->n && h.nchunks == info.size() && h.nsub == b->nsub &&
+                     h.stream_len == t->stream_len && t->index_len == sizeof(h) + h.nsub * sizeof(uint2);
+        if (have_index)
+            CK(cudaMemcpyAsync(b->ckpt, static_cast<const uint8_t*>(t->index) + sizeof(h), b->nsub * sizeof(uint2),
+                               cudaMemcpyHostToDevice, s));
+    }
+    if (!have_index) {
+        // K8: rebuild the checkpoint index by decoding every chunk once on
+        // the GPU (full reference validation, ans.hpp:229-256).
+        seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
+            b->stream, b->chunk_info, nullptr, S, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k, b->ckpt,
+            nullptr, b->err);
+        CK(cudaGetLastError());
+        rc = sync_status(s, b->err, true);
+        if (rc) return rc;
+    }
+    return compute_window(b, s);
+}
+
+int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision, uint32_t block,
+                  uint32_t chunk_syms, uint32_t interval, cudaStream_t s) {
+    if (!valid_precision(precision) || n == 0 || !v) return NZGPU_INVALID_ARGUMENT;  // tensorstore.hpp:47-53
+    if (precision != 7 && block == 0) return NZGPU_INVALID_ARGUMENT;              // tensorstore.hpp:146-148
+    if (reinterpret_cast<uintptr_t>(v) & 15) return NZGPU_INVALID_ARGUMENT;
+    if (chunk_syms == 0) chunk_syms = kDefaultChunk;
+    if (interval == 0) interval = NZGPU_DEFAULT_INTERVAL;
+    const int log2k = log2_of(interval);
+    if (log2k < 0 || chunk_syms % interval) return NZGPU_INVALID_ARGUMENT;
+    b->n = n;
+    b->precision = precision;
+    b->block = precision == 7 ? 0 : block;
+    b->chunk_syms = chunk_syms;
+    b->interval = interval;
+    b->log2k = log2k;
+    b->nchunks = ceil_div(n, chunk_syms);
+    b->nsub = ceil_div(n, interval);
+    b->mant_len = mant_bytes(n, precision);
+    b->scales_len = precision == 7 ? 0 : ceil_div(n, block);
+    b->flags = 0;
+    int rc = blob_alloc(b, false);
+    if (rc) return rc;
+    // Temporaries (stream-ordered allocator).
+    const uint64_t slot = align_up(2ull * chunk_syms + 8, 16);
+    Carve cv;
+    const uint64_t o_exps = cv.take(n + 16);
+    const uint64_t o_items = cv.take(precision == 7 ? 16 : n + 16);
+    const uint64_t o_scratch = cv.take(b->nchunks * slot + 16);
+    const uint64_t o_counts = cv.take(256 * 8);
+    const uint64_t o_plen = cv.take(b->nchunks * 4);
+    const uint64_t o_total = cv.take(16);
+    const uint64_t o_enc = cv.take(256 * sizeof(EncSym));
+    const uint64_t o_hdr = cv.take(16);
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), cv.size, s));
+    uint8_t* exps = tmp + o_exps;
+    uint8_t* items = tmp + o_items;
+    uint8_t* scratch = tmp + o_scratch;
+    auto* counts = reinterpret_cast<unsigned long long*>(tmp + o_counts);
+    auto* plen = reinterpret_cast<uint32_t*>(tmp + o_plen);
+    auto* total = reinterpret_cast<unsigned long long*>(tmp + o_total);
+    auto* enc = reinterpret_cast<EncSym*>(tmp + o_enc);
+    uint8_t* hdr = tmp + o_hdr;
+    CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
+    CK(cudaMemsetAsync(b->err, 0, 64, s));
+    if (precision == 7) {
+        split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>(v, n, exps, b->mant, counts);
+    } else {
+        lossy_normalize_kernel<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, s>>>(v, n, precision, block,
+                                                                                       b->scales, exps, items, b->err);
+        byte_hist_kernel<<<grid_for(n / 16 + 1, 256), 256, 0, s>>>(exps, n, counts);
+        pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
+    }
+    build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
+    ans_encode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(exps, n, chunk_syms, (uint32_t)log2k, enc,
+                                                                          scratch, slot, plen, b->ckpt, b->err);
+    stream_scan_kernel<<<1, 1024, 0, s>>>(plen, b->nchunks, n, chunk_syms, b->chunk_info, hdr, total);
+    CK(cudaGetLastError());
+    uint32_t info[3] = {0, 0, 0};
+    uint32_t err_bits = 0;
+    unsigned long long stream_len = 0;
+    CK(cudaMemcpyAsync(info, b->scratch_u32, 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&err_bits, b->err, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&stream_len, total, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (err_bits | info[2]) {
+        cudaFreeAsync(tmp, s);
+        return status_from_bits(err_bits | info[2]);
+    }
+    b->flags = info[0] & kFlagSingleSymbol;
+    b->single_symbol = info[1];
+    b->stream_len = stream_len;
+    CK(cudaMalloc(reinterpret_cast<void**>(&b->stream), align_up(stream_len, 16) + 32));
+    CK(cudaMemcpyAsync(b->stream, hdr, 4, cudaMemcpyDeviceToDevice, s));
+    stream_copy_kernel<<<(unsigned)b->nchunks, 256, 0, s>>>(scratch, slot, b->chunk_info, b->stream);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, s));
+    return compute_window(b, s);
+}
+
+// Device-tier calls run on the caller's stream (NULL = the legacy default
+// stream); host-tier calls (OwnStream) use a private non-blocking stream.
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    bool own = false;
+    explicit StreamGuard(void* user) : s(static_cast<cudaStream_t>(user)) {}
+    struct Own {};
+    explicit StreamGuard(Own) {
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) own = true;
+    }
+    ~StreamGuard() {
+        if (own) cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ plan --
+struct nzgpu_plan_s {
+    int count = 0;
+    int precision = 7;
+    int log2k = 7;
+    uint64_t tiles = 0;
+    uint32_t win_cap = 0;
+    DecodeDesc* d_descs = nullptr;
+    uint64_t* d_prefix = nullptr;
+    uint32_t* d_err = nullptr;
+    ~nzgpu_plan_s() {
+        if (d_descs) cudaFree(d_descs);
+        if (d_prefix) cudaFree(d_prefix);
+        if (d_err) cudaFree(d_err);
+    }
+};
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* nzgpu_status_string(int status) {
+    switch (status) {
+        case NZGPU_OK: return "ok";
+        case NZGPU_INVALID_ARGUMENT: return "invalid argument";
+        case NZGPU_FORMAT_TRUNCATED: return "ans decode: truncated chunk payload";
+        case NZGPU_FORMAT_DESYNC: return "ans decode: state desynchronization";
+        case NZGPU_FORMAT_LENGTH: return "payload length mismatch";
+        case NZGPU_NONFINITE: return "compress_lossy: NaN/Inf in input";
+        case NZGPU_FORMAT_TABLE: return "frequency table does not sum to 4096";
+        case NZGPU_CUDA_ERROR: return "CUDA error";
+        case NZGPU_OUT_OF_MEMORY: return "out of device memory";
+        case NZGPU_NO_DEVICE: return "no CUDA device (the codec has no CPU fallback)";
+        default: return "unknown status";
+    }
+}
+
+int nzgpu_version(void) { return 100; }
+
+const char* nzgpu_last_error_message(void) { return g_msg; }
+
+int nzgpu_device_check(int* device_count) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        count = 0;
+    }
+    if (device_count) *device_count = count;
+    return count > 0 ? NZGPU_OK : NZGPU_NO_DEVICE;
+}
+
+int nzgpu_compress(const uint16_t* d_values, uint64_t n, int precision, uint32_t block_size,
+                   uint32_t chunk_symbols, uint32_t interval, void* cuda_stream, nzgpu_blob* out) {
+    if (!out) return NZGPU_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (int rc = device_ready()) return rc;
+    std::unique_ptr<nzgpu_blob_s> b(new (std::nothrow) nzgpu_blob_s);
+    if (!b) return NZGPU_OUT_OF_MEMORY;
+    StreamGuard sg(cuda_stream);
+    const int rc = compress_into(b.get(), d_values, n, precision, block_size, chunk_symbols, interval, sg.s);
+    if (sg.own) cudaStreamSynchronize(sg.s);
+    if (rc) return rc;
+    *out = b.release();
+    return NZGPU_OK;
+}
+
+int nzgpu_decompress(nzgpu_blob blob, uint16_t* d_out, void* cuda_stream) {
+    if (!blob || (!d_out && blob->n) || (reinterpret_cast<uintptr_t>(d_out) & 15)) return NZGPU_INVALID_ARGUMENT;
+    return decode_blob(blob, d_out, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int nzgpu_blob_status(nzgpu_blob blob, void* cuda_stream) {
+    if (!blob) return NZGPU_INVALID_ARGUMENT;
+    return sync_status(static_cast<cudaStream_t>(cuda_stream), blob->err, true);
+}
+
+int nzgpu_blob_info_get(nzgpu_blob b, nzgpu_blob_info* info) {
+    if (!b || !info) return NZGPU_INVALID_ARGUMENT;
+    std::memset(info, 0, sizeof(*info));
+    info->n = b->n;
+    info->precision = b->precision;
+    info->block_size = b->block;
+    info->chunk_symbols = b->chunk_syms;
+    info->interval = b->interval;
+    info->num_chunks = b->nchunks;
+    info->stream_len = b->stream_len;
+    info->mantissa_len = b->mant_len;
+    info->scales_len = b->scales_len;
+    info->index_len = (b->flags & kFlagIrregular) ? 0 : sizeof(IndexHeader) + b->nsub * sizeof(uint2);
+    info->payload_bytes = b->stream_len + b->mant_len + b->scales_len + 512;
+    info->d_stream = b->stream;
+    info->d_freqs = b->freqs;
+    info->d_mantissas = b->mant;
+    info->d_scales = b->scales_len ? b->scales : nullptr;
+    info->flags = b->flags;
+    info->max_window = b->max_window;
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_free(nzgpu_blob blob) {
+    delete blob;
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_export(nzgpu_blob b, uint16_t* freqs, uint8_t* stream, uint8_t* mantissas, uint8_t* scales,
+                      void* index) {
+    if (!b) return NZGPU_INVALID_ARGUMENT;
+    CK(cudaDeviceSynchronize());
+    if (freqs) CK(cudaMemcpy(freqs, b->freqs, 512, cudaMemcpyDeviceToHost));
+    if (stream && b->stream_len) CK(cudaMemcpy(stream, b->stream, b->stream_len, cudaMemcpyDeviceToHost));
+    if (mantissas && b->mant_len) CK(cudaMemcpy(mantissas, b->mant, b->mant_len, cudaMemcpyDeviceToHost));
+    if (scales && b->scales_len) CK(cudaMemcpy(scales, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
+    if (index && !(b->flags & kFlagIrregular)) {
+        IndexHeader h{kIndexMagic, kIndexVersion, b->chunk_syms, b->interval, b->n, b->nchunks, b->nsub, b->stream_len};
+        std::memcpy(index, &h, sizeof(h));
+        if (b->nsub)
+            CK(cudaMemcpy(static_cast<uint8_t*>(index) + sizeof(h), b->ckpt, b->nsub * sizeof(uint2),
+                          cudaMemcpyDeviceToHost));
+    }
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_import(const nzgpu_host_tensor* t, uint32_t interval, void* cuda_stream, nzgpu_blob* out) {
+    if (!out) return NZGPU_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (int rc = device_ready()) return rc;
+    std::unique_ptr<nzgpu_blob_s> b(new (std::nothrow) nzgpu_blob_s);
+    if (!b) return NZGPU_OUT_OF_MEMORY;
+    StreamGuard sg(cuda_stream);
+    const int rc = import_into(b.get(), t, interval, sg.s);
+    cudaStreamSynchronize(sg.s);
+    if (rc) return rc;
+    *out = b.release();
+    return NZGPU_OK;
+}
+
+int nzgpu_plan_create(const nzgpu_blob* blobs, uint16_t* const* d_outs, int count, nzgpu_plan* out) {
+    if (!out || count <= 0 || !blobs || !d_outs) return NZGPU_INVALID_ARGUMENT;
+    *out = nullptr;
+    std::unique_ptr<nzgpu_plan_s> p(new (std::nothrow) nzgpu_plan_s);
+    if (!p) return NZGPU_OUT_OF_MEMORY;
+    p->count = count;
+    p->precision = blobs[0]->precision;
+    p->log2k = blobs[0]->log2k;
+    std::vector<DecodeDesc> descs;
+    std::vector<uint64_t> prefix;
+    CK(cudaMalloc(&p->d_err, 16));
+    CK(cudaMemset(p->d_err, 0, 16));
+    uint64_t tiles = 0;
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = blobs[i];
+        if (!b || b->precision != p->precision || b->log2k != p->log2k || (b->flags & kFlagIrregular) ||
+            (reinterpret_cast<uintptr_t>(d_outs[i]) & 15))
+            return NZGPU_INVALID_ARGUMENT;
+        if (b->n == 0) continue;
+        DecodeDesc d = b->desc(d_outs[i]);
+        d.err = p->d_err;
+        descs.push_back(d);
+        prefix.push_back(tiles);
+        tiles += b->tiles();
+        p->win_cap = std::max(p->win_cap, b->max_window);
+    }
+    p->tiles = tiles;
+    p->count = (int)descs.size();
+    if (!descs.empty()) {
+        CK(cudaMalloc(&p->d_descs, descs.size() * sizeof(DecodeDesc)));
+        CK(cudaMalloc(&p->d_prefix, prefix.size() * sizeof(uint64_t)));
+        CK(cudaMemcpy(p->d_descs, descs.data(), descs.size() * sizeof(DecodeDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_prefix, prefix.data(), prefix.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    }
+    *out = p.release();
+    return NZGPU_OK;
+}
+
+int nzgpu_plan_launch(nzgpu_plan p, void* cuda_stream) {
+    if (!p) return NZGPU_INVALID_ARGUMENT;
+    if (!p->tiles) return NZGPU_OK;
+    DecodeDesc none{};
+    CK(launch_decode(p->log2k, p->precision, p->d_descs, p->count, p->d_prefix, none, p->tiles, p->win_cap,
+                     static_cast<cudaStream_t>(cuda_stream)));
+    return NZGPU_OK;
+}
+
+int nzgpu_plan_status(nzgpu_plan p, void* cuda_stream) {
+    if (!p) return NZGPU_INVALID_ARGUMENT;
+    return sync_status(static_cast<cudaStream_t>(cuda_stream), p->d_err, true);
+}
+
+int nzgpu_plan_free(nzgpu_plan p) {
+    delete p;
+    return NZGPU_OK;
+}
+
+int nzgpu_plan_launch_count(nzgpu_plan p) { return p && p->tiles ? 1 : 0; }
+
+// ---------------------------------------------------------------- host tier
+int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint32_t block_size,
+                        uint32_t chunk_symbols, uint32_t interval, nzgpu_blob* out) {
+    if (!out) return NZGPU_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (int rc = device_ready()) return rc;
+    if (!values || n == 0) return NZGPU_INVALID_ARGUMENT;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint16_t* d = nullptr;
+    CK(cudaMallocAsync(&d, n * 2 + 16, sg.s));
+    CK(cudaMemcpyAsync(d, values, n * 2, cudaMemcpyHostToDevice, sg.s));
+    std::unique_ptr<nzgpu_blob_s> b(new (std::nothrow) nzgpu_blob_s);
+    int rc = compress_into(b.get(), d, n, precision, block_size, chunk_symbols, interval, sg.s);
+    cudaFreeAsync(d, sg.s);
+    cudaStreamSynchronize(sg.s);
+    if (rc) return rc;
+    *out = b.release();
+    return NZGPU_OK;
+}
+
+namespace {
+struct HostCtx {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    uint16_t* out[2] = {nullptr, nullptr};
+    uint64_t out_cap[2] = {0, 0};
+    ~HostCtx() {
+        for (int i = 0; i < 2; ++i) {
+            if (out[i]) cudaFree(out[i]);
+            if (s[i]) cudaStreamDestroy(s[i]);
+        }
+    }
+    int ensure(int i, uint64_t bytes) {
+        if (!s[i]) CK(cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking));
+        if (out_cap[i] < bytes) {
+            if (out[i]) cudaFree(out[i]);
+            out[i] = nullptr;
+            out_cap[i] = 0;
+            CK(cudaMalloc(&out[i], bytes));
+            out_cap[i] = bytes;
+        }
+        return NZGPU_OK;
+    }
+};
+thread_local std::unique_ptr<HostCtx> g_host;
+}  // namespace
+
+int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t* const* outs) {
+    if (count < 0 || (count && (!ts || !outs))) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    if (!g_host) g_host.reset(new HostCtx);
+    HostCtx& h = *g_host;
+    std::unique_ptr<nzgpu_blob_s> blobs[2];
+    for (int i = 0; i < count; ++i) {
+        const int slot = i & 1;
+        const nzgpu_host_tensor* t = ts + i;
+        if (int rc = h.ensure(slot, align_up(t->n * 2, 16) + 16)) return rc;
+        cudaStream_t s = h.s[slot];
+        blobs[slot].reset(new nzgpu_blob_s);  // frees the blob from i-2 (its stream work is done)
+        if (int rc = import_into(blobs[slot].get(), t, 0, s)) return rc;
+        if (int rc = decode_blob(blobs[slot].get(), h.out[slot], s)) return rc;
+        if (t->n) CK(cudaMemcpyAsync(outs[i], h.out[slot], t->n * 2, cudaMemcpyDeviceToHost, s));
+        if (int rc = sync_status(s, blobs[slot]->err, true)) return rc;
+    }
+    return NZGPU_OK;
+}
+
+int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out) { return nzgpu_decompress_host_batch(t, 1, &out); }
+
+// ------------------------------------------------------------ building blocks
+int nzgpu_split(const uint16_t* d_values, uint64_t n, uint8_t* d_exponents, uint8_t* d_signmant, uint64_t* d_counts,
+                void* cuda_stream) {
+    if ((reinterpret_cast<uintptr_t>(d_values) & 15) || (reinterpret_cast<uintptr_t>(d_exponents) & 7) ||
+        (reinterpret_cast<uintptr_t>(d_signmant) & 7))
+        return NZGPU_INVALID_ARGUMENT;
+    if (n == 0) return NZGPU_OK;
+    split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+        d_values, n, d_exponents, d_signmant, reinterpret_cast<unsigned long long*>(d_counts));
+    CK(cudaGetLastError());
+    return NZGPU_OK;
+}
+
+int nzgpu_build_table(const uint64_t* d_counts, uint16_t* d_freqs, void* cuda_stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    uint32_t* info = nullptr;
+    CK(cudaMallocAsync(&info, 16, s));
+    CK(cudaMemsetAsync(info, 0, 16, s));
+    build_table_kernel<<<1, 256, 0, s>>>(reinterpret_cast<const unsigned long long*>(d_counts), nullptr, d_freqs,
+                                         nullptr, nullptr, info);
+    CK(cudaGetLastError());
+    uint32_t h[3];
+    CK(cudaMemcpyAsync(h, info, 12, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(info, s));
+    CK(cudaStreamSynchronize(s));
+    return status_from_bits(h[2]);
+}
+
+int nzgpu_build_table_host(const uint64_t* counts, uint16_t* freqs) {
+    if (!counts || !freqs) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint64_t* dc = nullptr;
+    uint16_t* df = nullptr;
+    CK(cudaMallocAsync(&dc, 2048, sg.s));
+    CK(cudaMallocAsync(&df, 512, sg.s));
+    CK(cudaMemcpyAsync(dc, counts, 2048, cudaMemcpyHostToDevice, sg.s));
+    const int rc = nzgpu_build_table(dc, df, sg.s);
+    if (!rc) CK(cudaMemcpyAsync(freqs, df, 512, cudaMemcpyDeviceToHost, sg.s));
+    cudaFreeAsync(dc, sg.s);
+    cudaFreeAsync(df, sg.s);
+    CK(cudaStreamSynchronize(sg.s));
+    return rc;
+}
+
+int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* freqs, uint32_t chunk_symbols,
+                          uint8_t* stream, uint64_t stream_cap, uint64_t* stream_len) {
+    if (!freqs || !stream_len || (n && !symbols)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    if (chunk_symbols == 0) chunk_symbols = kDefaultChunk;
+    uint32_t sum = 0;
+    for (int i = 0; i < 256; ++i) sum += freqs[i];
+    if (sum != kProbScale) return NZGPU_FORMAT_TABLE;
+    const uint64_t nchunks = ceil_div(n, chunk_symbols);
+    if (n == 0) {
+        *stream_len = 4;
+        if (stream_cap < 4) return NZGPU_INVALID_ARGUMENT;
+        std::memset(stream, 0, 4);
+        return NZGPU_OK;
+    }
+    StreamGuard sg{StreamGuard::Own{}};
+    cudaStream_t s = sg.s;
+    const uint64_t slot = align_up(2ull * chunk_symbols + 8, 16);
+    Carve cv;
+    const uint64_t o_sym = cv.take(n + 16), o_scr = cv.take(nchunks * slot + 16), o_plen = cv.take(nchunks * 4);
+    const uint64_t o_info = cv.take(nchunks * 16);
+    const uint64_t o_tot = cv.take(16), o_enc = cv.take(256 * sizeof(EncSym)), o_fr = cv.take(512);
+    const uint64_t o_meta = cv.take(64), o_hdr = cv.take(16);
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), cv.size, s));
+    auto* meta = reinterpret_cast<uint32_t*>(tmp + o_meta);
+    CK(cudaMemsetAsync(meta, 0, 64, s));
+    CK(cudaMemcpyAsync(tmp + o_sym, symbols, n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(tmp + o_fr, freqs, 512, cudaMemcpyHostToDevice, s));
+    build_table_kernel<<<1, 256, 0, s>>>(nullptr, reinterpret_cast<uint16_t*>(tmp + o_fr), nullptr,
+                                         reinterpret_cast<EncSym*>(tmp + o_enc), nullptr, meta);
+    // The raw coder needs no side index: checkpoints off.
+    ans_encode_kernel<<<grid_for(nchunks, 128, 1u << 30), 128, 0, s>>>(
+        tmp + o_sym, n, chunk_symbols, 0u, reinterpret_cast<EncSym*>(tmp + o_enc), tmp + o_scr, slot,
+        reinterpret_cast<uint32_t*>(tmp + o_plen), nullptr, meta + 4);
+    stream_scan_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<uint32_t*>(tmp + o_plen), nchunks, n, chunk_symbols,
+                                          reinterpret_cast<uint4*>(tmp + o_info), tmp + o_hdr,
+                                          reinterpret_cast<unsigned long long*>(tmp + o_tot));
+    CK(cudaGetLastError());
+    uint32_t m[8];
+    unsigned long long total = 0;
+    CK(cudaMemcpyAsync(m, meta, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&total, tmp + o_tot, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int rc = status_from_bits(m[2] | m[4]);
+    if (!rc && total > stream_cap) rc = NZGPU_INVALID_ARGUMENT;
+    uint8_t* dstream = nullptr;
+    if (!rc) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&dstream), align_up(total, 16) + 32, s));
+        CK(cudaMemcpyAsync(dstream, tmp + o_hdr, 4, cudaMemcpyDeviceToDevice, s));
+        stream_copy_kernel<<<(unsigned)nchunks, 256, 0, s>>>(tmp + o_scr, slot, reinterpret_cast<uint4*>(tmp + o_info),
+                                                             dstream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(stream, dstream, total, cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(dstream, s));
+        *stream_len = total;
+    }
+    CK(cudaFreeAsync(tmp, s));
+    CK(cudaStreamSynchronize(s));
+    return rc;
+}
+
+int nzgpu_ans_decode_host(const uint8_t* stream, uint64_t stream_len, const uint16_t* freqs, uint8_t* symbols,
+                          uint64_t n) {
+    if (!stream || !freqs || (n && !symbols)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    // Reuse the tensor import path with a zero mantissa plane; decode symbols only.
+    nzgpu_host_tensor t{};
+    t.n = n;
+    t.precision = 7;
+    t.freqs = freqs;
+    t.stream = stream;
+    t.stream_len = stream_len;
+    std::vector<uint8_t> zeros(n ? n : 1, 0);
+    t.mantissas = zeros.data();
+    t.mantissa_len = n;
+    StreamGuard sg{StreamGuard::Own{}};
+    nzgpu_blob_s b;
+    int rc = import_into(&b, &t, 0, sg.s);
+    if (rc) return rc;
+    if (n == 0) return NZGPU_OK;
+    uint16_t* dout = nullptr;
+    CK(cudaMallocAsync(&dout, n * 2 + 16, sg.s));
+    rc = decode_blob(&b, dout, sg.s);
+    if (!rc) rc = sync_status(sg.s, b.err, true);
+    if (!rc) {
+        // Exponent bytes of the bf16 output are the decoded symbols (mantissas were zero).
+        std::vector<uint16_t> tmp(n);
+        CK(cudaMemcpyAsync(tmp.data(), dout, n * 2, cudaMemcpyDeviceToHost, sg.s));
+        CK(cudaStreamSynchronize(sg.s));
+        for (uint64_t i = 0; i < n; ++i) symbols[i] = (uint8_t)((tmp[i] >> 7) & 0xFF);
+    }
+    cudaFreeAsync(dout, sg.s);
+    cudaStreamSynchronize(sg.s);
+    return rc;
+}
+
+int nzgpu_lossy_roundtrip_host(const uint16_t* values, const uint8_t* scales, uint64_t n, int k, uint16_t* out) {
+    if (k != 0 && k != 1 && k != 3) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    if (n == 0) return NZGPU_OK;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * 5 + 64, sg.s));
+    uint16_t* dv = reinterpret_cast<uint16_t*>(tmp);
+    uint16_t* dout = reinterpret_cast<uint16_t*>(tmp + align_up(n * 2, 16));
+    uint8_t* ds = tmp + 2 * align_up(n * 2, 16);
+    CK(cudaMemcpyAsync(dv, values, n * 2, cudaMemcpyHostToDevice, sg.s));
+    CK(cudaMemcpyAsync(ds, scales, n, cudaMemcpyHostToDevice, sg.s));
+    lossy_roundtrip_kernel<<<grid_for(n, 256), 256, 0, sg.s>>>(dv, ds, n, k, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout, n * 2, cudaMemcpyDeviceToHost, sg.s));
+    CK(cudaFreeAsync(tmp, sg.s));
+    CK(cudaStreamSynchronize(sg.s));
+    return NZGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,162 @@
+// encode.cu -- K3 (chunked rANS encode) and K4 (stream compaction) of the
+// B200 NeuZip codec.
+//
+// K3 restates ans_encode_chunk (ans.hpp:202-225) one chunk per thread: the
+// state is a single serial chain per chunk (format-inherent: one 32-bit
+// state per 65,536-symbol chunk), so parallelism comes from chunks.  The
+// reference's `state / f` and `state % f` become a reciprocal multiply
+// (umulhi with floor(2^32/f)) plus one correction step, exact for every
+// x < 2^32 (tests/test_oracle.py::test_encoder_reciprocal_division_identity).
+// Renormalisation bytes are emitted in reverse consumption order, so they
+// are written backwards from the end of a per-chunk scratch slot; the
+// payload (ans.hpp:222-223) is then contiguous and in decoder order.
+// Every K symbols the encoder also records {state, bytes emitted so far} --
+// the checkpoint side index that lets the decoder split a chunk into
+// independent sub-ranges.
+//
+// K4 restates serialize_stream (ans.hpp:306-316): an exclusive scan of
+// (8 + len) over chunks, then a copy of every payload behind its header.
+#include "nzgpu_internal.cuh"
+
+namespace nzgpu {
+
+__global__ void __launch_bounds__(128) ans_encode_kernel(const uint8_t* __restrict__ exps, uint64_t n,
+                                                         uint32_t chunk_syms, uint32_t log2_interval,
+                                                         const EncSym* __restrict__ enc_g,
+                                                         uint8_t* __restrict__ scratch,
+                                                         uint64_t slot_bytes,
+                                                         uint32_t* __restrict__ payload_len,
+                                                         uint2* __restrict__ ckpt,
+                                                         uint32_t* __restrict__ err) {
+    __shared__ EncSym enc[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) enc[i] = enc_g[i];
+    __syncthreads();
+    const uint64_t nchunks = ceil_div(n, chunk_syms);
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    const uint64_t begin = c * chunk_syms;
+    const uint32_t len = (uint32_t)min((uint64_t)chunk_syms, n - begin);
+    uint8_t* const slot_end = scratch + (c + 1) * slot_bytes;  // 16-byte aligned
+    uint8_t* out = slot_end - 4;
+    const uint8_t* src = exps + begin;
+
+    uint32_t x = kStateLow;
+    uint32_t emitted = 0;
+    for (uint32_t i = len; i-- > 0;) {
+        const uint32_t s = __ldg(src + i);
+        const EncSym e = enc[s];
+        if (e.freq == 0) {  // ans.hpp:210-212
+            atomicOr(err, kErrZeroFreq);
+            return;
+        }
+        // ans.hpp:214-218: at most two renormalisation bytes per symbol.
+        const uint32_t limit = e.freq << 19;
+        while (x >= limit) {
+            *--out = (uint8_t)(x & 0xFFu);
+            x >>= 8;
+            ++emitted;
+        }
+        // ans.hpp:219: x = (x/f << 12) + x%f + cum
+        uint32_t q = __umulhi(x, e.rcp);
+        uint32_t r = x - q * e.freq;
+        if (r >= e.freq) {
+            q += 1;
+            r -= e.freq;
+        }
+        x = (q << kProbBits) + r + e.cum;
+        if (ckpt && (i & ((1u << log2_interval) - 1)) == 0) ckpt[(begin + i) >> log2_interval] = make_uint2(x, emitted);
+    }
+    // ans.hpp:223: final state little-endian at the tail (aligned store).
+    *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
+    payload_len[c] = emitted + 4;
+}
+
+// Exclusive scan of (8 + len) over chunks -> chunk_info {off_lo, off_hi,
+// len, nsym}; writes the stream's leading u32 chunk count and the total
+// stream length.  One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) stream_scan_kernel(const uint32_t* __restrict__ payload_len,
+                                                           uint64_t nchunks, uint64_t n,
+                                                           uint32_t chunk_syms,
+                                                           uint4* __restrict__ chunk_info,
+                                                           uint8_t* __restrict__ stream,
+                                                           unsigned long long* __restrict__ total_out) {
+    __shared__ unsigned long long warp_sums[32];
+    __shared__ unsigned long long carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 4;  // leading u32 chunk count
+    __syncthreads();
+    for (uint64_t base = 0; base < nchunks; base += blockDim.x) {
+        const uint64_t c = base + tid;
+        const unsigned long long v = c < nchunks ? 8ull + payload_len[c] : 0ull;
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) warp_sums[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o) w += y;
+            }
+            warp_sums[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long excl = carry + (warp ? warp_sums[warp - 1] : 0ull) + incl - v;
+        if (c < nchunks) {
+            const uint64_t off = excl + 8;  // payload start
+            const uint32_t nsym = (uint32_t)min((uint64_t)chunk_syms, n - c * chunk_syms);
+            chunk_info[c] = make_uint4((uint32_t)off, (uint32_t)(off >> 32), payload_len[c], nsym);
+        }
+        __syncthreads();
+        if (tid == 0) carry += warp_sums[31];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const uint32_t cnt = (uint32_t)nchunks;
+        stream[0] = cnt & 0xFF;
+        stream[1] = (cnt >> 8) & 0xFF;
+        stream[2] = (cnt >> 16) & 0xFF;
+        stream[3] = cnt >> 24;
+        *total_out = carry;
+    }
+}
+
+// One CTA per chunk: header [nsym][len] + payload copy from the scratch slot.
+__global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restrict__ scratch,
+                                                          uint64_t slot_bytes,
+                                                          const uint4* __restrict__ chunk_info,
+                                                          uint8_t* __restrict__ stream) {
+    const uint64_t c = blockIdx.x;
+    const uint4 ci = chunk_info[c];
+    const uint64_t off = (uint64_t)ci.x | ((uint64_t)ci.y << 32);
+    const uint32_t len = ci.z;
+    const uint8_t* src = scratch + (c + 1) * slot_bytes - len;
+    uint8_t* dst = stream + off;
+    if (threadIdx.x < 8) {
+        const uint32_t v = threadIdx.x < 4 ? ci.w : len;
+        dst[-8 + (int)threadIdx.x] = (uint8_t)(v >> (8 * (threadIdx.x & 3)));
+    }
+    // Byte-granular head until dst is 4-aligned, then word copies assembled
+    // from the (differently aligned) source with funnel shifts.
+    const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3);
+    for (uint32_t i = threadIdx.x; i < min(head, len); i += blockDim.x) dst[i] = src[i];
+    if (len <= head) return;
+    const uint32_t body = (len - head) / 4;
+    const uint8_t* s = src + head;
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst + head);
+    const uint32_t mis = (uint32_t)((uintptr_t)s & 3);
+    const uint32_t* sa = reinterpret_cast<const uint32_t*>(s - mis);
+    for (uint32_t w = threadIdx.x; w < body; w += blockDim.x) {
+        const uint32_t lo = __ldg(sa + w);
+        const uint32_t hi = mis ? __ldg(sa + w + 1) : 0u;
+        d[w] = mis ? __funnelshift_r(lo, hi, 8 * mis) : lo;
+    }
+    for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+}
+
+}  // namespace nzgpu

@@ -1,0 +1,133 @@
+// nzgpu_internal.cuh -- shared definitions of the B200 NeuZip codec kernels.
+//
+// Stream format (unchanged from the reference, ans.hpp:304-316):
+//   [u32 nchunks] then per chunk [u32 nsym][u32 len][payload(len)]
+//   payload = renormalisation bytes in decoder order || LE32(final state)
+// Table: 256 x u16 frequencies summing to 4096 (ans.hpp:111-118).
+//
+// Side index (ours; NOT part of the reference format or the ratio):
+//   ckpt[j] = {state, E} for global symbol j*K, where state is the decoder
+//   state before symbol j*K (= the encoder state after encoding it) and E is
+//   the number of renormalisation bytes that follow the decoder's position
+//   there (bytes the encoder emitted for symbols j*K..end of chunk).  The
+//   decoder position of sub-range j is (len-4) - E; the sentinel after the
+//   last sub-range of a chunk is {2^23, 0}, which is exactly the reference's
+//   end-of-chunk check (ans.hpp:252).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nzgpu {
+
+constexpr uint32_t kProbBits = 12;          // ans.hpp:30
+constexpr uint32_t kProbScale = 1u << 12;   // ans.hpp:31
+constexpr uint32_t kStateLow = 1u << 23;    // ans.hpp:32
+constexpr uint32_t kDefaultChunk = 65536;   // ans.hpp:33
+
+// Device error word bits (sticky, OR-ed by kernels).
+enum : uint32_t {
+    kErrTruncated = 1u << 0,   // ans.hpp:232, :246
+    kErrDesync = 1u << 1,      // ans.hpp:253
+    kErrLength = 1u << 2,      // framing / count mismatch
+    kErrZeroFreq = 1u << 3,    // ans.hpp:210-212 (invalid_argument)
+    kErrNonFinite = 1u << 4,   // tensorstore.hpp:153-157
+    kErrTable = 1u << 5,       // ans.hpp:99-101
+};
+
+// Packed decode LUT entry: sym | (slot - cum) << 8 | freq << 20.
+// freq == 4096 (single-symbol table) does not fit; such tensors take the
+// constant path (flag kFlagSingleSymbol).
+__host__ __device__ inline uint32_t lut_entry(uint32_t sym, uint32_t bias, uint32_t freq) {
+    return sym | (bias << 8) | (freq << 20);
+}
+
+enum : uint32_t { kFlagSingleSymbol = 1u };
+
+// Per-symbol encoder constants (ans.hpp:209-219):
+// rcp = floor(2^32 / f) (f == 1: 0xFFFFFFFF), used with one correction step.
+struct EncSym {
+    uint32_t freq;
+    uint32_t cum;
+    uint32_t rcp;
+    uint32_t pad;
+};
+
+// Device view of one compressed tensor, as the decode kernels consume it.
+struct DecodeDesc {
+    const uint8_t* stream;        // serialized stream (reference layout), 16-B aligned + 16 B pad
+    const uint8_t* mant;          // lossless: n bytes (s<<7|m); lossy: packed (k+1)-bit items
+    const uint8_t* scales;        // lossy block scale bytes
+    const uint2* ckpt;            // {state, E} per K symbols
+    const uint4* chunk_info;      // {payload offset lo, hi, len, nsym} per chunk
+    const uint32_t* lut;          // 4096 packed decode entries
+    uint16_t* out;                // bf16 output, 16-B aligned
+    uint32_t* err;                // sticky error word
+    uint64_t n;                   // elements
+    uint32_t chunk_syms;          // uniform chunk size S (multiple of K)
+    uint32_t flags;               // kFlagSingleSymbol
+    uint32_t single_symbol;       // the exponent when kFlagSingleSymbol
+    int32_t precision;            // 7 lossless, 0/1/3 lossy
+    uint32_t block_size;          // lossy block size B
+    uint32_t pad;
+};
+
+// ------------------------------------------------------------------ PTX --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// TMA bulk copy global -> shared (cp.async.bulk, SASS UBLKCP); dst/src
+// 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// L2 prefetch of a global range (cp.async.bulk.prefetch.L2); 16-byte
+// aligned address, size a multiple of 16.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_u32le_bytes(const uint8_t* p) {
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+// Bf16::from_float, bitfloat.hpp:25-32.
+__device__ __forceinline__ uint16_t bf16_from_float(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u & 0x7FFFFFFFu) > 0x7F800000u) return (uint16_t)((u >> 16) | 0x0040u);
+    return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace nzgpu

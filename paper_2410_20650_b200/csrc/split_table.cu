@@ -1,0 +1,260 @@
+// split_table.cu -- K1 (bit split + exponent histogram) and K2 (frequency
+// table build) of the B200 NeuZip codec.
+//
+// K1 replaces the serial split/count loop of compress_lossless
+// (tensorstore.hpp:93-102): bf16 -> exponent plane + (s<<7|m) byte plane,
+// 256-bin u64 histogram.  HBM-bound: 2 B read + 2 B written per element.
+//
+// K2 restates FrequencyTable::from_counts (ans.hpp:52-93) exactly in one CTA
+// and also emits the derived tables the coder needs: cumulative starts and
+// reciprocals for the encoder (ans.hpp:209-219) and the packed 4096-slot
+// decode LUT (ans.hpp:137-147 slot_to_symbol, plus freq and slot-cum).
+#include "nzgpu_internal.cuh"
+
+namespace nzgpu {
+
+// ------------------------------------------------------------------ K1 ---
+constexpr int kHistCopies = 8;
+
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t e) {
+    // Aggregate equal exponents across the warp first: weight-sharing
+    // Gaussians put most lanes on a handful of bins.
+    const uint32_t peers = __match_any_sync(__activemask(), e);
+    const int leader = __ffs(peers) - 1;
+    if ((threadIdx.x & 31) == leader) atomicAdd(&h[e], __popc(peers));
+}
+
+// Split 8 bf16 (one uint4) into 8 exponent bytes + 8 sign/mantissa bytes.
+__device__ __forceinline__ void split8(uint4 w, uint2& e8, uint2& s8) {
+    const uint32_t in[4] = {w.x, w.y, w.z, w.w};
+    uint32_t e[4], s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t v = in[i];
+        e[i] = ((v >> 7) & 0xFFu) | (((v >> 23) & 0xFFu) << 8);
+        s[i] = (((v >> 8) & 0x80u) | (v & 0x7Fu)) | ((((v >> 24) & 0x80u) | ((v >> 16) & 0x7Fu)) << 8);
+    }
+    e8.x = e[0] | (e[1] << 16);
+    e8.y = e[2] | (e[3] << 16);
+    s8.x = s[0] | (s[1] << 16);
+    s8.y = s[2] | (s[3] << 16);
+}
+
+__global__ void __launch_bounds__(256) split_hist_kernel(const uint16_t* __restrict__ v, uint64_t n,
+                                                         uint8_t* __restrict__ exps,
+                                                         uint8_t* __restrict__ signmant,
+                                                         unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t hist[kHistCopies][256];
+    for (int i = threadIdx.x; i < kHistCopies * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t* h = hist[(threadIdx.x >> 5) & (kHistCopies - 1)];
+
+    const uint64_t groups = n / 8;
+    const uint4* v4 = reinterpret_cast<const uint4*>(v);
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 w = __ldcs(v4 + g);
+        uint2 e8, s8;
+        split8(w, e8, s8);
+        if (exps) reinterpret_cast<uint2*>(exps)[g] = e8;
+        if (signmant) reinterpret_cast<uint2*>(signmant)[g] = s8;
+        if (counts) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) hist_add(h, (e8.x >> (8 * b)) & 0xFFu);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) hist_add(h, (e8.y >> (8 * b)) & 0xFFu);
+        }
+    }
+    // Tail (n % 8 elements) in block 0.
+    if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {
+        const uint64_t i = groups * 8 + threadIdx.x;
+        const uint32_t b = v[i];
+        const uint32_t e = (b >> 7) & 0xFFu;
+        if (exps) exps[i] = (uint8_t)e;
+        if (signmant) signmant[i] = (uint8_t)(((b >> 8) & 0x80u) | (b & 0x7Fu));
+        if (counts) atomicAdd(&h[e], 1u);
+    }
+    if (!counts) return;
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int c = 0; c < kHistCopies; ++c) sum += hist[c][b];
+        if (sum) atomicAdd(counts + b, (unsigned long long)sum);
+    }
+}
+
+// Histogram of an exponent plane (lossy path: post-normalisation exponents,
+// tensorstore.hpp:201-203).
+__global__ void __launch_bounds__(256) byte_hist_kernel(const uint8_t* __restrict__ x, uint64_t n,
+                                                        unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t hist[kHistCopies][256];
+    for (int i = threadIdx.x; i < kHistCopies * 256; i += blockDim.x) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t* h = hist[(threadIdx.x >> 5) & (kHistCopies - 1)];
+    const uint64_t groups = n / 16;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < groups;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 w = reinterpret_cast<const uint4*>(x)[g];
+        const uint32_t in[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) hist_add(h, (in[i] >> (8 * b)) & 0xFFu);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 15)) atomicAdd(&h[x[groups * 16 + threadIdx.x]], 1u);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int c = 0; c < kHistCopies; ++c) sum += hist[c][b];
+        if (sum) atomicAdd(counts + b, (unsigned long long)sum);
+    }
+}
+
+// ------------------------------------------------------------------ K2 ---
+// One CTA of 256 threads; thread s owns symbol s.
+//   info[0] = flags (kFlagSingleSymbol), info[1] = that symbol,
+//   info[2] |= error bits.
+__global__ void __launch_bounds__(256) build_table_kernel(const unsigned long long* __restrict__ counts,
+                                                          const uint16_t* __restrict__ given_freqs,
+                                                          uint16_t* __restrict__ freqs_out,
+                                                          EncSym* __restrict__ enc,
+                                                          uint32_t* __restrict__ lut,
+                                                          uint32_t* __restrict__ info) {
+    __shared__ unsigned long long rem[256];
+    __shared__ uint32_t freq[256];
+    __shared__ uint32_t cum[257];
+    __shared__ unsigned long long red[8];
+    __shared__ uint32_t redf[8];
+    const int s = threadIdx.x;
+    const int lane = s & 31, warp = s >> 5;
+
+    uint32_t f;
+    if (given_freqs) {
+        // FrequencyTable::from_frequencies (ans.hpp:96-103): sum must be 4096.
+        f = given_freqs[s];
+    } else {
+        // ans.hpp:56-70: total, floor(c*4096/T), remainders.
+        const unsigned long long c = counts[s];
+        unsigned long long t = c;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xFFFFFFFFu, t, o);
+        if (lane == 0) red[warp] = t;
+        __syncthreads();
+        unsigned long long total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) total += red[w];
+        if (total == 0) {  // ans.hpp:58-60 -> invalid_argument
+            if (s == 0) atomicOr(info + 2, kErrZeroFreq);
+            return;
+        }
+        const unsigned long long scaled = c * (unsigned long long)kProbScale;
+        f = (uint32_t)(scaled / total);
+        rem[s] = scaled % total;
+        // ans.hpp:72-80: stable sort by remainder desc, +1 to the first
+        // `deficit` entries.  Restated as a rank: the stable position of s.
+        uint32_t a = f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        if (lane == 0) redf[warp] = a;
+        __syncthreads();
+        uint32_t assigned = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) assigned += redf[w];
+        const uint32_t deficit = kProbScale - assigned;
+        const unsigned long long mine = rem[s];
+        uint32_t rank = 0;
+        for (int j = 0; j < 256; ++j) {
+            const unsigned long long r = rem[j];
+            rank += (r > mine) || (r == mine && j < s);
+        }
+        f += rank < deficit ? 1u : 0u;
+        freq[s] = f;
+        __syncthreads();
+        // ans.hpp:83-91: floor-at-1 repair in ascending symbol order, donor =
+        // first argmax of the current frequencies.  Warp 0, serial over the
+        // symbols that need it (a repair never zeroes the donor: max >= 16).
+        if (warp == 0) {
+            for (int base = 0; base < 256; base += 32) {
+                const int sym = base + lane;
+                uint32_t need = __ballot_sync(0xFFFFFFFFu, counts[sym] > 0 && freq[sym] == 0);
+                while (need) {
+                    const int t = base + __ffs(need) - 1;
+                    need &= need - 1;
+                    uint32_t best = 0, best_i = 0;
+                    for (int k = 0; k < 8; ++k) {  // lane owns symbols lane*8 .. lane*8+7
+                        const uint32_t v = freq[lane * 8 + k];
+                        if (v > best) { best = v; best_i = lane * 8 + k; }
+                    }
+                    // first argmax: larger value wins, ties to the lower index
+                    uint64_t key = ((uint64_t)best << 32) | (0xFFFFFFFFu - best_i);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+                        key = other > key ? other : key;
+                    }
+                    const uint32_t donor = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
+                    if (lane == 0) {
+                        freq[donor] -= 1;
+                        freq[t] = 1;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        f = freq[s];
+    }
+    freq[s] = f;
+    __syncthreads();
+    // Cumulative starts (ans.hpp:139-146): inclusive warp scans + warp offsets.
+    uint32_t incl = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) redf[warp] = incl;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += redf[w];
+    cum[s] = off + incl - f;
+    if (s == 255) cum[256] = off + incl;
+    __syncthreads();
+    if (cum[256] != kProbScale) {  // ans.hpp:99-101 FormatError
+        if (s == 0) atomicOr(info + 2, kErrTable);
+        return;
+    }
+    if (freqs_out) freqs_out[s] = (uint16_t)f;
+    if (enc) {
+        EncSym e;
+        e.freq = f;
+        e.cum = cum[s];
+        e.rcp = f <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / f);
+        e.pad = 0;
+        enc[s] = e;
+    }
+    if (f == kProbScale) {
+        info[0] = kFlagSingleSymbol;
+        info[1] = (uint32_t)s;
+    }
+    // Decode LUT: thread s fills slots s*16 .. s*16+15 (binary search in cum).
+    if (lut) {
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t slot = (uint32_t)s * 16 + k;
+            // The largest symbol with cum <= slot always has freq > 0
+            // (zero-frequency symbols share the cum of their successor).
+            int lo = 0, hi = 255;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (cum[mid] <= slot) lo = mid; else hi = mid - 1;
+            }
+            const int sym = lo;
+            const uint32_t fs = freq[sym];
+            lut[slot] = lut_entry((uint32_t)sym, slot - cum[sym], fs == kProbScale ? 0u : fs);
+        }
+    }
+}
+
+}  // namespace nzgpu

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+frozen outputs (tests/golden/golden.json, made from the unmodified
+reference) and against the C oracle on the same seeded inputs.  Bit-exact
+everywhere: streams, tables, sign/mantissa planes, scales, decoded bf16."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from tests import golden_cases as G
+from tests import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b):
+    if isinstance(b, np.ndarray):
+        b = np.ascontiguousarray(b).tobytes()
+    return hashlib.sha256(b).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def nz():
+    import paper_2410_20650_b200 as nz
+
+    if nz.nzgpu.device_count() == 0:
+        pytest.fail("no CUDA device visible to a gpu-marked test")
+    return nz
+
+
+# ----------------------------------------------------------- lossless ------
+@pytest.mark.parametrize("case", G.lossless_cases(), ids=lambda c: c[0])
+def test_gpu_lossless_matches_reference(nz, port, golden, case):
+    name, gen, chunk, _ = case
+    rec = golden["lossless"][name]
+    v = gen(port)
+    blob = nz.compress_lossless(v, chunk_symbols=chunk, interval=64 if chunk % 128 else 128)
+    assert blob.freqs.tobytes().hex() == rec["freqs"]
+    assert len(blob.stream) == rec["stream_len"] and sha(blob.stream) == rec["stream_sha"]
+    assert sha(blob.signmant) == rec["signmant_sha"]
+    assert nz.footprint(blob).total() == rec["footprint"]
+    back = nz.decompress_lossless(blob)
+    assert (back == v).all()
+
+
+@pytest.mark.parametrize("case", [c for c in G.lossless_cases() if c[2] == 65536], ids=lambda c: c[0])
+def test_gpu_decodes_reference_produced_streams(nz, port, case):
+    """Streams from the CPU path carry no side index: the GPU rebuilds it
+    (sequential validation, ans.hpp:229-256) and then runs the tiled decoder."""
+    name, gen, chunk, _ = case
+    v = gen(port)
+    freqs, stream, sm = port.compress_lossless(v, chunk)
+    blob = nz.LosslessBlob(nz.TensorMeta((v.size,)), freqs, stream, sm)
+    assert (nz.decompress_lossless(blob) == v).all()
+
+
+@pytest.mark.parametrize("interval", [64, 128, 256])
+def test_gpu_checkpoint_intervals(nz, port, interval):
+    v = port.gaussian_bf16(123, 3 * 65536 + 777, 0.02)
+    blob = nz.compress_lossless(v, interval=interval)
+    f, s, sm = port.compress_lossless(v)
+    assert blob.stream == s and (blob.signmant == sm).all()
+    assert (nz.decompress_lossless(blob) == v).all()
+
+
+def test_gpu_c1_headline_tensor(nz, port, golden):
+    rec = golden["c1_4096sq_seed42"]
+    v = port.gaussian_bf16(42, 4096 * 4096)
+    blob = nz.compress_lossless(v, nz.TensorMeta((4096, 4096)))
+    assert len(blob.stream) == rec["stream_len"] and sha(blob.stream) == rec["stream_sha"]
+    assert nz.footprint(blob).total() == rec["footprint"]
+    assert round(nz.ratio(blob), 6) == round(rec["ratio"], 6)
+    assert (nz.decompress_lossless(blob) == v).all()
+    for k in (0, 1, 3):
+        lb = nz.compress_lossy(v, k, 512)
+        r = rec[f"lossy_k{k}"]
+        assert sha(lb.stream) == r["stream_sha"] and sha(lb.signmant) == r["packed_sha"]
+        assert sha(lb.scales) == r["scales_sha"]
+
+
+# ----------------------------------------------------------- coder ---------
+@pytest.mark.parametrize("case", G.coder_cases(), ids=lambda c: c[0])
+def test_gpu_coder_matches_reference(nz, golden, case):
+    name, gen, _ = case
+    rec = golden["coder"][name]
+    x = gen()
+    freqs = nz.build_table(inputs.counts_of(x))
+    assert freqs.tobytes().hex() == rec["freqs"]
+    stream = nz.ans_encode(x, freqs)
+    assert len(stream) == rec["stream_len"] and sha(stream) == rec["stream_sha"]
+    assert (nz.ans_decode(stream, freqs, x.size) == x).all()
+
+
+def test_gpu_tables_match_reference(nz, golden):
+    for name, counts in G.table_cases():
+        assert nz.build_table(counts).tobytes().hex() == golden["tables"][name], name
+
+
+# ----------------------------------------------------------- lossy ---------
+@pytest.mark.parametrize("case", G.lossy_cases(), ids=lambda c: c[0])
+def test_gpu_lossy_matches_reference(nz, port, golden, case):
+    name, gen, k, block, _ = case
+    rec = golden["lossy"][name]
+    v = gen(port)
+    blob = nz.compress_lossy(v, k, block)
+    assert blob.freqs.tobytes().hex() == rec["freqs"]
+    assert sha(blob.scales) == rec["scales_sha"]
+    assert len(blob.stream) == rec["stream_len"] and sha(blob.stream) == rec["stream_sha"]
+    assert sha(blob.signmant) == rec["packed_sha"]
+    assert nz.footprint(blob).total() == rec["footprint"]
+    back = nz.decompress_lossy(blob)
+    assert sha(back) == rec["decoded_sha"]
+
+
+@pytest.mark.parametrize("k", [0, 1, 3])
+def test_gpu_lossy_elementwise_exhaustive(nz, port, k):
+    """Every finite bf16 pattern x every scale byte (65,280 x 256 pairs)
+    against the oracle's double-precision restatement."""
+    pats = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    pats = pats[(pats & 0x7F80) != 0x7F80]
+    vals = np.tile(pats, 256)
+    scales = np.repeat(np.arange(256, dtype=np.uint8), pats.size)
+    got = nz.lossy_roundtrip(vals, scales, k)
+    want = port.lossy_roundtrip_many(vals, scales, k)
+    assert (got == want).all(), int((got != want).sum())
+
+
+def test_gpu_lossy_decodes_reference_produced_blobs(nz, port):
+    v = port.gaussian_bf16(31, 200003, 0.02)
+    for k, B in ((0, 512), (1, 7), (3, 64)):
+        f, sc, st, pk = port.compress_lossy(v, k, B)
+        blob = nz.LossyBlob(nz.TensorMeta((v.size,)), k, B, sc, f, st, pk)
+        assert (nz.decompress_lossy(blob) == port.decompress_lossy(f, sc, st, pk, k, B, v.size)).all()
+
+
+# ----------------------------------------------------------- errors --------
+def test_gpu_error_contract(nz, port):
+    # test_tensorstore.cpp:313-322: meta/stream mismatch and corrupt byte
+    v = port.gaussian_bf16(31, 1000, 0.02)
+    blob = nz.compress_lossless(v)
+    bad_meta = nz.LosslessBlob(nz.TensorMeta((999,)), blob.freqs, blob.stream, blob.signmant[:999])
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(bad_meta)
+    s = bytearray(blob.stream)
+    s[-1] ^= 0x10  # final-state byte of the (only) chunk
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(nz.LosslessBlob(blob.meta, blob.freqs, bytes(s), blob.signmant, blob.index))
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(nz.LosslessBlob(blob.meta, blob.freqs, bytes(s), blob.signmant))
+    # test_ans.cpp:239-249: truncated payload (framing now lies) and tiny payload
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(nz.LosslessBlob(blob.meta, blob.freqs, blob.stream[:-5], blob.signmant))
+    # test_ans.cpp:259-274: trailing bytes
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(nz.LosslessBlob(blob.meta, blob.freqs, blob.stream + b"\0", blob.signmant))
+    # ans.hpp:99-101: table must sum to 4096
+    bad = blob.freqs.copy()
+    bad[0] += 1
+    with pytest.raises(nz.FormatError):
+        nz.decompress_lossless(nz.LosslessBlob(blob.meta, bad, blob.stream, blob.signmant))
+    # tensorstore.hpp:153-157 / :143-148
+    with pytest.raises(nz.NonFiniteError):
+        nz.compress_lossy(np.array([0x3F80, 0x7FC1], np.uint16), 3, 512)
+    with pytest.raises(nz.NonFiniteError):
+        nz.compress_lossy(np.array([0xFF80], np.uint16), 0, 512)
+    with pytest.raises(ValueError):
+        nz.compress_lossy(np.array([0x3F80], np.uint16), 2, 512)
+    with pytest.raises(ValueError):
+        nz.compress_lossy(np.array([0x3F80], np.uint16), 3, 0)
+    with pytest.raises(ValueError):
+        nz.compress_lossless(np.zeros(0, np.uint16))
+    # ans.hpp:210-212: symbol with zero frequency
+    c = np.zeros(256, np.uint64)
+    c[1] = 10
+    with pytest.raises(ValueError):
+        nz.ans_encode(np.array([1, 2, 1], np.uint8), nz.build_table(c))
+    with pytest.raises(ValueError):
+        nz.build_table(np.zeros(256, np.uint64))
+
+
+def test_gpu_corruption_sweep_is_always_detected_or_exact(nz, port):
+    """Flip bytes across the payload (stride 37, like the NZT checksum test
+    test_tensorstore.cpp:279-299 but without a CRC): every decode either
+    raises FormatError or -- if the corruption is invisible to the reference
+    too -- returns exactly what the reference decoder returns."""
+    v = port.gaussian_bf16(29, 70000, 0.02)
+    blob = nz.compress_lossless(v)
+    for pos in range(4, len(blob.stream), 37):
+        s = bytearray(blob.stream)
+        s[pos] ^= 0x40
+        try:
+            ref = port.decompress_lossless(blob.freqs, bytes(s), blob.signmant, v.size)
+        except Exception:
+            ref = None
+        try:
+            got = nz.decompress_lossless(nz.LosslessBlob(blob.meta, blob.freqs, bytes(s), blob.signmant, blob.index))
+        except nz.FormatError:
+            got = None
+        if got is not None:
+            assert ref is not None and (got == ref).all(), pos
+
+
+# ----------------------------------------------------------- device API ----
+def test_gpu_device_blob_and_plan(nz, port):
+    import torch
+
+    tensors = [port.gaussian_bf16(port.derive(42, i), n, 0.02) for i, n in enumerate([4096, 70000, 1 << 20, 65536 * 3])]
+    tensors.append(np.full(4096, 0x3F80, np.uint16))  # RMSNorm weight: single-symbol table
+    dev = [torch.from_numpy(t.view(np.int16)).cuda() for t in tensors]
+    blobs = [nz.DeviceBlob.compress(d) for d in dev]
+    for b, t in zip(blobs, tensors):
+        f, s, sm = port.compress_lossless(t)
+        h = b.to_host()
+        assert h.stream == s and (h.signmant == sm).all() and (h.freqs == f).all()
+        out = b.decompress()
+        assert (out.view(torch.int16).cpu().numpy().view(np.uint16) == t).all()
+    outs = [torch.empty(t.size, dtype=torch.bfloat16, device="cuda") for t in tensors]
+    plan = nz.DecodePlan(blobs, outs)
+    assert plan.launches == 1
+    plan.launch()
+    plan.status()
+    for o, t in zip(outs, tensors):
+        assert (o.view(torch.int16).cpu().numpy().view(np.uint16) == t).all()
+
+
+def test_gpu_batch_host_decode(nz, port):
+    vs = [port.gaussian_bf16(i, 50000 + 1000 * i, 0.02) for i in range(5)]
+    blobs = [nz.compress_lossless(v) for v in vs]
+    outs = nz.decompress_batch(blobs)
+    for o, v in zip(outs, vs):
+        assert (o == v).all()

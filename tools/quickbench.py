@@ -1,0 +1,37 @@
+"""Quick decode timing of one tensor (dev tool, not the contract bench)."""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2410_20650_b200 as nz
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096 * 4096
+    torch.manual_seed(0)
+    w = (torch.randn(n, device="cuda") * 0.02).to(torch.bfloat16)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for prec in (7, 3, 0):
+        for K in (64, 128, 256):
+            t0 = time.time()
+            blob = nz.DeviceBlob.compress(w, precision=prec, interval=K)
+            torch.cuda.synchronize(); tc = time.time() - t0
+            out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            plan = nz.DecodePlan([blob], [out])
+            for _ in range(3): plan.launch()
+            plan.status()
+            if prec == 7:
+                assert torch.equal(out.view(torch.int16), w.view(torch.int16))
+            times = []
+            for _ in range(20):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+                a.record(); plan.launch(); b.record(); b.synchronize()
+                times.append(a.elapsed_time(b) * 1e-3)
+            t = float(np.median(times))
+            info = blob.info
+            algo = info.payload_bytes + 2 * n
+            print(f"prec={prec} K={K} n={n} compress={tc*1e3:.1f}ms decode={t*1e6:.1f}us "
+                  f"algoGB/s={algo/t/1e9:.1f} frac={algo/t/6536.4e9:.3f} bf16GB/s={2*n/t/1e9:.1f} "
+                  f"ratio={2*n/(info.payload_bytes+35+8):.4f} win={info.max_window}", flush=True)
+            plan.free(); blob.free()
+
+main()
