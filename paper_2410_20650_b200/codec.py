@@ -179,7 +179,7 @@ class DeviceBlob:
     # -- construction
     @classmethod
     def compress(cls, values, precision: int = kLosslessPrecision, block_size: int = kDefaultBlockSize,
-                 chunk_symbols: int = kChunkSymbols, interval: int = N.DEFAULT_INTERVAL, stream=None,
+                 chunk_symbols: int = kChunkSymbols, interval: int = 0, stream=None,
                  meta: Optional[TensorMeta] = None) -> "DeviceBlob":
         """values: CUDA tensor of bf16 (or int16/uint16 bit patterns), 16-B aligned."""
         import torch
@@ -194,7 +194,7 @@ class DeviceBlob:
         return cls(h, meta)
 
     @classmethod
-    def from_host(cls, blob: Blob, interval: int = N.DEFAULT_INTERVAL) -> "DeviceBlob":
+    def from_host(cls, blob: Blob, interval: int = 0) -> "DeviceBlob":
         t, keep = _host_tensor(blob)
         h = C.c_void_p()
         N.check(N.lib.nzgpu_blob_import(C.byref(t), interval, None, C.byref(h)), "import")
@@ -288,7 +288,7 @@ Error = N.Error
 
 # --------------------------------------------------------- reference API ---
 def compress_lossless(values, meta: Optional[TensorMeta] = None, chunk_symbols: int = kChunkSymbols,
-                      interval: int = N.DEFAULT_INTERVAL) -> LosslessBlob:
+                      interval: int = 0) -> LosslessBlob:
     """tensorstore.hpp:87-110"""
     v = _as_u16(values)
     meta = meta or TensorMeta((v.size,))
@@ -306,7 +306,7 @@ def compress_lossless(values, meta: Optional[TensorMeta] = None, chunk_symbols: 
 
 
 def compress_lossy(values, k: int, block_size: int = kDefaultBlockSize, meta: Optional[TensorMeta] = None,
-                   chunk_symbols: int = kChunkSymbols, interval: int = N.DEFAULT_INTERVAL) -> LossyBlob:
+                   chunk_symbols: int = kChunkSymbols, interval: int = 0) -> LossyBlob:
     """tensorstore.hpp:141-213"""
     if k not in (0, 1, 3):
         raise ValueError("compress_lossy: precision must be 0, 1 or 3")

@@ -155,6 +155,7 @@ struct nzgpu_blob_s {
     uint64_t scales_len = 0;
     uint4* chunk_info = nullptr;
     uint64_t* chunk_sym0 = nullptr;  // irregular framing only
+    bool sym0_valid = false;          // chunk_sym0 filled (imported non-uniform framing)
     uint2* ckpt = nullptr;
     uint32_t* err = nullptr;
     uint32_t* scratch_u32 = nullptr;  // 4 words: table info[3] + window
@@ -280,7 +281,8 @@ int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
         uint8_t* exps = nullptr;
         CK(cudaMallocAsync(&exps, b->n, s));
         seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
-            b->stream, b->chunk_info, b->chunk_sym0, 0u, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k,
+            b->stream, b->chunk_info, b->sym0_valid ? b->chunk_sym0 : nullptr, b->chunk_syms, b->nchunks, b->lut,
+            b->flags & kFlagSingleSymbol, b->log2k,
             nullptr, exps, b->err);
         merge_plane_kernel<<<grid_for(b->n, 256), 256, 0, s>>>(exps, b->mant, b->scales, b->n, b->precision,
                                                                 b->block ? b->block : 1, d_out);
@@ -295,8 +297,7 @@ int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
 // Fill a blob from host sections (reference formats).
 int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, cudaStream_t s) {
     if (!t || !valid_precision(t->precision)) return NZGPU_INVALID_ARGUMENT;
-    if (interval == 0) interval = NZGPU_DEFAULT_INTERVAL;
-    if (log2_of(interval) < 0) return NZGPU_INVALID_ARGUMENT;
+    if (interval != 0 && log2_of(interval) < 0) return NZGPU_INVALID_ARGUMENT;
     if (!t->freqs || (!t->stream && t->stream_len)) return NZGPU_INVALID_ARGUMENT;
     std::vector<uint4> info;
     uint64_t total = 0;
@@ -317,6 +318,10 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
         if (t->block_size == 0) return NZGPU_INVALID_ARGUMENT;
         if (t->scales_len != ceil_div(t->n, t->block_size) || (t->scales_len && !t->scales))
             return NZGPU_FORMAT_LENGTH;  // tensorstore.hpp:223-227
+    }
+    if (interval == 0) {  // auto: the default stride if it divides the chunk size, else 64
+        const uint32_t s0 = info.empty() ? kDefaultChunk : info[0].w;
+        interval = s0 % NZGPU_DEFAULT_INTERVAL == 0 ? NZGPU_DEFAULT_INTERVAL : 64;
     }
     b->n = t->n;
     b->precision = t->precision;
@@ -355,6 +360,7 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
             acc += info[c].w;
         }
         CK(cudaMemcpyAsync(b->chunk_sym0, sym0.data(), sym0.size() * 8, cudaMemcpyHostToDevice, s));
+        b->sym0_valid = true;
         CK(cudaStreamSynchronize(s));  // sym0 is a stack vector
     }
     rc = install_table(b, t->freqs, s);
@@ -390,9 +396,16 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
     if (precision != 7 && block == 0) return NZGPU_INVALID_ARGUMENT;              // tensorstore.hpp:146-148
     if (reinterpret_cast<uintptr_t>(v) & 15) return NZGPU_INVALID_ARGUMENT;
     if (chunk_syms == 0) chunk_syms = kDefaultChunk;
-    if (interval == 0) interval = NZGPU_DEFAULT_INTERVAL;
+    // interval 0 = auto: the default stride if it divides S, else 64; chunk
+    // sizes divisible by neither keep the reference format but decode with
+    // the sequential kernel (no side index).
+    bool irregular = false;
+    if (interval == 0) {
+        interval = chunk_syms % NZGPU_DEFAULT_INTERVAL == 0 ? NZGPU_DEFAULT_INTERVAL : 64;
+        irregular = chunk_syms % interval != 0;
+    }
     const int log2k = log2_of(interval);
-    if (log2k < 0 || chunk_syms % interval) return NZGPU_INVALID_ARGUMENT;
+    if (log2k < 0 || (!irregular && chunk_syms % interval)) return NZGPU_INVALID_ARGUMENT;
     b->n = n;
     b->precision = precision;
     b->block = precision == 7 ? 0 : block;
@@ -438,8 +451,8 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
         pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
     }
     build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
-    ans_encode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(exps, n, chunk_syms, (uint32_t)log2k, enc,
-                                                                          scratch, slot, plen, b->ckpt, b->err);
+    ans_encode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
+        exps, n, chunk_syms, (uint32_t)log2k, enc, scratch, slot, plen, irregular ? nullptr : b->ckpt, b->err);
     stream_scan_kernel<<<1, 1024, 0, s>>>(plen, b->nchunks, n, chunk_syms, b->chunk_info, hdr, total);
     CK(cudaGetLastError());
     uint32_t info[3] = {0, 0, 0};
@@ -453,7 +466,7 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
         cudaFreeAsync(tmp, s);
         return status_from_bits(err_bits | info[2]);
     }
-    b->flags = info[0] & kFlagSingleSymbol;
+    b->flags = (info[0] & kFlagSingleSymbol) | (irregular ? kFlagIrregular : 0u);
     b->single_symbol = info[1];
     b->stream_len = stream_len;
     CK(cudaMalloc(reinterpret_cast<void**>(&b->stream), align_up(stream_len, 16) + 32));

@@ -34,7 +34,7 @@ def test_gpu_lossless_matches_reference(nz, port, golden, case):
     name, gen, chunk, _ = case
     rec = golden["lossless"][name]
     v = gen(port)
-    blob = nz.compress_lossless(v, chunk_symbols=chunk, interval=64 if chunk % 128 else 128)
+    blob = nz.compress_lossless(v, chunk_symbols=chunk)
     assert blob.freqs.tobytes().hex() == rec["freqs"]
     assert len(blob.stream) == rec["stream_len"] and sha(blob.stream) == rec["stream_sha"]
     assert sha(blob.signmant) == rec["signmant_sha"]

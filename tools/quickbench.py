@@ -1,4 +1,5 @@
-"""Quick decode timing of one tensor (dev tool, not the contract bench)."""
+"""Quick decode timing of one tensor (dev tool, not the contract bench).
+usage: quickbench.py [n] [precisions e.g. 7,3,0] [intervals e.g. 64,128,256] [iters]"""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -6,11 +7,14 @@ import paper_2410_20650_b200 as nz
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096 * 4096
+    precs = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "7,3,0").split(",")]
+    ks = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "64,128,256").split(",")]
+    iters = int(sys.argv[4]) if len(sys.argv) > 4 else 20
     torch.manual_seed(0)
     w = (torch.randn(n, device="cuda") * 0.02).to(torch.bfloat16)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for prec in (7, 3, 0):
-        for K in (64, 128, 256):
+    for prec in precs:
+        for K in ks:
             t0 = time.time()
             blob = nz.DeviceBlob.compress(w, precision=prec, interval=K)
             torch.cuda.synchronize(); tc = time.time() - t0
@@ -21,7 +25,7 @@ def main():
             if prec == 7:
                 assert torch.equal(out.view(torch.int16), w.view(torch.int16))
             times = []
-            for _ in range(20):
+            for _ in range(iters):
                 flush.zero_()
                 a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
                 a.record(); plan.launch(); b.record(); b.synchronize()
