@@ -5,9 +5,14 @@ with -lineinfo (ncu source mapping), the nvcc IEEE defaults kept explicit
 (-ftz=false -prec-div=true -prec-sqrt=true; never --use_fast_math: the lossy
 path's __fdiv_rn/__fmul_rn must stay bit-exact with the reference), and
 linked into one shared library with a static CUDA runtime so it loads next to
-torch without library-path games.  nvcc cross-compiles without a GPU."""
+torch without library-path games.  nvcc cross-compiles without a GPU.
+
+Tuning variants (dev only): ``python _build.py --define NZ_CHAINS=4 --out
+libnzgpu_ch4.so`` builds a side library in build_<tag>/ that
+``NZGPU_LIB=<path>`` can point the package at."""
 from __future__ import annotations
 
+import argparse
 import concurrent.futures as cf
 import os
 import subprocess
@@ -15,7 +20,6 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libnzgpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -35,33 +39,42 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > os.path.getmtime(obj) for d in deps if os.path.exists(d))
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+def _compile(args) -> tuple[str, str]:
+    src, build_dir, defines = args
+    obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
     if not _stale(obj, src):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     out = subprocess.run(cmd, capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{out.stdout}\n{out.stderr}")
     return obj, out.stderr
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, defines=(), lib: str = LIB) -> str:
+    tag = "_".join(d.replace("=", "") for d in defines)
+    build_dir = os.path.join(HERE, "build" + (("_" + tag) if tag else ""))
+    os.makedirs(build_dir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        results = list(ex.map(_compile, sources()))
+        results = list(ex.map(_compile, [(s, build_dir, list(defines)) for s in sources()]))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             if log:
                 sys.stderr.write(log)
-    if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+    if not os.path.exists(lib) or any(os.path.getmtime(o) > os.path.getmtime(lib) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError(f"link failed:\n{out.stdout}\n{out.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--define", action="append", default=[])
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    out = os.path.join(HERE, a.out) if a.out else LIB
+    print(build(verbose=a.v, defines=a.define, lib=out))

@@ -40,13 +40,13 @@ cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int
                           const DecodeDesc& one, uint64_t tiles, uint32_t win_cap, cudaStream_t s);
 cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
 uint32_t decode_smem_for(int log2k, uint32_t win_cap);
+uint64_t decode_tiles_for(uint64_t nsub);
 }  // namespace nzgpu
 
 using namespace nzgpu;
 
 namespace {
 
-constexpr int kDecodeThreads = 128;
 constexpr uint32_t kIndexMagic = 0x58495A4Eu;  // "NZIX"
 constexpr uint32_t kIndexVersion = 1;
 constexpr uint32_t kFlagIrregular = 2u;
@@ -186,7 +186,7 @@ struct nzgpu_blob_s {
         d.block_size = block ? block : 1;
         return d;
     }
-    uint64_t tiles() const { return ceil_div(nsub, kDecodeThreads); }
+    uint64_t tiles() const { return decode_tiles_for(nsub); }
 };
 
 namespace {

@@ -1,0 +1,396 @@
+// decode_tiles.cu -- K5/K7: tiled rANS decode fused with bf16 reassembly.
+//
+// Replaces ans_decode (ans.hpp:273-293) + decompress_lossless's merge loop
+// (tensorstore.hpp:119-123) / decompress_lossy's rebuild loop
+// (tensorstore.hpp:229-236) with ONE kernel launch per layer (a plan groups
+// many tensors).  A CTA of 128 threads decodes a tile of 128*kChains
+// sub-ranges of K symbols (the checkpoint side index gives every sub-range
+// its starting state and byte position):
+//
+//   1. thread 0 arms an mbarrier and issues TMA bulk copies (cp.async.bulk,
+//      SASS UBLKCP) of the tensor's 16 KiB packed decode LUT and of the tile's
+//      contiguous payload window, plus an L2 bulk prefetch of the tile's
+//      sign/mantissa bytes;
+//   2. every thread runs kChains independent ANS lanes interleaved for ILP,
+//      entirely out of shared memory: LUT lookup, state transition, a
+//      predicated one-byte renormalisation and a rarely taken second byte.
+//      Four exponents are packed per 32-bit word into a padded
+//      (bank-conflict-free) exponent tile.  Every lane must land exactly on
+//      the next checkpoint -- the reference's end-of-chunk desync check
+//      (ans.hpp:252) applied to every sub-range;
+//   3. the CTA merges exponents with the sign/mantissa plane in 16-element
+//      groups: 128-bit coalesced loads, PRMT/LOP3 bit assembly, two 128-bit
+//      streaming stores per group.
+//
+// Byte format, ratio and every output bit are the reference's.
+#include "decode_common.cuh"
+
+namespace nzgpu {
+
+namespace {
+
+constexpr uint32_t kLutOff = kSmemHeader;
+constexpr uint32_t kExpOff = kSmemHeader + kLutBytes;
+
+template <int LOG2K>
+__host__ __device__ constexpr uint32_t win_off() {
+    return kExpOff + kTileSubs * exps_row_words(LOG2K) * 4;
+}
+
+}  // namespace
+
+// Shared-memory loads on 32-bit shared-window addresses (volatile: they must
+// stay behind the mbarrier wait that publishes the TMA data).
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// One decode step (ans.hpp:240-251).  `lut` is the shared address of the
+// packed LUT, `p` the shared address of the next payload byte and `b` that
+// byte (prefetched).  With v = f<<20 | (slot-cum)<<8 | sym:
+//   f*(x>>12) + slot - cum  ==  f*((x>>12) - 4096) + (v>>8)   (mod 2^32),
+// which saves the bias mask.  One renormalisation byte is predicated; the
+// second (only possible when f < 16) is predicated too.
+#define NZ_DECODE_STEP(lut, x, p, b, v)                                                      \
+    do {                                                                                     \
+        uint32_t a_;                                                                         \
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"((x) & 0xFFFu), "r"(lut));           \
+        v = lds32(a_);                                                                       \
+        x = ((v) >> 20) * (((x) >> kProbBits) - kProbScale) + ((v) >> 8);                    \
+        asm volatile(                                                                        \
+            "{\n\t.reg .pred q;\n\t"                                                         \
+            "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
+            "@q mad.lo.u32 %0, %0, 256, %2;\n\t"                                             \
+            "@q add.u32 %1, %1, 1;\n\t}"                                                     \
+            : "+r"(x), "+r"(p)                                                               \
+            : "r"(b));                                                                       \
+        b = lds8(p);                                                                         \
+        asm volatile(                                                                        \
+            "{\n\t.reg .pred q;\n\t"                                                         \
+            "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
+            "@q mad.lo.u32 %0, %0, 256, %2;\n\t"                                             \
+            "@q add.u32 %1, %1, 1;\n\t"                                                      \
+            "@q ld.shared.u8 %2, [%1];\n\t}"                                                 \
+            : "+r"(x), "+r"(p), "+r"(b));                                                    \
+    } while (0)
+
+template <int LOG2K, int P>
+__global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const DecodeDesc* __restrict__ descs,
+                                                                      int ndesc,
+                                                                      const uint64_t* __restrict__ tile_prefix,
+                                                                      DecodeDesc one, uint32_t win_cap) {
+    constexpr int T = kDecodeThreads;
+    constexpr int CH = kChains;
+    constexpr int TS = kTileSubs;
+    constexpr int K = 1 << LOG2K;
+    constexpr uint32_t RW = exps_row_words(LOG2K);
+    constexpr uint32_t kWinOff = win_off<LOG2K>();
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* exps_s = reinterpret_cast<uint32_t*>(smem + kExpOff);
+    const int tid = threadIdx.x;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t lut = sbase + kLutOff;
+
+    // Locate the tensor of this tile (plans group many tensors per launch).
+    uint64_t tile = blockIdx.x;
+    const DecodeDesc* dp = &one;
+    if (descs) {
+        int lo = 0, hi = ndesc - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(tile_prefix + mid) <= tile) lo = mid; else hi = mid - 1;
+        }
+        dp = descs + lo;
+        tile -= __ldg(tile_prefix + lo);
+    }
+    const DecodeDesc d = *dp;
+    const uint64_t nsub = ceil_div(d.n, K);
+    const uint64_t sub0 = tile * TS;
+    const uint32_t tile_subs = (uint32_t)min((uint64_t)TS, nsub - sub0);
+    const uint64_t sym0 = sub0 << LOG2K;
+    const uint32_t tile_syms = (uint32_t)min((uint64_t)TS * K, d.n - sym0);
+    const bool single = d.flags & kFlagSingleSymbol;
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        uint32_t st = 0;
+        uint64_t wa = 0;
+        if (!single) {
+            uint64_t a, b;
+            tile_window(d, sub0, tile_subs, LOG2K, nsub, a, b);
+            wa = a & ~15ull;
+            uint64_t bytes = ((b + 15) & ~15ull) - wa;
+            if (bytes > win_cap) {  // corrupt index: never overrun shared memory
+                st = kErrDesync;
+                bytes = 0;
+            }
+            mbar_arrive_expect_tx(bar, kLutBytes + (uint32_t)bytes);
+            bulk_g2s(smem + kLutOff, d.lut, kLutBytes, bar);
+            if (bytes) bulk_g2s(smem + kWinOff, d.stream + wa, (uint32_t)bytes, bar);
+        }
+        // Sign/mantissa bytes of the tile: warm L2 while the ANS lanes run.
+        const uint64_t mb = ((uint64_t)tile_syms * (P + 1) / 8) & ~15ull;
+        if (mb) prefetch_l2(d.mant + (sym0 * (P + 1) / 8), (uint32_t)mb);
+        *reinterpret_cast<uint64_t*>(smem + 16) = wa;
+        *reinterpret_cast<uint32_t*>(smem + 24) = st;
+    }
+    __syncthreads();
+
+    const uint64_t wa = *reinterpret_cast<const uint64_t*>(smem + 16);
+    uint32_t errs = *reinterpret_cast<const uint32_t*>(smem + 24);
+    uint32_t x[CH], p[CH], xe[CH], pe[CH], cnt[CH];
+    bool all_full = true;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint32_t r = c * T + tid;  // tile-local sub-range == exponent-tile row
+        cnt[c] = 0;
+        x[c] = xe[c] = kStateLow;
+        p[c] = pe[c] = sbase + kWinOff;
+        if (r < tile_subs) {
+            const uint64_t spc = d.chunk_syms >> LOG2K;
+            const uint64_t j = sub0 + r;
+            const uint64_t ch = j / spc;
+            const uint64_t jin = j - ch * spc;
+            const uint4 ci = d.chunk_info[ch];
+            const uint64_t off = chunk_offset(ci);
+            const uint32_t len = ci.z, nsym = ci.w;
+            const uint32_t sym_in = (uint32_t)(jin << LOG2K);
+            cnt[c] = nsym > sym_in ? min((uint32_t)K, nsym - sym_in) : 0u;
+            if (jin == 0) {
+                // The chunk's framing must agree with the index (ans.hpp:332-340).
+                if (ld_u32le_bytes(d.stream + off - 8) != nsym || ld_u32le_bytes(d.stream + off - 4) != len)
+                    errs |= kErrLength;
+            }
+            if (len < 4) errs |= kErrTruncated;  // ans.hpp:231-233
+            if (single) {
+                // A one-symbol table keeps the state at 2^23 and consumes no
+                // bytes: every chunk payload must be exactly LE32(2^23).
+                if (jin == 0 && len >= 4) {
+                    const uint32_t x0 = ld_u32le_bytes(d.stream + off + len - 4);
+                    if (x0 != kStateLow || len != 4) errs |= x0 < kStateLow ? kErrTruncated : kErrDesync;
+                }
+            } else {
+                const uint32_t limit = len >= 4 ? len - 4 : 0;
+                const uint2 rec = d.ckpt[j];
+                const bool last = sym_in + K >= nsym;
+                const uint2 end = last ? make_uint2(kStateLow, 0u) : d.ckpt[j + 1];
+                const uint32_t e_start = jin == 0 ? limit : rec.y;
+                x[c] = jin == 0 ? ld_u32le_bytes(d.stream + off + limit) : rec.x;
+                xe[c] = end.x;
+                const int64_t p0 = (int64_t)(off + limit - e_start) - (int64_t)wa;
+                const int64_t p1 = (int64_t)(off + limit - min(end.y, limit)) - (int64_t)wa;
+                if (e_start > limit || end.y > limit || p0 < 0 || p0 > (int64_t)win_cap || p1 < p0)
+                    errs |= kErrDesync;
+                else {
+                    p[c] = sbase + kWinOff + (uint32_t)p0;
+                    pe[c] = sbase + kWinOff + (uint32_t)p1;
+                }
+            }
+        }
+        all_full &= cnt[c] == (uint32_t)K;
+    }
+
+    if (single) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            uint32_t* row = exps_s + (c * T + tid) * RW;
+            const uint32_t w = d.single_symbol * 0x01010101u;
+            for (uint32_t i = 0; i < (cnt[c] + 3) / 4; ++i) row[i] = w;
+        }
+    } else {
+        mbar_wait(bar, 0);  // LUT + payload window landed (never exit with a TMA in flight)
+        if (!errs) {
+            uint32_t b[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) b[c] = lds8(p[c]);
+            if (all_full) {
+                // Hot loop: CH independent ANS lanes interleaved per thread.
+#pragma unroll 1
+                for (uint32_t w = 0; w < (uint32_t)K / 4; ++w) {
+                    uint32_t v[CH][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                        for (int c = 0; c < CH; ++c) NZ_DECODE_STEP(lut, x[c], p[c], b[c], v[c][u]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < CH; ++c)
+                        exps_s[(c * T + tid) * RW + w] = __byte_perm(__byte_perm(v[c][0], v[c][1], 0x0040),
+                                                                     __byte_perm(v[c][2], v[c][3], 0x0040), 0x5410);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    uint32_t* row = exps_s + (c * T + tid) * RW;
+                    uint32_t word = 0;
+                    for (uint32_t i = 0; i < cnt[c]; ++i) {
+                        uint32_t v;
+                        NZ_DECODE_STEP(lut, x[c], p[c], b[c], v);
+                        word |= (v & 0xFFu) << (8 * (i & 3));
+                        if ((i & 3) == 3 || i + 1 == cnt[c]) {
+                            row[i >> 2] = word;
+                            word = 0;
+                        }
+                    }
+                }
+            }
+            // End of every lane: the next checkpoint, or the reference's
+            // end-of-chunk condition (x == 2^23, pos == len-4).
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+                if (cnt[c] && (x[c] != xe[c] || p[c] != pe[c])) errs |= p[c] > pe[c] ? kErrTruncated : kErrDesync;
+        }
+    }
+    if (errs) atomicOr(d.err, errs);
+    __syncthreads();
+
+    // ---- merge: exponents (smem) + sign/mantissa plane -> bf16 ---------------
+    const uint32_t groups = tile_syms >> 4;
+    uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
+    if constexpr (P == 7) {
+        const uint4* sm4 = reinterpret_cast<const uint4*>(d.mant + sym0);
+        for (uint32_t g = tid; g < groups; g += T) {
+            const uint32_t e = g << 4;
+            const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
+            const uint4 s = __ldcs(sm4 + g);
+            const uint32_t e0 = er[0], e1 = er[1], e2 = er[2], e3 = er[3];
+            __stcs(out + 2 * g, merge8(e0, s.x, e1, s.y));
+            __stcs(out + 2 * g + 1, merge8(e2, s.z, e3, s.w));
+        }
+        for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
+            const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
+            const uint32_t sm = __ldg(d.mant + sym0 + i);
+            d.out[sym0 + i] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
+        }
+    } else {
+        constexpr uint32_t W = P + 1;
+        const uint8_t* packed = d.mant + sym0 * W / 8;
+        const uint32_t B = d.block_size;
+        for (uint32_t g = tid; g < groups; g += T) {
+            const uint32_t e = g << 4;
+            const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
+            // 16 items = 2W bytes, MSB-first: gather big-endian into the top bits.
+            uint64_t bits;
+            if constexpr (W == 4) {
+                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(packed) + g);
+                bits = ((uint64_t)__byte_perm(v.x, 0, 0x0123) << 32) | __byte_perm(v.y, 0, 0x0123);
+            } else if constexpr (W == 2) {
+                bits = (uint64_t)__byte_perm(__ldcs(reinterpret_cast<const uint32_t*>(packed) + g), 0, 0x0123) << 32;
+            } else {
+                bits = (uint64_t)__byte_perm(__ldcs(reinterpret_cast<const unsigned short*>(packed) + g), 0, 0x0144)
+                       << 32;
+            }
+            const uint64_t gi = sym0 + e;
+            const uint64_t b0 = gi / B;
+            const float c0 = scale_coef(__ldg(d.scales + b0));
+            const uint32_t split = (uint32_t)min((uint64_t)16, (b0 + 1) * B - gi);
+            const float c1 = split < 16 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+            const uint32_t ew[4] = {er[0], er[1], er[2], er[3]};
+            uint32_t res[8];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint32_t ex = (ew[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+                const uint32_t item = (uint32_t)(bits >> (64 - (q + 1) * W)) & ((1u << W) - 1u);
+                float c = q < (int)split ? c0 : c1;
+                if (B < 16 && q >= (int)split) c = scale_coef(__ldg(d.scales + (gi + q) / B));
+                const uint32_t h = lossy_rebuild(item, ex, P, c);
+                if (q & 1) res[q >> 1] |= h << 16; else res[q >> 1] = h;
+            }
+            __stcs(out + 2 * g, make_uint4(res[0], res[1], res[2], res[3]));
+            __stcs(out + 2 * g + 1, make_uint4(res[4], res[5], res[6], res[7]));
+        }
+        for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
+            const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
+            const uint64_t gi = sym0 + i;
+            const uint32_t item = packed_item(d.mant, gi, P);
+            d.out[gi] = lossy_rebuild(item, ex, P, scale_coef(__ldg(d.scales + gi / B)));
+        }
+    }
+}
+
+// Largest payload window any tile of a tensor needs (sizes dynamic smem).
+template <int LOG2K>
+__global__ void window_max_kernel(DecodeDesc d, uint32_t* __restrict__ out) {
+    const uint64_t nsub = ceil_div(d.n, 1u << LOG2K);
+    const uint64_t tiles = ceil_div(nsub, kTileSubs);
+    uint32_t best = 0;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < tiles; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t sub0 = t * kTileSubs;
+        const uint32_t subs = (uint32_t)min((uint64_t)kTileSubs, nsub - sub0);
+        uint64_t a, b;
+        tile_window(d, sub0, subs, LOG2K, nsub, a, b);
+        const uint64_t bytes = ((b + 15) & ~15ull) - (a & ~15ull);
+        best = max(best, (uint32_t)min(bytes, (uint64_t)0xFFFFFFFFu));
+    }
+    atomicMax(out, best);
+}
+
+// ------------------------------------------------------------ launchers --
+template <int LOG2K, int P>
+static cudaError_t launch_decode_t(const DecodeDesc* descs, int ndesc, const uint64_t* prefix, const DecodeDesc& one,
+                                   uint64_t tiles, uint32_t win_cap, cudaStream_t s) {
+    const uint32_t smem = decode_smem_bytes(LOG2K, win_cap);
+    static uint32_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(decode_tiles_kernel<LOG2K, P>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    decode_tiles_kernel<LOG2K, P><<<(unsigned)tiles, kDecodeThreads, smem, s>>>(descs, ndesc, prefix, one, win_cap);
+    return cudaGetLastError();
+}
+
+template <int LOG2K>
+static cudaError_t launch_decode_k(int precision, const DecodeDesc* descs, int ndesc, const uint64_t* prefix,
+                                   const DecodeDesc& one, uint64_t tiles, uint32_t win_cap, cudaStream_t s) {
+    switch (precision) {
+        case 7: return launch_decode_t<LOG2K, 7>(descs, ndesc, prefix, one, tiles, win_cap, s);
+        case 3: return launch_decode_t<LOG2K, 3>(descs, ndesc, prefix, one, tiles, win_cap, s);
+        case 1: return launch_decode_t<LOG2K, 1>(descs, ndesc, prefix, one, tiles, win_cap, s);
+        case 0: return launch_decode_t<LOG2K, 0>(descs, ndesc, prefix, one, tiles, win_cap, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int ndesc, const uint64_t* prefix,
+                          const DecodeDesc& one, uint64_t tiles, uint32_t win_cap, cudaStream_t s) {
+    if (tiles == 0) return cudaSuccess;
+    switch (log2k) {
+        case 6: return launch_decode_k<6>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
+        case 7: return launch_decode_k<7>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
+        case 8: return launch_decode_k<8>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+uint32_t decode_smem_for(int log2k, uint32_t win_cap) {
+    switch (log2k) {
+        case 6: return decode_smem_bytes(6, win_cap);
+        case 7: return decode_smem_bytes(7, win_cap);
+        default: return decode_smem_bytes(8, win_cap);
+    }
+}
+
+uint64_t decode_tiles_for(uint64_t nsub) { return ceil_div(nsub, kTileSubs); }
+
+cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s) {
+    switch (log2k) {
+        case 6: window_max_kernel<6><<<148, 256, 0, s>>>(d, out); break;
+        case 7: window_max_kernel<7><<<148, 256, 0, s>>>(d, out); break;
+        case 8: window_max_kernel<8><<<148, 256, 0, s>>>(d, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace nzgpu

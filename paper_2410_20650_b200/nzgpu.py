@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnzgpu.so")
+# NZGPU_LIB may select an in-tree tuning variant (e.g. libnzgpu_ch4.so).
+LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("NZGPU_LIB", "libnzgpu.so")))
 
 OK, INVALID_ARGUMENT, FORMAT_TRUNCATED, FORMAT_DESYNC, FORMAT_LENGTH = 0, 1, 2, 3, 4
 NONFINITE, FORMAT_TABLE, CUDA_ERROR, OUT_OF_MEMORY, NO_DEVICE = 5, 6, 7, 8, 9
