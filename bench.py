@@ -1,0 +1,471 @@
+"""Headline benchmark: NeuZip layer-by-layer decode of Llama-3-8B-shaped
+weights on B200 (BASELINE.json configs[1]; metric: decode GB/s of
+reconstructed bf16 weights, % of HBM roofline; ratio).
+
+One step = decode every tensor of the model once, layer by layer, each layer
+(7 projections + 2 RMSNorms) as ONE grouped kernel launch into a reused
+output buffer (the reference's Alg. 1 usage: one uncompressed layer live,
+nn.hpp:228-248), plus embed, lm_head and the final norm.
+
+Algorithmic bytes per tensor:
+    stream_len + mantissa_len + scale_len + 512-byte table + 2n (bf16 out)
+i.e. the reference-format compressed payload read plus the bf16 written.
+The checkpoint side index is NOT counted (it is reported as overhead).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision 7|3|1|0]
+    python bench.py --impl reference ...   # the reference's CPU codec arm
+
+Multi-GPU (torchrun, one process per GPU): every rank decodes its own
+Llama-3-8B-shaped model (weak scaling: per-GPU work fixed, no collective on
+the data path); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+# Llama-3-8B: hidden 4096, ffn 14336, 32 layers, 32 heads / 8 KV heads, vocab 128256, untied.
+LLAMA3_8B = dict(hidden=4096, ffn=14336, layers=32, kv=1024, vocab=128256)
+
+
+def llama_layout(cfg=LLAMA3_8B):
+    h, f, kv = cfg["hidden"], cfg["ffn"], cfg["kv"]
+    groups = []
+    for layer in range(cfg["layers"]):
+        groups.append((f"layer{layer}", [
+            ("q_proj", (h, h), "w"), ("k_proj", (kv, h), "w"), ("v_proj", (kv, h), "w"),
+            ("o_proj", (h, h), "w"), ("gate_proj", (f, h), "w"), ("up_proj", (f, h), "w"),
+            ("down_proj", (h, f), "w"), ("input_layernorm", (h,), "norm"),
+            ("post_attention_layernorm", (h,), "norm")]))
+    groups.append(("embed_tokens", [("embed_tokens", (cfg["vocab"], h), "w")]))
+    groups.append(("lm_head", [("lm_head", (cfg["vocab"], h), "w"), ("norm", (h,), "norm")]))
+    return groups
+
+
+def numel(shape):
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", HBM_FALLBACK)), "measured"
+    return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------- GPU arm ---
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_2410_20650_b200 as nz
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    # ---- synthetic model: HF Llama init N(0, 0.02^2) weights, RMSNorm = 1.0,
+    # different tensors per rank (weak scaling: each rank owns a model).
+    groups = llama_layout()
+    blobs, plans_meta = [], []
+    t0 = time.time()
+    gen = torch.Generator(device=dev)
+    tensor_idx = 0
+    for gname, tensors in groups:
+        gb = []
+        for tname, shape, kind in tensors:
+            n = numel(shape)
+            if kind == "norm":
+                w = torch.ones(n, dtype=torch.bfloat16, device=dev)
+            else:
+                gen.manual_seed(args.seed * 1000003 + rank * 10007 + tensor_idx)
+                w = (torch.randn(n, device=dev, generator=gen) * 0.02).to(torch.bfloat16)
+            blob = nz.DeviceBlob.compress(w, precision=args.precision, block_size=args.block,
+                                          interval=args.interval, meta=nz.TensorMeta(shape))
+            if args.verify and kind == "w" and tensor_idx < 10:
+                back = torch.empty_like(w)
+                blob.decompress_into(back)
+                blob.status()
+                if args.precision == 7:
+                    assert torch.equal(back.view(torch.int16), w.view(torch.int16)), f"round trip {tname}"
+            del w
+            gb.append((tname, shape, blob))
+            tensor_idx += 1
+        blobs.append((gname, gb))
+    torch.cuda.synchronize()
+    t_compress = time.time() - t0
+
+    # ---- per-layer grouped decode plans into one reused output buffer
+    max_elems = max(sum(b.n for _, _, b in gb) for _, gb in blobs)
+    outbuf = torch.empty(max_elems + 64 * 16, dtype=torch.bfloat16, device=dev)
+    plans, bytes_algo, total_n, total_fp, index_bytes = [], 0, 0, 0, 0
+    for gname, gb in blobs:
+        outs, off = [], 0
+        for _, _, b in gb:
+            outs.append(outbuf[off:off + b.n])
+            off += (b.n + 63) // 64 * 64  # keep every output 128-byte aligned
+        plans.append(nz.DecodePlan([b for _, _, b in gb], outs))
+        for _, shape, b in gb:
+            i = b.info
+            bytes_algo += int(i.payload_bytes) + 2 * b.n
+            total_n += b.n
+            total_fp += int(i.payload_bytes) + nz.codec.nzt_header_bytes(len(shape))  # footprint().total()
+            index_bytes += int(i.index_len)
+    launches_per_step = sum(p.launches for p in plans)
+
+    # L2 (126 MB) is far smaller than one step's traffic (~26 GB): no flush needed.
+    def step(events=None):
+        for k, p in enumerate(plans):
+            if events is not None:
+                events[k][0].record(stream)
+            p.launch(stream)
+            if events is not None:
+                events[k][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    for p in plans:
+        p.status(stream)
+    torch.cuda.synchronize()
+
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plans]
+          for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for s in range(args.steps):
+            step(ev[s])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    for p in plans:
+        p.status(stream)  # every decode passed its checkpoint/desync checks
+    elapsed = start.elapsed_time(stop) / 1e3
+    kernel_time = sum(a.elapsed_time(b) for row in ev for a, b in row) / 1e3
+    t_max = elapsed
+    if dist:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+
+    value = world * bytes_algo * args.steps / t_max / 1e9
+    peak, peak_kind = load_peaks()
+    achieved = bytes_algo * args.steps / kernel_time / 1e9  # per-launch bytes / launch time, aggregated
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            tj = json.load(fh)
+        if tj.get("precision") == args.precision:
+            traffic = tj.get("dram_bytes_per_algo_byte")
+
+    # ---- e2e through the reference-facing host API (host buffers in/out)
+    e2e = run_e2e(args, nz, blobs, torch) if rank == 0 else None
+    if dist:
+        dist.barrier()
+
+    line = {
+        "metric": "decode GB/s of reconstructed bf16 weights (% HBM roofline); ratio",
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_max / args.steps * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8" if args.precision == 7 else "u8+f32",
+        "data": "synthetic: random-init N(0,0.02^2) bf16 weights (torch.randn on GPU), RMSNorm=1.0",
+        "config": {
+            "workload": "Llama-3-8B-shaped per-layer decode" + ("" if args.precision == 7 else f" lossy k={args.precision} B={args.block}"),
+            "model": "llama-3-8b (random init)",
+            "params_per_gpu": total_n,
+            "precision": args.precision,
+            "chunk_symbols": 65536,
+            "checkpoint_interval": int(blobs[0][1][0][2].info.interval),
+            "launches_per_step": launches_per_step,
+            "bytes_algo_per_step_per_gpu": bytes_algo,
+            "index_bytes_per_gpu": index_bytes,
+            "ratio": round(2 * total_n / total_fp, 6),
+            "l2": "no flush: one step moves ~26 GB >> 126 MB L2",
+            "parallelism": f"weak dp{world}: one model replica per GPU, no collective",
+            "compress_s": round(t_compress, 2),
+        },
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": "decode_tiles_kernel (one launch per layer)"},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+    }
+    if rank == 0:
+        line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, nz, blobs, torch):
+    """Same metric through nzgpu_decompress_host_batch: compressed sections
+    H2D from pinned host memory, GPU decode, bf16 D2H to pinned memory, every
+    step.  Bounded to the first `--e2e-layers` layers to cap host memory."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_2410_20650_b200 import nzgpu as N
+
+    sel = [b for _, gb in blobs[: args.e2e_layers] for _, _, b in gb]
+    hosts = [b.to_host() for b in sel]
+    pinned = []
+
+    def pin(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        pinned.append(t)
+        return t
+
+    ts = []
+    h2d = 0
+    for h in hosts:
+        t = N.HostTensor()
+        f = pin(h.freqs)
+        s = pin(np.frombuffer(h.stream, np.uint8))
+        m = pin(h.signmant)
+        ix = pin(np.frombuffer(h.index, np.uint8)) if h.index else None
+        t.n = h.meta.element_count()
+        t.precision = h.precision
+        t.freqs = f.data_ptr()
+        t.stream, t.stream_len = s.data_ptr(), s.numel()
+        t.mantissas, t.mantissa_len = m.data_ptr(), m.numel()
+        if h.precision != 7:
+            sc = pin(h.scales)
+            t.block_size, t.scales, t.scales_len = h.block_size, sc.data_ptr(), sc.numel()
+            h2d += sc.numel()
+        if ix is not None:
+            t.index, t.index_len = ix.data_ptr(), ix.numel()
+            h2d += ix.numel()
+        h2d += 512 + s.numel() + m.numel()
+        ts.append(t)
+    outs = [torch.empty(h.meta.element_count(), dtype=torch.int16).pin_memory() for h in hosts]
+    arr = (N.HostTensor * len(ts))(*ts)
+    ptrs = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    algo = sum(int(b.info.payload_bytes) + 2 * b.n for b in sel)
+    d2h = sum(2 * b.n for b in sel)
+    N.check(N.lib.nzgpu_decompress_host_batch(arr, len(ts), ptrs), "e2e warmup")
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        N.check(N.lib.nzgpu_decompress_host_batch(arr, len(ts), ptrs), "e2e")
+    dt = time.perf_counter() - t0
+    return {"value": round(algo * steps / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "sample": f"first {args.e2e_layers} layers ({len(sel)} tensors), "
+            f"{steps} steps, nzgpu_decompress_host_batch (pinned host buffers)"}
+
+
+# ------------------------------------------------------ CPU reference arm ---
+def cpu_sample(args):
+    """Bounded sample of the workload for the CPU: the first layer's tensors
+    (same shapes and N(0,0.02^2) init via the reference's own RNG)."""
+    from oracle.oracle import Oracle
+
+    gen = Oracle("port")
+    h, f, kv = 4096, 14336, 1024
+    shapes = [(h, h), (kv, h), (kv, h), (h, h), (f, h), (f, h), (h, f)][: args.cpu_tensors]
+    vals = [gen.gaussian_bf16(gen.derive(42, i), numel(s), 0.02) for i, s in enumerate(shapes)]
+    return shapes, vals
+
+
+def reference_lib():
+    from oracle.oracle import Oracle, ref_available
+
+    if ref_available():
+        return Oracle("ref"), "reference"
+    return Oracle("port"), "port"
+
+
+def cpu_decoders(ref, kind, vals, args):
+    """[(decode_callable, algorithmic_bytes)] for each sample tensor.  With
+    the reference library the blob is parsed once and only the reference's
+    decompress_lossless / decompress_lossy is timed."""
+    out = []
+    for v in vals:
+        if args.precision == 7:
+            f, s, m = ref.compress_lossless(v)
+            algo = len(s) + m.size + 512 + 2 * v.size
+            if kind == "reference":
+                out.append((ref.prepared(f, s, m, v.size).decode, algo))
+            else:
+                out.append((lambda f=f, s=s, m=m, n=v.size: ref.decompress_lossless(f, s, m, n), algo))
+        else:
+            f, sc, s, pk = ref.compress_lossy(v, args.precision, args.block)
+            algo = len(s) + pk.size + sc.size + 512 + 2 * v.size
+            if kind == "reference":
+                out.append((ref.prepared(f, s, pk, v.size, args.precision, sc, args.block).decode, algo))
+            else:
+                out.append((lambda f=f, sc=sc, s=s, pk=pk, n=v.size: ref.decompress_lossy(
+                    f, sc, s, pk, args.precision, args.block, n), algo))
+    return out
+
+
+def cpu_baseline(args):
+    """The reference CPU codec on the GPU box's host cores (rank 0, N=1 only)."""
+    try:
+        ref, kind = reference_lib()
+        shapes, vals = cpu_sample(args)
+        cores = min(os.cpu_count() or 1, 64) if kind == "reference" else 1
+        os.environ["NEUZIP_THREADS"] = str(cores)
+        decs = cpu_decoders(ref, kind, vals, args)
+        algo = 0
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            for fn, a in decs:
+                fn()
+                algo += a
+            reps += 1
+            if time.perf_counter() - t0 > args.cpu_seconds or reps >= 50:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": round(algo / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                "sample": f"decompress of layer-0 tensors {shapes}, {reps} reps, NEUZIP_THREADS={cores} "
+                          f"(reference caps workers at 64, parallel.hpp:24); host nproc={os.cpu_count()}"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": repr(e)}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    ref, kind = reference_lib()
+    cores = min(os.cpu_count() or 1, 64) if kind == "reference" else 1
+    os.environ["NEUZIP_THREADS"] = str(cores)
+    shapes, vals = cpu_sample(args)
+    decs = cpu_decoders(ref, kind, vals, args)
+
+    def step():
+        algo = 0
+        for fn, a in decs:
+            fn()
+            algo += a
+        return algo
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    algo = sum(step() for _ in range(args.steps))
+    dt = time.perf_counter() - t0
+    value = algo / dt / 1e9
+    sample = f"decompress of Llama-3-8B layer-0 tensors {shapes} per step, NEUZIP_THREADS={cores}"
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "decode GB/s of reconstructed bf16 weights (% HBM roofline); ratio",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8" if args.precision == 7 else "u8+f64", "data": "synthetic (reference rng.hpp)",
+        "config": {"workload": "Llama-3-8B-shaped per-layer decode (CPU sample: layer 0)", "precision": args.precision},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--precision", type=int, default=7, choices=[7, 3, 1, 0])
+    ap.add_argument("--block", type=int, default=512)
+    ap.add_argument("--interval", type=int, default=0, help="checkpoint stride K (0 = auto)")
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--e2e-layers", type=int, default=4)
+    ap.add_argument("--cpu-tensors", type=int, default=7)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--verify", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

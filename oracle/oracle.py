@@ -97,6 +97,9 @@ class Oracle:
             self._unpack = fn("unpack_signed_mantissas", _int, [_vp, _u64, _int, _u64, _vp, _vp])
             self._from_float = fn("bf16_from_float", C.c_uint16, [C.c_float])
         else:
+            self._prepare = fn("prepare", _vp, [_vp, _u64, _vp, _vp, _u64, _vp, _u64, _int, _u32, _u64])
+            self._dec_prepared = fn("decompress_prepared", _int, [_vp, _vp])
+            self._free_prepared = fn("free_prepared", None, [_vp])
             self._entropy = fn("entropy_report", None, [_vp, _u64, _vp])
             self._nzt = fn("write_nzt_lossless", _i64, [_vp, _vp, _int, _vp, _u64])
 
@@ -250,6 +253,34 @@ class Oracle:
         return int(self._from_float(f))
 
     # ref-only helpers
+    def prepared(self, freqs, stream: bytes, mant, n: int, k: int = 7, scales=None, block: int = 0):
+        """A reference Blob built once; .decode(out) times decompress_* alone."""
+        lib = self
+        buf = np.frombuffer(stream, np.uint8).copy()
+        f = np.ascontiguousarray(freqs, dtype=np.uint16)
+        m = np.ascontiguousarray(mant, dtype=np.uint8)
+        sc = np.ascontiguousarray(scales if scales is not None else np.zeros(1, np.uint8), dtype=np.uint8)
+        h = self._prepare(_p(buf), buf.size, _p(f), _p(m), m.size, _p(sc), sc.size if scales is not None else 0,
+                          k, block, n)
+        if not h:
+            raise OracleError(INVALID, "prepare")
+
+        class Prepared:
+            def __init__(self):
+                self.h, self.n = h, n
+                self.out = np.zeros(max(n, 1), np.uint16)
+
+            def decode(self):
+                rc = lib._dec_prepared(self.h, _p(self.out))
+                if rc:
+                    raise OracleError(rc, "decompress")
+                return self.out[: self.n]
+
+            def __del__(self):
+                lib._free_prepared(self.h)
+
+        return Prepared()
+
     def entropy_report(self, values):
         v = np.ascontiguousarray(values, dtype=np.uint16)
         out = np.zeros(5, np.float64)

@@ -170,6 +170,37 @@ int ref_decompress_lossless(const std::uint8_t* stream, std::uint64_t stream_len
     GUARD_END
 }
 
+// Prepared blobs: parse once, then time decompress_lossless / decompress_lossy
+// alone (tensorstore.hpp:112-125, :215-238) -- the CPU baseline measures the
+// reference's decode, not this shim's marshalling.
+void* ref_prepare(const std::uint8_t* stream, std::uint64_t stream_len, const std::uint16_t* freqs,
+                  const std::uint8_t* mant, std::uint64_t mant_len, const std::uint8_t* scales,
+                  std::uint64_t scales_len, int k, std::uint32_t block, std::uint64_t n) {
+    try {
+        if (k == kLosslessPrecision) {
+            return new Blob(LosslessBlob{TensorMeta{{n}}, parse_stream(stream, stream_len, freqs),
+                                         std::vector<std::uint8_t>(mant, mant + mant_len)});
+        }
+        return new Blob(LossyBlob{TensorMeta{{n}}, k, block, std::vector<std::uint8_t>(scales, scales + scales_len),
+                                  parse_stream(stream, stream_len, freqs),
+                                  std::vector<std::uint8_t>(mant, mant + mant_len)});
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+int ref_decompress_prepared(void* h, std::uint16_t* out) {
+    GUARD_BEGIN
+    const Blob& b = *static_cast<Blob*>(h);
+    const std::vector<Bf16> back = std::holds_alternative<LosslessBlob>(b) ? decompress_lossless(std::get<LosslessBlob>(b))
+                                                                          : decompress_lossy(std::get<LossyBlob>(b));
+    std::memcpy(out, back.data(), back.size() * 2);
+    return kOk;
+    GUARD_END
+}
+
+void ref_free_prepared(void* h) { delete static_cast<Blob*>(h); }
+
 std::int64_t ref_compress_lossy(const std::uint16_t* values, std::uint64_t n, int k, std::uint32_t block,
                                 std::uint64_t chunk, std::uint16_t* freqs, std::uint8_t* scales,
                                 std::uint8_t* stream, std::uint8_t* packed) {

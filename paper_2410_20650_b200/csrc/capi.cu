@@ -184,6 +184,8 @@ struct nzgpu_blob_s {
         d.single_symbol = single_symbol;
         d.precision = precision;
         d.block_size = block ? block : 1;
+        const uint32_t spc = interval ? chunk_syms / interval : 0;
+        d.log2_spc = (spc && !(spc & (spc - 1))) ? (uint32_t)__builtin_ctz(spc) : 0xFFFFFFFFu;
         return d;
     }
     uint64_t tiles() const { return decode_tiles_for(nsub); }
@@ -323,6 +325,7 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
         const uint32_t s0 = info.empty() ? kDefaultChunk : info[0].w;
         interval = s0 % NZGPU_DEFAULT_INTERVAL == 0 ? NZGPU_DEFAULT_INTERVAL : 64;
     }
+    if (ceil_div(t->n, interval) >= 0xFFFFFFFFull) return NZGPU_INVALID_ARGUMENT;  // 32-bit sub-range ids
     b->n = t->n;
     b->precision = t->precision;
     b->block = t->precision == 7 ? 0 : t->block_size;
@@ -406,6 +409,7 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
     }
     const int log2k = log2_of(interval);
     if (log2k < 0 || (!irregular && chunk_syms % interval)) return NZGPU_INVALID_ARGUMENT;
+    if (ceil_div(n, interval) >= 0xFFFFFFFFull) return NZGPU_INVALID_ARGUMENT;  // 32-bit sub-range ids
     b->n = n;
     b->precision = precision;
     b->block = precision == 7 ? 0 : block;

@@ -24,21 +24,36 @@ __host__ __device__ constexpr uint32_t decode_smem_bytes(int log2k, uint32_t win
 
 __device__ __forceinline__ uint64_t chunk_offset(uint4 ci) { return (uint64_t)ci.x | ((uint64_t)ci.y << 32); }
 
+// Sub-range j -> (chunk, index within chunk).  Sub-range indices are 32-bit
+// (the host rejects tensors with >= 2^32 sub-ranges); S/K is usually a
+// power of two (65536/128), which turns the division into shifts.
+__device__ __forceinline__ void sub_to_chunk(const DecodeDesc& d, int log2k, uint32_t j, uint32_t& ch, uint32_t& jin) {
+    if (d.log2_spc != 0xFFFFFFFFu) {
+        ch = j >> d.log2_spc;
+        jin = j & ((1u << d.log2_spc) - 1u);
+    } else {
+        const uint32_t spc = d.chunk_syms >> log2k;
+        ch = j / spc;
+        jin = j - ch * spc;
+    }
+}
+
 // Absolute stream window [a, b) of renormalisation bytes a tile reads.
-__device__ __forceinline__ void tile_window(const DecodeDesc& d, uint64_t sub0, uint32_t tile_subs, int log2k,
-                                            uint64_t nsub, uint64_t& a, uint64_t& b) {
-    const uint64_t spc = d.chunk_syms >> log2k;
-    const uint64_t c0 = sub0 / spc;
+__device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, uint32_t tile_subs, int log2k,
+                                            uint32_t nsub, uint64_t& a, uint64_t& b) {
+    uint32_t c0, j0in, c1, jlin;
+    sub_to_chunk(d, log2k, sub0, c0, j0in);
     const uint4 ci0 = d.chunk_info[c0];
-    const uint64_t lim0 = ci0.z >= 4 ? ci0.z - 4 : 0;
-    const uint64_t e0 = (sub0 % spc == 0) ? lim0 : min((uint64_t)d.ckpt[sub0].y, lim0);
+    const uint32_t lim0 = ci0.z >= 4 ? ci0.z - 4 : 0;
+    const uint32_t e0 = j0in == 0 ? lim0 : min(d.ckpt[sub0].y, lim0);
     a = chunk_offset(ci0) + lim0 - e0;
-    const uint64_t jl = sub0 + tile_subs - 1;
-    const uint64_t c1 = jl / spc;
+    const uint32_t jl = sub0 + tile_subs - 1;
+    sub_to_chunk(d, log2k, jl, c1, jlin);
     const uint4 ci1 = d.chunk_info[c1];
-    const uint64_t lim1 = ci1.z >= 4 ? ci1.z - 4 : 0;
-    const uint64_t jn = jl + 1;
-    const uint64_t e1 = (jn < nsub && jn % spc != 0) ? min((uint64_t)d.ckpt[jn].y, lim1) : 0;
+    const uint32_t lim1 = ci1.z >= 4 ? ci1.z - 4 : 0;
+    const uint32_t jn = jl + 1;
+    const bool chunk_end = ((uint64_t)(jlin + 1) << log2k) >= ci1.w;
+    const uint32_t e1 = (jn < nsub && !chunk_end) ? min(d.ckpt[jn].y, lim1) : 0;
     b = chunk_offset(ci1) + lim1 - e1;
     if (b < a) b = a;
 }

@@ -9,18 +9,18 @@
 //
 //   1. thread 0 arms an mbarrier and issues TMA bulk copies (cp.async.bulk,
 //      SASS UBLKCP) of the tensor's 16 KiB packed decode LUT and of the tile's
-//      contiguous payload window, plus an L2 bulk prefetch of the tile's
-//      sign/mantissa bytes;
+//      contiguous payload window; meanwhile every thread issues its 128-bit
+//      loads of the tile's sign/mantissa plane into registers, so they are in
+//      flight during the whole decode;
 //   2. every thread runs kChains independent ANS lanes interleaved for ILP,
 //      entirely out of shared memory: LUT lookup, state transition, a
-//      predicated one-byte renormalisation and a rarely taken second byte.
+//      predicated one-byte renormalisation and a predicated second byte.
 //      Four exponents are packed per 32-bit word into a padded
 //      (bank-conflict-free) exponent tile.  Every lane must land exactly on
 //      the next checkpoint -- the reference's end-of-chunk desync check
 //      (ans.hpp:252) applied to every sub-range;
 //   3. the CTA merges exponents with the sign/mantissa plane in 16-element
-//      groups: 128-bit coalesced loads, PRMT/LOP3 bit assembly, two 128-bit
-//      streaming stores per group.
+//      groups: PRMT/LOP3 bit assembly, two 128-bit streaming stores per group.
 //
 // Byte format, ratio and every output bit are the reference's.
 #include "decode_common.cuh"
@@ -36,6 +36,26 @@ template <int LOG2K>
 __host__ __device__ constexpr uint32_t win_off() {
     return kExpOff + kTileSubs * exps_row_words(LOG2K) * 4;
 }
+
+// Sign/mantissa bytes of one 16-element group: lossless 16 B, lossy 2(k+1) B.
+template <int P>
+struct GroupBits;
+template <>
+struct GroupBits<7> {
+    using T = uint4;
+};
+template <>
+struct GroupBits<3> {
+    using T = uint2;
+};
+template <>
+struct GroupBits<1> {
+    using T = uint32_t;
+};
+template <>
+struct GroupBits<0> {
+    using T = unsigned short;
+};
 
 }  // namespace
 
@@ -56,8 +76,9 @@ __device__ __forceinline__ uint32_t lds8(uint32_t addr) {
 // packed LUT, `p` the shared address of the next payload byte and `b` that
 // byte (prefetched).  With v = f<<20 | (slot-cum)<<8 | sym:
 //   f*(x>>12) + slot - cum  ==  f*((x>>12) - 4096) + (v>>8)   (mod 2^32),
-// which saves the bias mask.  One renormalisation byte is predicated; the
-// second (only possible when f < 16) is predicated too.
+// which saves the bias mask (the >>12 and -4096 fuse into one LEA.HI).  The
+// first renormalisation byte is predicated; the second (only possible when
+// f < 16) is predicated too, so the warp never diverges.
 #define NZ_DECODE_STEP(lut, x, p, b, v)                                                      \
     do {                                                                                     \
         uint32_t a_;                                                                         \
@@ -92,6 +113,9 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     constexpr int K = 1 << LOG2K;
     constexpr uint32_t RW = exps_row_words(LOG2K);
     constexpr uint32_t kWinOff = win_off<LOG2K>();
+    constexpr int G = TS * K / 16 / T;          // 16-element merge groups per thread
+    constexpr int PF = G < 8 ? G : 8;           // groups prefetched into registers
+    using GB = typename GroupBits<P>::T;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint32_t* exps_s = reinterpret_cast<uint32_t*>(smem + kExpOff);
@@ -100,7 +124,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     const uint32_t lut = sbase + kLutOff;
 
     // Locate the tensor of this tile (plans group many tensors per launch).
-    uint64_t tile = blockIdx.x;
+    uint32_t tile = blockIdx.x;
     const DecodeDesc* dp = &one;
     if (descs) {
         int lo = 0, hi = ndesc - 1;
@@ -109,14 +133,15 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
             if (__ldg(tile_prefix + mid) <= tile) lo = mid; else hi = mid - 1;
         }
         dp = descs + lo;
-        tile -= __ldg(tile_prefix + lo);
+        tile -= (uint32_t)__ldg(tile_prefix + lo);
     }
     const DecodeDesc d = *dp;
-    const uint64_t nsub = ceil_div(d.n, K);
-    const uint64_t sub0 = tile * TS;
-    const uint32_t tile_subs = (uint32_t)min((uint64_t)TS, nsub - sub0);
-    const uint64_t sym0 = sub0 << LOG2K;
+    const uint32_t nsub = (uint32_t)ceil_div(d.n, K);
+    const uint32_t sub0 = tile * TS;
+    const uint32_t tile_subs = min((uint32_t)TS, nsub - sub0);
+    const uint64_t sym0 = (uint64_t)sub0 << LOG2K;
     const uint32_t tile_syms = (uint32_t)min((uint64_t)TS * K, d.n - sym0);
+    const uint32_t groups = tile_syms >> 4;
     const bool single = d.flags & kFlagSingleSymbol;
 
     if (tid == 0) {
@@ -137,11 +162,18 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
             bulk_g2s(smem + kLutOff, d.lut, kLutBytes, bar);
             if (bytes) bulk_g2s(smem + kWinOff, d.stream + wa, (uint32_t)bytes, bar);
         }
-        // Sign/mantissa bytes of the tile: warm L2 while the ANS lanes run.
-        const uint64_t mb = ((uint64_t)tile_syms * (P + 1) / 8) & ~15ull;
-        if (mb) prefetch_l2(d.mant + (sym0 * (P + 1) / 8), (uint32_t)mb);
         *reinterpret_cast<uint64_t*>(smem + 16) = wa;
         *reinterpret_cast<uint32_t*>(smem + 24) = st;
+    }
+
+    // Sign/mantissa plane of this tile: issue the loads now, use them after
+    // the decode (group g = tid + i*T, coalesced across the CTA).
+    const GB* gbits = reinterpret_cast<const GB*>(d.mant + sym0 * (P + 1) / 8);
+    GB pre[PF];
+#pragma unroll
+    for (int i = 0; i < PF; ++i) {
+        const uint32_t g = tid + i * T;
+        if (g < groups) pre[i] = __ldcs(gbits + g);
     }
     __syncthreads();
 
@@ -156,35 +188,35 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
         x[c] = xe[c] = kStateLow;
         p[c] = pe[c] = sbase + kWinOff;
         if (r < tile_subs) {
-            const uint64_t spc = d.chunk_syms >> LOG2K;
-            const uint64_t j = sub0 + r;
-            const uint64_t ch = j / spc;
-            const uint64_t jin = j - ch * spc;
+            const uint32_t j = sub0 + r;
+            uint32_t ch, jin;
+            sub_to_chunk(d, LOG2K, j, ch, jin);
             const uint4 ci = d.chunk_info[ch];
             const uint64_t off = chunk_offset(ci);
             const uint32_t len = ci.z, nsym = ci.w;
-            const uint32_t sym_in = (uint32_t)(jin << LOG2K);
+            const uint32_t sym_in = jin << LOG2K;
             cnt[c] = nsym > sym_in ? min((uint32_t)K, nsym - sym_in) : 0u;
+            if (len < 4) errs |= kErrTruncated;  // ans.hpp:231-233
+            const uint32_t limit = len >= 4 ? len - 4 : 0;
             if (jin == 0) {
-                // The chunk's framing must agree with the index (ans.hpp:332-340).
+                // The chunk's framing must agree with the index (ans.hpp:332-340),
+                // and the chunk's first lane starts from the stream's own final
+                // state (ans.hpp:235-236), not from the index.
                 if (ld_u32le_bytes(d.stream + off - 8) != nsym || ld_u32le_bytes(d.stream + off - 4) != len)
                     errs |= kErrLength;
+                x[c] = ld_u32le_bytes(d.stream + off + limit);
             }
-            if (len < 4) errs |= kErrTruncated;  // ans.hpp:231-233
             if (single) {
                 // A one-symbol table keeps the state at 2^23 and consumes no
                 // bytes: every chunk payload must be exactly LE32(2^23).
-                if (jin == 0 && len >= 4) {
-                    const uint32_t x0 = ld_u32le_bytes(d.stream + off + len - 4);
-                    if (x0 != kStateLow || len != 4) errs |= x0 < kStateLow ? kErrTruncated : kErrDesync;
-                }
+                if (jin == 0 && len >= 4 && (x[c] != kStateLow || len != 4))
+                    errs |= x[c] < kStateLow ? kErrTruncated : kErrDesync;
             } else {
-                const uint32_t limit = len >= 4 ? len - 4 : 0;
                 const uint2 rec = d.ckpt[j];
                 const bool last = sym_in + K >= nsym;
                 const uint2 end = last ? make_uint2(kStateLow, 0u) : d.ckpt[j + 1];
                 const uint32_t e_start = jin == 0 ? limit : rec.y;
-                x[c] = jin == 0 ? ld_u32le_bytes(d.stream + off + limit) : rec.x;
+                if (jin != 0) x[c] = rec.x;
                 xe[c] = end.x;
                 const int64_t p0 = (int64_t)(off + limit - e_start) - (int64_t)wa;
                 const int64_t p1 = (int64_t)(off + limit - min(end.y, limit)) - (int64_t)wa;
@@ -254,47 +286,36 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     __syncthreads();
 
     // ---- merge: exponents (smem) + sign/mantissa plane -> bf16 ---------------
-    const uint32_t groups = tile_syms >> 4;
     uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
-    if constexpr (P == 7) {
-        const uint4* sm4 = reinterpret_cast<const uint4*>(d.mant + sym0);
-        for (uint32_t g = tid; g < groups; g += T) {
-            const uint32_t e = g << 4;
-            const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
-            const uint4 s = __ldcs(sm4 + g);
-            const uint32_t e0 = er[0], e1 = er[1], e2 = er[2], e3 = er[3];
+    const uint32_t B = d.block_size;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const uint32_t g = tid + i * T;
+        if (g >= groups) break;
+        const GB s = i < PF ? pre[i < PF ? i : 0] : __ldcs(gbits + g);
+        const uint32_t e = g << 4;
+        const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
+        const uint32_t e0 = er[0], e1 = er[1], e2 = er[2], e3 = er[3];
+        if constexpr (P == 7) {
             __stcs(out + 2 * g, merge8(e0, s.x, e1, s.y));
             __stcs(out + 2 * g + 1, merge8(e2, s.z, e3, s.w));
-        }
-        for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
-            const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
-            const uint32_t sm = __ldg(d.mant + sym0 + i);
-            d.out[sym0 + i] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
-        }
-    } else {
-        constexpr uint32_t W = P + 1;
-        const uint8_t* packed = d.mant + sym0 * W / 8;
-        const uint32_t B = d.block_size;
-        for (uint32_t g = tid; g < groups; g += T) {
-            const uint32_t e = g << 4;
-            const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
-            // 16 items = 2W bytes, MSB-first: gather big-endian into the top bits.
+        } else {
+            constexpr uint32_t W = P + 1;
+            // 16 items of W bits, MSB-first: gather big-endian into the top bits.
             uint64_t bits;
             if constexpr (W == 4) {
-                const uint2 v = __ldcs(reinterpret_cast<const uint2*>(packed) + g);
-                bits = ((uint64_t)__byte_perm(v.x, 0, 0x0123) << 32) | __byte_perm(v.y, 0, 0x0123);
+                bits = ((uint64_t)__byte_perm(s.x, 0, 0x0123) << 32) | __byte_perm(s.y, 0, 0x0123);
             } else if constexpr (W == 2) {
-                bits = (uint64_t)__byte_perm(__ldcs(reinterpret_cast<const uint32_t*>(packed) + g), 0, 0x0123) << 32;
+                bits = (uint64_t)__byte_perm(s, 0, 0x0123) << 32;
             } else {
-                bits = (uint64_t)__byte_perm(__ldcs(reinterpret_cast<const unsigned short*>(packed) + g), 0, 0x0144)
-                       << 32;
+                bits = (uint64_t)__byte_perm((uint32_t)s, 0, 0x0144) << 32;
             }
             const uint64_t gi = sym0 + e;
             const uint64_t b0 = gi / B;
             const float c0 = scale_coef(__ldg(d.scales + b0));
             const uint32_t split = (uint32_t)min((uint64_t)16, (b0 + 1) * B - gi);
             const float c1 = split < 16 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
-            const uint32_t ew[4] = {er[0], er[1], er[2], er[3]};
+            const uint32_t ew[4] = {e0, e1, e2, e3};
             uint32_t res[8];
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -308,11 +329,16 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
             __stcs(out + 2 * g, make_uint4(res[0], res[1], res[2], res[3]));
             __stcs(out + 2 * g + 1, make_uint4(res[4], res[5], res[6], res[7]));
         }
-        for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
-            const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
-            const uint64_t gi = sym0 + i;
-            const uint32_t item = packed_item(d.mant, gi, P);
-            d.out[gi] = lossy_rebuild(item, ex, P, scale_coef(__ldg(d.scales + gi / B)));
+    }
+    // Tail of the tensor (n % 16 elements).
+    for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
+        const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
+        const uint64_t gi = sym0 + i;
+        if constexpr (P == 7) {
+            const uint32_t sm = __ldg(d.mant + gi);
+            d.out[gi] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
+        } else {
+            d.out[gi] = lossy_rebuild(packed_item(d.mant, gi, P), ex, P, scale_coef(__ldg(d.scales + gi / B)));
         }
     }
 }
@@ -320,12 +346,12 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
 // Largest payload window any tile of a tensor needs (sizes dynamic smem).
 template <int LOG2K>
 __global__ void window_max_kernel(DecodeDesc d, uint32_t* __restrict__ out) {
-    const uint64_t nsub = ceil_div(d.n, 1u << LOG2K);
-    const uint64_t tiles = ceil_div(nsub, kTileSubs);
+    const uint32_t nsub = (uint32_t)ceil_div(d.n, 1u << LOG2K);
+    const uint32_t tiles = (uint32_t)ceil_div(nsub, kTileSubs);
     uint32_t best = 0;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < tiles; t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t sub0 = t * kTileSubs;
-        const uint32_t subs = (uint32_t)min((uint64_t)kTileSubs, nsub - sub0);
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gridDim.x * blockDim.x) {
+        const uint32_t sub0 = t * kTileSubs;
+        const uint32_t subs = min((uint32_t)kTileSubs, nsub - sub0);
         uint64_t a, b;
         tile_window(d, sub0, subs, LOG2K, nsub, a, b);
         const uint64_t bytes = ((b + 15) & ~15ull) - (a & ~15ull);

@@ -68,7 +68,7 @@ struct DecodeDesc {
     uint32_t single_symbol;       // the exponent when kFlagSingleSymbol
     int32_t precision;            // 7 lossless, 0/1/3 lossy
     uint32_t block_size;          // lossy block size B
-    uint32_t pad;
+    uint32_t log2_spc;            // log2(S/K) when S/K is a power of two, else 0xFFFFFFFF
 };
 
 // ------------------------------------------------------------------ PTX --
