@@ -50,7 +50,7 @@ typedef enum nzgpu_status {
 #define NZGPU_LOSSLESS 7            /* kLosslessPrecision, tensorstore.hpp:36 */
 #define NZGPU_DEFAULT_BLOCK 512     /* kDefaultBlockSize, tensorstore.hpp:35  */
 #define NZGPU_DEFAULT_CHUNK 65536   /* ans::kChunkSymbols, ans.hpp:33         */
-#define NZGPU_DEFAULT_INTERVAL 128  /* checkpoint stride K (symbols)          */
+#define NZGPU_DEFAULT_INTERVAL 64   /* checkpoint stride K (symbols)          */
 
 typedef struct nzgpu_blob_s* nzgpu_blob; /* device-resident compressed tensor */
 typedef struct nzgpu_plan_s* nzgpu_plan; /* grouped decode of several blobs   */
@@ -106,7 +106,7 @@ const char* nzgpu_last_error_message(void);
 /* ---- device tier: device pointers, stream-ordered ---------------------- */
 /* Compress n bf16 values resident on the device (compress_lossless,
  * tensorstore.hpp:87-106, precision 7; compress_lossy, :141-208, k in
- * {0,1,3}).  chunk_symbols S (0 = 65536) and interval K (0 = 128, a power of
+ * {0,1,3}).  chunk_symbols S (0 = 65536) and interval K (0 = 64, a power of
  * two in {64,128,256} dividing S).  Synchronises `stream` once (to size the
  * exact stream allocation).  d_values must be 16-byte aligned. */
 int nzgpu_compress(const uint16_t* d_values, uint64_t n, int precision, uint32_t block_size,
@@ -128,7 +128,7 @@ int nzgpu_blob_export(nzgpu_blob blob, uint16_t* freqs, uint8_t* stream, uint8_t
  * validating framing and table (deserialize_table / deserialize_stream,
  * ans.hpp:120-130, :318-347) and building the checkpoint index on the GPU
  * when t->index is absent (full sequential validation, ans.hpp:229-256).
- * interval 0 = 128. */
+ * interval 0 = auto (64). */
 int nzgpu_blob_import(const nzgpu_host_tensor* t, uint32_t interval, void* cuda_stream, nzgpu_blob* out);
 
 /* Grouped decode: one kernel launch decodes all blobs (e.g. one transformer

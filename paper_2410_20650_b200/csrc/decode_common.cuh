@@ -3,12 +3,16 @@
 #include "nzgpu_internal.cuh"
 
 #ifndef NZ_CHAINS
-#define NZ_CHAINS 2
+#define NZ_CHAINS 1
 #endif
 
 namespace nzgpu {
 
-constexpr int kDecodeThreads = 128;       // threads per decode CTA
+#ifndef NZ_THREADS
+#define NZ_THREADS 256
+#endif
+
+constexpr int kDecodeThreads = NZ_THREADS;  // threads per decode CTA
 constexpr int kChains = NZ_CHAINS;        // interleaved sub-ranges (ANS lanes) per thread
 constexpr int kTileSubs = kDecodeThreads * kChains;
 constexpr uint32_t kLutBytes = 4096 * 4;
@@ -58,20 +62,20 @@ __device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, 
     if (b < a) b = a;
 }
 
-// Two bf16 from two exponent bytes and two sign/mantissa bytes packed as
-// Y = e<<8 | s<<7 | m per 16-bit lane  ->  s<<15 | e<<7 | m
-// (merge, bitfloat.hpp:64-71, on the tensorstore.hpp:119-123 fields).
-__device__ __forceinline__ uint32_t assemble2(uint32_t y) {
-    return ((y >> 1) & 0x7F807F80u) | (y & 0x007F007Fu) | ((y << 8) & 0x80008000u);
+// Four bf16 from four exponent bytes E and four sign/mantissa bytes S
+// (merge, bitfloat.hpp:64-71, on the tensorstore.hpp:119-123 fields):
+// bf16 = s<<15 | e<<7 | m has high byte s<<7 | e>>1 and low byte
+// (e&1)<<7 | m, so build all four high bytes and all four low bytes with
+// one shift + one LOP3 each, then interleave them with two PRMTs.
+__device__ __forceinline__ uint2 merge4(uint32_t e4, uint32_t s4) {
+    const uint32_t hi = ((e4 >> 1) & 0x7F7F7F7Fu) | (s4 & 0x80808080u);
+    const uint32_t lo = ((e4 << 7) & 0x80808080u) | (s4 & 0x7F7F7F7Fu);
+    return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
 }
 
 __device__ __forceinline__ uint4 merge8(uint32_t e4a, uint32_t s4a, uint32_t e4b, uint32_t s4b) {
-    uint4 o;
-    o.x = assemble2(__byte_perm(s4a, e4a, 0x5140));
-    o.y = assemble2(__byte_perm(s4a, e4a, 0x7362));
-    o.z = assemble2(__byte_perm(s4b, e4b, 0x5140));
-    o.w = assemble2(__byte_perm(s4b, e4b, 0x7362));
-    return o;
+    const uint2 a = merge4(e4a, s4a), b = merge4(e4b, s4b);
+    return make_uint4(a.x, a.y, b.x, b.y);
 }
 
 // decompress_lossy element (tensorstore.hpp:229-236) in exact FP32

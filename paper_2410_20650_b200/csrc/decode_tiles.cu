@@ -37,24 +37,24 @@ __host__ __device__ constexpr uint32_t win_off() {
     return kExpOff + kTileSubs * exps_row_words(LOG2K) * 4;
 }
 
-// Sign/mantissa bytes of one 16-element group: lossless 16 B, lossy 2(k+1) B.
+// Sign/mantissa bytes of one 8-element group: lossless 8 B, lossy (k+1) B.
 template <int P>
 struct GroupBits;
 template <>
 struct GroupBits<7> {
-    using T = uint4;
-};
-template <>
-struct GroupBits<3> {
     using T = uint2;
 };
 template <>
-struct GroupBits<1> {
+struct GroupBits<3> {
     using T = uint32_t;
 };
 template <>
-struct GroupBits<0> {
+struct GroupBits<1> {
     using T = unsigned short;
+};
+template <>
+struct GroupBits<0> {
+    using T = unsigned char;
 };
 
 }  // namespace
@@ -74,11 +74,14 @@ __device__ __forceinline__ uint32_t lds8(uint32_t addr) {
 
 // One decode step (ans.hpp:240-251).  `lut` is the shared address of the
 // packed LUT, `p` the shared address of the next payload byte and `b` that
-// byte (prefetched).  With v = f<<20 | (slot-cum)<<8 | sym:
+// byte, loaded one step ahead.  With v = f<<20 | (slot-cum)<<8 | sym:
 //   f*(x>>12) + slot - cum  ==  f*((x>>12) - 4096) + (v>>8)   (mod 2^32),
-// which saves the bias mask (the >>12 and -4096 fuse into one LEA.HI).  The
-// first renormalisation byte is predicated; the second (only possible when
-// f < 16) is predicated too, so the warp never diverges.
+// which saves the bias mask (the >>12 and -4096 fuse into one LEA.HI).
+// Renormalisation is predicated, never divergent, and the byte reload is
+// predicated on consumption: only the ~1/3 of lanes that consumed a byte
+// touch shared memory, which cuts the bank-conflict wavefronts of the
+// (random-address) byte loads -- shared-memory wavefronts, not issue slots,
+// bound this loop (ncu: L1 data pipe 94% busy).
 #define NZ_DECODE_STEP(lut, x, p, b, v)                                                      \
     do {                                                                                     \
         uint32_t a_;                                                                         \
@@ -89,12 +92,8 @@ __device__ __forceinline__ uint32_t lds8(uint32_t addr) {
             "{\n\t.reg .pred q;\n\t"                                                         \
             "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
             "@q mad.lo.u32 %0, %0, 256, %2;\n\t"                                             \
-            "@q add.u32 %1, %1, 1;\n\t}"                                                     \
-            : "+r"(x), "+r"(p)                                                               \
-            : "r"(b));                                                                       \
-        b = lds8(p);                                                                         \
-        asm volatile(                                                                        \
-            "{\n\t.reg .pred q;\n\t"                                                         \
+            "@q add.u32 %1, %1, 1;\n\t"                                                      \
+            "@q ld.shared.u8 %2, [%1];\n\t"                                                  \
             "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
             "@q mad.lo.u32 %0, %0, 256, %2;\n\t"                                             \
             "@q add.u32 %1, %1, 1;\n\t"                                                      \
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     constexpr int K = 1 << LOG2K;
     constexpr uint32_t RW = exps_row_words(LOG2K);
     constexpr uint32_t kWinOff = win_off<LOG2K>();
-    constexpr int G = TS * K / 16 / T;          // 16-element merge groups per thread
+    constexpr int G = TS * K / 8 / T;           // 8-element merge groups per thread
     constexpr int PF = G < 8 ? G : 8;           // groups prefetched into registers
     using GB = typename GroupBits<P>::T;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -141,7 +140,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     const uint32_t tile_subs = min((uint32_t)TS, nsub - sub0);
     const uint64_t sym0 = (uint64_t)sub0 << LOG2K;
     const uint32_t tile_syms = (uint32_t)min((uint64_t)TS * K, d.n - sym0);
-    const uint32_t groups = tile_syms >> 4;
+    const uint32_t groups = tile_syms >> 3;
     const bool single = d.flags & kFlagSingleSymbol;
 
     if (tid == 0) {
@@ -290,48 +289,46 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     const uint32_t B = d.block_size;
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-        const uint32_t g = tid + i * T;
+        const uint32_t g = tid + i * T;  // 8-element group: one 16-byte store per lane, coalesced
         if (g >= groups) break;
         const GB s = i < PF ? pre[i < PF ? i : 0] : __ldcs(gbits + g);
-        const uint32_t e = g << 4;
+        const uint32_t e = g << 3;
         const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
-        const uint32_t e0 = er[0], e1 = er[1], e2 = er[2], e3 = er[3];
+        const uint32_t e0 = er[0], e1 = er[1];
         if constexpr (P == 7) {
-            __stcs(out + 2 * g, merge8(e0, s.x, e1, s.y));
-            __stcs(out + 2 * g + 1, merge8(e2, s.z, e3, s.w));
+            __stcs(out + g, merge8(e0, s.x, e1, s.y));
         } else {
             constexpr uint32_t W = P + 1;
-            // 16 items of W bits, MSB-first: gather big-endian into the top bits.
-            uint64_t bits;
+            // 8 items of W bits, MSB-first: gather big-endian into the top bits.
+            uint32_t bits;
             if constexpr (W == 4) {
-                bits = ((uint64_t)__byte_perm(s.x, 0, 0x0123) << 32) | __byte_perm(s.y, 0, 0x0123);
+                bits = __byte_perm(s, 0, 0x0123);
             } else if constexpr (W == 2) {
-                bits = (uint64_t)__byte_perm(s, 0, 0x0123) << 32;
+                bits = __byte_perm((uint32_t)s, 0, 0x0144) ;
             } else {
-                bits = (uint64_t)__byte_perm((uint32_t)s, 0, 0x0144) << 32;
+                bits = (uint32_t)s << 24;
             }
             const uint64_t gi = sym0 + e;
             const uint64_t b0 = gi / B;
             const float c0 = scale_coef(__ldg(d.scales + b0));
-            const uint32_t split = (uint32_t)min((uint64_t)16, (b0 + 1) * B - gi);
-            const float c1 = split < 16 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
-            const uint32_t ew[4] = {e0, e1, e2, e3};
-            uint32_t res[8];
+            const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gi);
+            const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+            const uint32_t ew[2] = {e0, e1};
+            uint32_t res[4];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
+            for (int q = 0; q < 8; ++q) {
                 const uint32_t ex = (ew[q >> 2] >> (8 * (q & 3))) & 0xFFu;
-                const uint32_t item = (uint32_t)(bits >> (64 - (q + 1) * W)) & ((1u << W) - 1u);
+                const uint32_t item = (bits >> (32 - (q + 1) * W)) & ((1u << W) - 1u);
                 float c = q < (int)split ? c0 : c1;
-                if (B < 16 && q >= (int)split) c = scale_coef(__ldg(d.scales + (gi + q) / B));
+                if (B < 8 && q >= (int)split) c = scale_coef(__ldg(d.scales + (gi + q) / B));
                 const uint32_t h = lossy_rebuild(item, ex, P, c);
                 if (q & 1) res[q >> 1] |= h << 16; else res[q >> 1] = h;
             }
-            __stcs(out + 2 * g, make_uint4(res[0], res[1], res[2], res[3]));
-            __stcs(out + 2 * g + 1, make_uint4(res[4], res[5], res[6], res[7]));
+            __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
         }
     }
-    // Tail of the tensor (n % 16 elements).
-    for (uint32_t i = groups * 16 + tid; i < tile_syms; i += T) {
+    // Tail of the tensor (n % 8 elements).
+    for (uint32_t i = groups * 8 + tid; i < tile_syms; i += T) {
         const uint32_t ex = (exps_s[(i >> LOG2K) * RW + ((i & (K - 1)) >> 2)] >> (8 * (i & 3))) & 0xFFu;
         const uint64_t gi = sym0 + i;
         if constexpr (P == 7) {

@@ -19,7 +19,7 @@ NONFINITE, FORMAT_TABLE, CUDA_ERROR, OUT_OF_MEMORY, NO_DEVICE = 5, 6, 7, 8, 9
 LOSSLESS = 7
 DEFAULT_BLOCK = 512
 DEFAULT_CHUNK = 65536
-DEFAULT_INTERVAL = 128
+DEFAULT_INTERVAL = 64
 
 
 # --- exception taxonomy of the reference (errors.hpp:9-32) ----------------
