@@ -8,6 +8,10 @@
 
 namespace nzgpu {
 
+#ifndef NZ_WINDOW
+#define NZ_WINDOW 1  // renormalisation bytes from a per-lane register window
+#endif
+
 #ifndef NZ_THREADS
 #define NZ_THREADS 256
 #endif
