@@ -4,7 +4,7 @@
  * The reference (arxiv 2410.20650, /root/reference/proj/include/neuzip/) is a
  * header-only C++20 library with no FFI; its public surface is the C++ API in
  * tensorstore.hpp / ans.hpp / bitfloat.hpp.  This header is the thin C layer
- * that the drop-in C++ headers (include/neuzip/*.hpp) and any foreign binding
+ * that the drop-in C++ headers (include/neuzip/ *.hpp) and any foreign binding
  * (ctypes, cgo, JNI -- see INTEGRATION.md) call.  Plain pointers and sizes
  * only; no exceptions cross it; every function returns an nzgpu_status.
  *
@@ -172,6 +172,11 @@ int nzgpu_ans_decode_host(const uint8_t* stream, uint64_t stream_len, const uint
  * :229-236) for every (value, scale) pair: out[i] = round trip of v[i] under
  * scale byte s[i]; the exhaustive parity check of the lossy arithmetic. */
 int nzgpu_lossy_roundtrip_host(const uint16_t* values, const uint8_t* scales, uint64_t n, int k, uint16_t* out);
+/* pack_signed_mantissas / unpack_signed_mantissas (bitfloat.hpp:124-164) on
+ * the device: items are (sign << k) | mantissa, one byte each, k in
+ * {0,1,3,7}; packed holds ceil(n(k+1)/8) MSB-first bytes. */
+int nzgpu_pack_host(const uint8_t* items, uint64_t n, int k, uint8_t* packed);
+int nzgpu_unpack_host(const uint8_t* packed, uint64_t nbytes, int k, uint64_t n, uint8_t* items);
 
 #ifdef __cplusplus
 }

@@ -34,7 +34,9 @@ from .codec import (  # noqa: F401
     kDefaultBlockSize,
     kLosslessPrecision,
     lossy_roundtrip,
+    pack_signed_mantissas,
     ratio,
+    unpack_signed_mantissas,
 )
 
 LIB_PATH = nzgpu.LIB_PATH

@@ -388,6 +388,29 @@ def ans_decode(stream: bytes, freqs, n: int) -> np.ndarray:
     return out[:n]
 
 
+def pack_signed_mantissas(signs, mants, k: int) -> np.ndarray:
+    """bitfloat.hpp:124-143 on the GPU: (k+1)-bit items, MSB-first."""
+    if k not in (0, 1, 3, 7):
+        raise ValueError("pack: k must be one of {0,1,3,7}")
+    s = np.ascontiguousarray(signs, dtype=np.uint8).reshape(-1)
+    m = np.ascontiguousarray(mants, dtype=np.uint8).reshape(-1)
+    items = ((s.astype(np.uint32) << k) | m).astype(np.uint8) if s.size else np.zeros(0, np.uint8)
+    if s.size and ((s > 1).any() or (m >= (1 << k)).any()):
+        raise ValueError("pack: item exceeds k+1 bits")
+    out = np.zeros(max((s.size * (k + 1) + 7) // 8, 1), np.uint8)
+    N.check(N.lib.nzgpu_pack_host(_ptr(items), s.size, k, _ptr(out)), "pack_signed_mantissas")
+    return out[: (s.size * (k + 1) + 7) // 8]
+
+
+def unpack_signed_mantissas(packed, k: int, n: int):
+    """bitfloat.hpp:145-164 on the GPU -> (signs, mantissas)."""
+    p = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+    items = np.zeros(max(n, 1), np.uint8)
+    N.check(N.lib.nzgpu_unpack_host(_ptr(p), p.size, k, n, _ptr(items)), "unpack_signed_mantissas")
+    items = items[:n]
+    return items >> k, items & ((1 << k) - 1)
+
+
 def lossy_roundtrip(values, scales, k: int) -> np.ndarray:
     """Element-wise lossy round trip under explicit scale bytes (exhaustive
     parity harness for tensorstore.hpp:179-198 + :229-236)."""

@@ -32,6 +32,7 @@ __global__ void lossy_normalize_kernel(const uint16_t*, uint64_t, int, uint32_t,
                                        uint32_t*);
 __global__ void pack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*, uint64_t);
 __global__ void lossy_roundtrip_kernel(const uint16_t*, const uint8_t*, uint64_t, int, uint16_t*);
+__global__ void unpack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*);
 __global__ void seq_decode_kernel(const uint8_t*, const uint4*, const uint64_t*, uint32_t, uint64_t, const uint32_t*,
                                   uint32_t, uint32_t, uint2*, uint8_t*, uint32_t*);
 __global__ void merge_plane_kernel(const uint8_t*, const uint8_t*, const uint8_t*, uint64_t, int, uint32_t,
@@ -901,6 +902,43 @@ int nzgpu_ans_decode_host(const uint8_t* stream, uint64_t stream_len, const uint
     cudaFreeAsync(dout, sg.s);
     cudaStreamSynchronize(sg.s);
     return rc;
+}
+
+int nzgpu_pack_host(const uint8_t* items, uint64_t n, int k, uint8_t* out) {
+    if (k != 0 && k != 1 && k != 3 && k != 7) return NZGPU_INVALID_ARGUMENT;  // bitfloat.hpp:126-128
+    if (n && (!items || !out)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    if (n == 0) return NZGPU_OK;
+    for (uint64_t i = 0; i < n; ++i)  // bitfloat.hpp:134-136: items must fit k+1 bits
+        if (items[i] >> (k + 1)) return NZGPU_INVALID_ARGUMENT;
+    const uint64_t nbytes = mant_bytes(n, k);
+    StreamGuard sg{StreamGuard::Own{}};
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n + nbytes + 32, sg.s));
+    CK(cudaMemcpyAsync(tmp, items, n, cudaMemcpyHostToDevice, sg.s));
+    pack_items_kernel<<<grid_for(nbytes, 256), 256, 0, sg.s>>>(tmp, n, k, tmp + align_up(n, 16), nbytes);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp + align_up(n, 16), nbytes, cudaMemcpyDeviceToHost, sg.s));
+    CK(cudaFreeAsync(tmp, sg.s));
+    CK(cudaStreamSynchronize(sg.s));
+    return NZGPU_OK;
+}
+
+int nzgpu_unpack_host(const uint8_t* packed, uint64_t nbytes, int k, uint64_t n, uint8_t* items) {
+    if (k != 0 && k != 1 && k != 3 && k != 7) return NZGPU_INVALID_ARGUMENT;  // bitfloat.hpp:147-149
+    if (nbytes != mant_bytes(n, k)) return NZGPU_INVALID_ARGUMENT;             // bitfloat.hpp:151-153
+    if (int rc = device_ready()) return rc;
+    if (n == 0) return NZGPU_OK;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint8_t* tmp = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n + nbytes + 32, sg.s));
+    CK(cudaMemcpyAsync(tmp, packed, nbytes, cudaMemcpyHostToDevice, sg.s));
+    unpack_items_kernel<<<grid_for(n, 256), 256, 0, sg.s>>>(tmp, n, k, tmp + align_up(nbytes, 16));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(items, tmp + align_up(nbytes, 16), n, cudaMemcpyDeviceToHost, sg.s));
+    CK(cudaFreeAsync(tmp, sg.s));
+    CK(cudaStreamSynchronize(sg.s));
+    return NZGPU_OK;
 }
 
 int nzgpu_lossy_roundtrip_host(const uint16_t* values, const uint8_t* scales, uint64_t n, int k, uint16_t* out) {

@@ -102,6 +102,16 @@ __global__ void pack_items_kernel(const uint8_t* __restrict__ items, uint64_t n,
     }
 }
 
+// unpack_signed_mantissas (bitfloat.hpp:145-164): one thread per item.
+__global__ void unpack_items_kernel(const uint8_t* __restrict__ packed, uint64_t n, int k, uint8_t* __restrict__ items) {
+    const uint32_t w = (uint32_t)k + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bit = i * w;
+        const uint32_t shift = 8 - w - (uint32_t)(bit & 7);
+        items[i] = (uint8_t)((packed[bit >> 3] >> shift) & ((1u << w) - 1u));
+    }
+}
+
 // Elementwise lossy round trip under an explicit scale byte (the exhaustive
 // parity harness; mirrors oracles.hpp:129-153 / tensorstore.hpp:179-198, 229-236).
 __global__ void lossy_roundtrip_kernel(const uint16_t* __restrict__ v, const uint8_t* __restrict__ sc, uint64_t n,

@@ -134,6 +134,8 @@ SIGNATURES = {
     "nzgpu_ans_encode_host": (_i, [_vp, _u64, _vp, _u32, _vp, _u64, _p(_u64)]),
     "nzgpu_ans_decode_host": (_i, [_vp, _u64, _vp, _vp, _u64]),
     "nzgpu_lossy_roundtrip_host": (_i, [_vp, _vp, _u64, _i, _vp]),
+    "nzgpu_pack_host": (_i, [_vp, _u64, _i, _vp]),
+    "nzgpu_unpack_host": (_i, [_vp, _u64, _i, _u64, _vp]),
 }
 
 

@@ -1,0 +1,214 @@
+// Acceptance-style test of the drop-in C++ API (include/neuzip/*.hpp) in the
+// spirit of the reference's own suites (proj/tests/test_bitfloat.cpp,
+// test_ans.cpp, test_tensorstore.cpp, acceptance.cpp): same calls, same
+// expected values and exception types, run against the B200 implementation.
+// Exits 0 when every check passes.  Built and run by tests/test_cpp_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+
+#include "neuzip/neuzip.hpp"
+
+using namespace neuzip;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        if (cond) {                                                            \
+            ++g_pass;                                                          \
+        } else {                                                               \
+            ++g_fail;                                                          \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);        \
+        }                                                                      \
+    } while (0)
+
+template <class E>
+static bool throws(const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// rng.hpp-style counter generator (splitmix64 + Box-Muller), test inputs only.
+static std::uint64_t mix64(std::uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static std::vector<Bf16> gaussian(std::uint64_t seed, std::size_t n, double sigma) {
+    std::vector<Bf16> v(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const double u1 = (static_cast<double>(mix64(seed + (2 * i + 1) * 0x9E3779B97F4A7C15ull) >> 11) + 1.0) * 0x1.0p-53;
+        const double u2 = static_cast<double>(mix64(seed + (2 * i + 2) * 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53;
+        v[i] = Bf16::from_float(static_cast<float>(sigma * std::sqrt(-2.0 * std::log(u1)) *
+                                                   std::cos(2.0 * 3.141592653589793238462643383279502884 * u2)));
+    }
+    return v;
+}
+
+static std::vector<std::uint64_t> counts_of(const std::vector<std::uint8_t>& xs) {
+    std::vector<std::uint64_t> c(256, 0);
+    for (auto s : xs) ++c[s];
+    return c;
+}
+
+int main() {
+    // --- bitfloat (test_bitfloat.cpp) ------------------------------------
+    {
+        int bad = 0;
+        for (std::uint32_t b = 0; b < 65536; ++b) {
+            const Bf16 x{static_cast<std::uint16_t>(b)};
+            if (merge(split(x)) != x) ++bad;
+        }
+        CHECK(bad == 0);
+        CHECK((split(Bf16{0x3F80}) == ComponentTriple{0, 127, 0}));
+        CHECK(Bf16::from_float(-5.0f).bits == 0xC0A0);
+        CHECK((split(Bf16{0xC0A0}) == ComponentTriple{1, 129, 32}));
+        CHECK(throws<std::invalid_argument>([] { (void)merge({2, 0, 0}); }));
+        CHECK(round_mantissa(0b1010110, 3).mantissa == 0b1010000);
+        CHECK(round_mantissa(127, 3).carry);
+        CHECK(throws<std::invalid_argument>([] { (void)round_mantissa(0, 2); }));
+        CHECK(Bf16::from_float(1.00390625f).bits == 0x3F80);
+        const std::vector<SignedMantissa> s8 = {{1, 0}, {0, 0}, {1, 0}, {0, 0}, {1, 0}, {0, 0}, {1, 0}, {0, 0}};
+        CHECK(pack_signed_mantissas(s8, 0) == std::vector<std::uint8_t>{0xAA});
+        const std::vector<SignedMantissa> s2 = {{0, 0b101}, {1, 0b001}};
+        CHECK(pack_signed_mantissas(s2, 3) == std::vector<std::uint8_t>{0x59});
+        CHECK(unpack_signed_mantissas(pack_signed_mantissas(s2, 3), 3, 2) == s2);
+        CHECK(throws<std::invalid_argument>([] { (void)pack_signed_mantissas(std::vector<SignedMantissa>{{0, 2}}, 1); }));
+        CHECK(throws<std::invalid_argument>([] { (void)unpack_signed_mantissas({}, 3, 5); }));
+    }
+    // --- ans (test_ans.cpp) ----------------------------------------------
+    {
+        std::vector<std::uint64_t> c(256, 0);
+        c[42] = 4096;
+        CHECK(build_table(c).freq(42) == 4096);
+        CHECK(build_table(std::vector<std::uint64_t>(256, 1000)).freq(7) == 16);
+        c.assign(256, 0);
+        c[0] = 3;
+        c[1] = 1;
+        CHECK(build_table(c).freq(0) == 3072 && build_table(c).freq(1) == 1024);
+        CHECK(throws<std::invalid_argument>([] { (void)build_table(std::vector<std::uint64_t>(256, 0)); }));
+        c.assign(256, 0);
+        c[0] = 4095;
+        c[1] = 1;
+        const auto tb = serialize_table(build_table(c));
+        CHECK(tb[0] == 0xFF && tb[1] == 0x0F && tb[2] == 0x01 && tb[3] == 0x00);
+        std::vector<std::uint8_t> bad(512, 0);
+        bad[0] = 1;
+        CHECK(throws<FormatError>([&] { (void)deserialize_table(bad); }));
+
+        std::mt19937_64 gen(8);
+        std::vector<double> w(256);
+        for (int s = 0; s < 256; ++s) w[s] = 1.0 / (1.0 + s);
+        std::discrete_distribution<int> zipf(w.begin(), w.end());
+        for (std::size_t n : {std::size_t{0}, std::size_t{1}, std::size_t{999}, std::size_t{65536}, std::size_t{65537},
+                              std::size_t{200000}}) {
+            std::vector<std::uint8_t> xs(n);
+            for (auto& x : xs) x = static_cast<std::uint8_t>(zipf(gen));
+            auto cnt = counts_of(xs);
+            if (n == 0) cnt[0] = 1;
+            const FrequencyTable t = build_table(cnt);
+            const AnsStream s = ans_encode(xs, t);
+            CHECK(s.chunks.size() == (n + 65535) / 65536);
+            CHECK(ans_decode(s) == xs);
+            const auto bytes = serialize_stream(s);
+            CHECK(bytes.size() == s.stream_bytes());
+            CHECK(deserialize_stream(bytes, t).chunks == s.chunks);
+            if (s.chunks.size() > 1) {
+                const auto mid = ans_decode_chunk(s.chunks[1], t);
+                CHECK(std::equal(mid.begin(), mid.end(), xs.begin() + 65536));
+                CHECK(ans_encode_chunk(std::span(xs).subspan(65536, 65536), t) == s.chunks[1]);
+            }
+        }
+        // errors (test_ans.cpp:231-257)
+        c.assign(256, 0);
+        c[1] = 10;
+        const FrequencyTable one = build_table(c);
+        CHECK(throws<std::invalid_argument>([&] { (void)ans_encode(std::vector<std::uint8_t>{1, 2, 1}, one); }));
+        std::vector<std::uint8_t> xs(5000);
+        for (auto& x : xs) x = static_cast<std::uint8_t>(gen());
+        const FrequencyTable t = build_table(counts_of(xs));
+        AnsStream s = ans_encode(xs, t);
+        s.chunks[0].payload.back() ^= 0x01;
+        CHECK(throws<FormatError>([&] { (void)ans_decode(s); }));
+        AnsStream tr = ans_encode(xs, t);
+        tr.chunks[0].payload.resize(tr.chunks[0].payload.size() - 5);
+        CHECK(throws<FormatError>([&] { (void)ans_decode(tr); }));
+        const auto framed = serialize_stream(ans_encode(xs, t));
+        auto trailing = framed;
+        trailing.push_back(0);
+        CHECK(throws<FormatError>([&] { (void)deserialize_stream(trailing, t); }));
+    }
+    // --- tensorstore (test_tensorstore.cpp, acceptance.cpp) -----------------
+    {
+        std::vector<Bf16> all(65536);
+        for (std::uint32_t b = 0; b < 65536; ++b) all[b] = Bf16{static_cast<std::uint16_t>(b)};
+        CHECK(decompress_lossless(compress_lossless(all)) == all);
+
+        const std::vector<Bf16> ones(16, Bf16{0x3F80});
+        const LosslessBlob c16 = compress_lossless(ones, TensorMeta{{16}});
+        CHECK(serialize_stream(c16.exp_stream) ==
+              (std::vector<std::uint8_t>{1, 0, 0, 0, 16, 0, 0, 0, 4, 0, 0, 0, 0, 0, 0x80, 0}));
+        CHECK(footprint(c16).total() == 587);  // the golden const16_k7.nzt size
+        CHECK(decompress_lossless(c16) == ones);
+
+        const auto g = gaussian(42, 4096 * 4096, 0.02);
+        const LosslessBlob big = compress_lossless(g, TensorMeta{{4096, 4096}});
+        CHECK(big.exp_stream.stream_bytes() == 5347963);
+        CHECK(std::fabs(2.0 * g.size() / footprint(big).total() - 1.5165336) < 1e-6);
+        CHECK(!big.gpu_index.empty());
+        CHECK(decompress_lossless(big) == g);
+        LosslessBlob no_index = big;  // as if the stream came from the reference
+        no_index.gpu_index.clear();
+        CHECK(decompress_lossless(no_index) == g);
+
+        LosslessBlob bad_meta = compress_lossless(std::span(g).first(1000));
+        bad_meta.meta.shape = {999};
+        CHECK(throws<FormatError>([&] { (void)decompress_lossless(bad_meta); }));
+        LosslessBlob corrupt = compress_lossless(std::span(g).first(1000));
+        corrupt.exp_stream.chunks[0].payload.back() ^= 0x10;
+        CHECK(throws<FormatError>([&] { (void)decompress_lossless(corrupt); }));
+
+        // lossy (test_tensorstore.cpp:104-215)
+        const std::vector<Bf16> two = {Bf16::from_float(1.0f), Bf16::from_float(0.5f)};
+        for (int k : {0, 1, 3}) {
+            const LossyBlob b = compress_lossy(two, k, 512);
+            CHECK(b.scales == std::vector<std::uint8_t>{0});
+            CHECK(decompress_lossy(b) == two);
+        }
+        const std::vector<Bf16> m = {Bf16::from_float(-1.75f), Bf16::from_float(0.3f)};
+        const LossyBlob lb = compress_lossy(m, 0, 512);
+        CHECK(lb.scales == std::vector<std::uint8_t>{96});
+        CHECK(decompress_lossy(lb)[0] == m[0]);
+        const auto sample = gaussian(7, 100000, 0.02);
+        for (int k : {0, 1, 3}) {
+            const LossyBlob b = compress_lossy(sample, k, 512);
+            const auto back = decompress_lossy(b);
+            double worst = 0;
+            for (std::size_t i = 0; i < sample.size(); ++i) {
+                if (split(sample[i]).exponent == 0) continue;
+                worst = std::max(worst, std::fabs(back[i].to_double() - sample[i].to_double()) /
+                                            std::fabs(sample[i].to_double()));
+            }
+            CHECK(worst <= std::pow(2.0, -k) + std::pow(2.0, -7));
+        }
+        CHECK(decompress_lossy(compress_lossy(std::span(sample).first(1000), 3, 1)) ==
+              std::vector<Bf16>(sample.begin(), sample.begin() + 1000));
+        CHECK(throws<NonFiniteError>([] { (void)compress_lossy(std::vector<Bf16>{Bf16{0x3F80}, Bf16{0x7FC1}}, 3, 512); }));
+        CHECK(throws<std::invalid_argument>([] { (void)compress_lossy(std::vector<Bf16>{Bf16{0x3F80}}, 2, 512); }));
+        CHECK(throws<std::invalid_argument>([] { (void)compress_lossy(std::vector<Bf16>{Bf16{0x3F80}}, 3, 0); }));
+        CHECK(throws<std::invalid_argument>([] { (void)compress_lossless(std::vector<Bf16>{}); }));
+    }
+    std::printf("dropin_test: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}

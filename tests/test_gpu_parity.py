@@ -133,6 +133,24 @@ def test_gpu_lossy_decodes_reference_produced_blobs(nz, port):
         assert (nz.decompress_lossy(blob) == port.decompress_lossy(f, sc, st, pk, k, B, v.size)).all()
 
 
+def test_gpu_pack_unpack_matches_oracle(nz, port):  # test_bitfloat.cpp:103-173
+    assert nz.pack_signed_mantissas([1, 0, 1, 0, 1, 0, 1, 0], [0] * 8, 0).tolist() == [0xAA]
+    assert nz.pack_signed_mantissas([0, 1], [0b101, 0b001], 3).tolist() == [0x59]
+    w = inputs.words(19, 2 * 100003)
+    for k in (0, 1, 3, 7):
+        for n in (1, 3, 17, 100, 257, 100003):
+            s = (w[:n] & np.uint64(1)).astype(np.uint8)
+            m = ((w[n:2 * n] >> np.uint64(5)) & np.uint64((1 << k) - 1)).astype(np.uint8)
+            packed = nz.pack_signed_mantissas(s, m, k)
+            assert (packed == port.pack(s, m, k)).all()
+            s2, m2 = nz.unpack_signed_mantissas(packed, k, n)
+            assert (s2 == s).all() and (m2 == m).all()
+    with pytest.raises(ValueError):
+        nz.pack_signed_mantissas([0], [2], 1)
+    with pytest.raises(ValueError):
+        nz.unpack_signed_mantissas(np.zeros(0, np.uint8), 3, 5)
+
+
 # ----------------------------------------------------------- errors --------
 def test_gpu_error_contract(nz, port):
     # test_tensorstore.cpp:313-322: meta/stream mismatch and corrupt byte
