@@ -42,6 +42,7 @@ cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int
 cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
 uint32_t decode_smem_for(int log2k, uint32_t win_cap);
 uint64_t decode_tiles_for(uint64_t nsub);
+uint64_t decode_tile_subs();
 }  // namespace nzgpu
 
 using namespace nzgpu;
@@ -164,7 +165,10 @@ struct nzgpu_blob_s {
     uint8_t* stream = nullptr;
     uint64_t stream_len = 0;
 
+    bool owns = true;  // false: a descriptor over buffers owned by a host-pipeline slot
+
     ~nzgpu_blob_s() {
+        if (!owns) return;
         if (base) cudaFree(base);
         if (stream) cudaFree(stream);
     }
@@ -715,29 +719,152 @@ int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint3
 }
 
 namespace {
-struct HostCtx {
-    cudaStream_t s[2] = {nullptr, nullptr};
-    uint16_t* out[2] = {nullptr, nullptr};
-    uint64_t out_cap[2] = {0, 0};
-    ~HostCtx() {
-        for (int i = 0; i < 2; ++i) {
-            if (out[i]) cudaFree(out[i]);
-            if (s[i]) cudaStreamDestroy(s[i]);
-        }
+
+// Grow-only device buffer owned by a host-pipeline slot.
+struct DevBuf {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    int ensure(uint64_t bytes, cudaStream_t s) {
+        if (cap >= bytes) return NZGPU_OK;
+        CK(cudaStreamSynchronize(s));  // the previous tensor of this slot may still use it
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const uint64_t want = align_up(bytes + bytes / 4, 1 << 20);
+        CK(cudaMalloc(&p, want));
+        cap = want;
+        return NZGPU_OK;
     }
-    int ensure(int i, uint64_t bytes) {
-        if (!s[i]) CK(cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking));
-        if (out_cap[i] < bytes) {
-            if (out[i]) cudaFree(out[i]);
-            out[i] = nullptr;
-            out_cap[i] = 0;
-            CK(cudaMalloc(&out[i], bytes));
-            out_cap[i] = bytes;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// One of two pipeline slots: tensor i runs on slot i%2 (own stream), so the
+// H2D of tensor i+1, the decode of tensor i and the D2H of tensor i-1
+// overlap; buffers persist across calls (no per-call cudaMalloc).
+struct HostSlot {
+    cudaStream_t s = nullptr;
+    DevBuf main, stream, out;
+    uint32_t* err = nullptr;
+    ~HostSlot() {
+        if (err) cudaFree(err);
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+struct HostCtx {
+    HostSlot slot[2];
+    int init() {
+        for (HostSlot& sl : slot) {
+            if (!sl.s) CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+            if (!sl.err) CK(cudaMalloc(&sl.err, 64));
         }
         return NZGPU_OK;
     }
 };
 thread_local std::unique_ptr<HostCtx> g_host;
+
+// Host replica of tile_window() over the host copy of the index: the decode
+// kernel's shared-memory window size without a device round trip.
+uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint64_t nsub, uint32_t S, int log2k) {
+    const uint64_t spc = S >> log2k, ts = decode_tile_subs();
+    uint64_t best = 0;
+    for (uint64_t sub0 = 0; sub0 < nsub; sub0 += ts) {
+        const uint64_t subs = std::min<uint64_t>(ts, nsub - sub0);
+        const uint4 c0 = info[sub0 / spc];
+        const uint64_t lim0 = c0.z >= 4 ? c0.z - 4 : 0;
+        const uint64_t e0 = sub0 % spc == 0 ? lim0 : std::min<uint64_t>(ckpt[sub0].y, lim0);
+        const uint64_t a = ((uint64_t)c0.x | ((uint64_t)c0.y << 32)) + lim0 - e0;
+        const uint64_t jl = sub0 + subs - 1;
+        const uint4 c1 = info[jl / spc];
+        const uint64_t lim1 = c1.z >= 4 ? c1.z - 4 : 0;
+        const bool chunk_end = (((jl % spc) + 1) << log2k) >= c1.w;
+        const uint64_t e1 = (jl + 1 < nsub && !chunk_end) ? std::min<uint64_t>(ckpt[jl + 1].y, lim1) : 0;
+        uint64_t b = ((uint64_t)c1.x | ((uint64_t)c1.y << 32)) + lim1 - e1;
+        if (b < a) b = a;
+        best = std::max<uint64_t>(best, align_up(b, 16) - (a & ~(uint64_t)15));
+    }
+    return (uint32_t)std::min<uint64_t>(best, 0xFFFFFFFFu);
+}
+
+// Stage + decode one host tensor on a slot without any host synchronisation
+// (uniform framing and a valid side index).  Returns 1 when the caller must
+// take the general (synchronising) path instead.
+int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_out) {
+    if (!t || !valid_precision(t->precision) || !t->freqs || !t->index) return 1;
+    std::vector<uint4> info;
+    uint64_t total = 0;
+    if (walk_stream(t->stream, t->stream_len, info, total) || info.empty() || total != t->n) return 1;
+    uint32_t sum = 0, single = 0xFFFFFFFFu;
+    for (int i = 0; i < 256; ++i) {
+        sum += t->freqs[i];
+        if (t->freqs[i] == kProbScale) single = (uint32_t)i;
+    }
+    if (sum != kProbScale || t->mantissa_len != mant_bytes(t->n, t->precision)) return 1;
+    if (t->precision != 7 && (t->block_size == 0 || t->scales_len != ceil_div(t->n, t->block_size))) return 1;
+    IndexHeader h;
+    if (t->index_len < sizeof(h)) return 1;
+    std::memcpy(&h, t->index, sizeof(h));
+    const uint32_t S = info[0].w;
+    const int log2k = log2_of(h.interval);
+    if (h.magic != kIndexMagic || h.version != kIndexVersion || log2k < 0 || h.chunk_syms != S || h.n != t->n ||
+        h.nchunks != info.size() || h.stream_len != t->stream_len || S % h.interval ||
+        h.nsub != ceil_div(t->n, h.interval) || t->index_len != sizeof(h) + h.nsub * sizeof(uint2))
+        return 1;
+    for (size_t c = 0; c < info.size(); ++c)
+        if (c + 1 < info.size() ? info[c].w != S : (info[c].w == 0 || info[c].w > S)) return 1;
+    const uint2* ck = reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(t->index) + sizeof(h));
+
+    nzgpu_blob_s& b = *new (std::nothrow) nzgpu_blob_s;  // descriptor only; buffers belong to the slot
+    std::unique_ptr<nzgpu_blob_s> guard(&b);
+    b.owns = false;
+    b.n = t->n;
+    b.precision = t->precision;
+    b.block = t->precision == 7 ? 0 : t->block_size;
+    b.interval = h.interval;
+    b.log2k = log2k;
+    b.chunk_syms = S;
+    b.nchunks = info.size();
+    b.nsub = h.nsub;
+    b.mant_len = t->mantissa_len;
+    b.scales_len = t->precision == 7 ? 0 : t->scales_len;
+    b.stream_len = t->stream_len;
+    b.flags = single != 0xFFFFFFFFu ? kFlagSingleSymbol : 0u;
+    b.single_symbol = single != 0xFFFFFFFFu ? single : 0u;
+    Carve cv;
+    const uint64_t o_freqs = cv.take(512), o_lut = cv.take(16384), o_mant = cv.take(b.mant_len + 16);
+    const uint64_t o_scales = cv.take(std::max<uint64_t>(b.scales_len, 1));
+    const uint64_t o_info = cv.take(info.size() * sizeof(uint4));
+    const uint64_t o_ckpt = cv.take(b.nsub * sizeof(uint2) + 16), o_scr = cv.take(64);
+    cudaStream_t s = sl.s;
+    if (int rc = sl.main.ensure(cv.size, s)) return rc;
+    if (int rc = sl.stream.ensure(align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32, s)) return rc;
+    if (int rc = sl.out.ensure(align_up(t->n * 2, 16) + 16, s)) return rc;
+    uint8_t* m = static_cast<uint8_t*>(sl.main.p);
+    b.freqs = reinterpret_cast<uint16_t*>(m + o_freqs);
+    b.lut = reinterpret_cast<uint32_t*>(m + o_lut);
+    b.mant = m + o_mant;
+    b.scales = m + o_scales;
+    b.chunk_info = reinterpret_cast<uint4*>(m + o_info);
+    b.ckpt = reinterpret_cast<uint2*>(m + o_ckpt);
+    b.scratch_u32 = reinterpret_cast<uint32_t*>(m + o_scr);
+    b.stream = static_cast<uint8_t*>(sl.stream.p);
+    b.err = sl.err;
+    CK(cudaMemcpyAsync(b.freqs, t->freqs, 512, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
+    if (b.mant_len) CK(cudaMemcpyAsync(b.mant, t->mantissas, b.mant_len, cudaMemcpyHostToDevice, s));
+    if (b.scales_len) CK(cudaMemcpyAsync(b.scales, t->scales, b.scales_len, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.chunk_info, info.data(), info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.ckpt, ck, b.nsub * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
+    CK(cudaGetLastError());
+    b.max_window = (b.flags & kFlagSingleSymbol) ? 0 : host_max_window(info, ck, b.nsub, S, log2k);
+    if (int rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), s)) return rc;
+    if (t->n) CK(cudaMemcpyAsync(host_out, sl.out.p, t->n * 2, cudaMemcpyDeviceToHost, s));
+    return NZGPU_OK;
+}
+
 }  // namespace
 
 int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t* const* outs) {
@@ -745,19 +872,39 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
     if (int rc = device_ready()) return rc;
     if (!g_host) g_host.reset(new HostCtx);
     HostCtx& h = *g_host;
-    std::unique_ptr<nzgpu_blob_s> blobs[2];
+    if (int rc = h.init()) return rc;
+    for (HostSlot& sl : h.slot) CK(cudaMemsetAsync(sl.err, 0, 64, sl.s));
     for (int i = 0; i < count; ++i) {
-        const int slot = i & 1;
+        HostSlot& sl = h.slot[i & 1];
         const nzgpu_host_tensor* t = ts + i;
-        if (int rc = h.ensure(slot, align_up(t->n * 2, 16) + 16)) return rc;
-        cudaStream_t s = h.s[slot];
-        blobs[slot].reset(new nzgpu_blob_s);  // frees the blob from i-2 (its stream work is done)
-        if (int rc = import_into(blobs[slot].get(), t, 0, s)) return rc;
-        if (int rc = decode_blob(blobs[slot].get(), h.out[slot], s)) return rc;
-        if (t->n) CK(cudaMemcpyAsync(outs[i], h.out[slot], t->n * 2, cudaMemcpyDeviceToHost, s));
-        if (int rc = sync_status(s, blobs[slot]->err, true)) return rc;
+        int rc = stage_and_decode(sl, t, outs[i]);
+        if (rc == 1) {
+            // General path (no/foreign index, irregular framing, or a format
+            // error to report exactly): import with full validation.
+            nzgpu_blob_s b;
+            rc = import_into(&b, t, 0, sl.s);
+            if (!rc && (rc = sl.out.ensure(align_up(t->n * 2, 16) + 16, sl.s)) == 0) {
+                rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), sl.s);
+                if (!rc && t->n) {
+                    const cudaError_t e = cudaMemcpyAsync(outs[i], sl.out.p, t->n * 2, cudaMemcpyDeviceToHost, sl.s);
+                    if (e != cudaSuccess) rc = fail_cuda(e, "cudaMemcpyAsync");
+                }
+                if (!rc) rc = sync_status(sl.s, b.err, true);
+            }
+            if (!rc) CK(cudaStreamSynchronize(sl.s));  // b's buffers die here
+        }
+        if (rc) {
+            cudaStreamSynchronize(h.slot[0].s);
+            cudaStreamSynchronize(h.slot[1].s);
+            return rc;
+        }
     }
-    return NZGPU_OK;
+    int rc = NZGPU_OK;
+    for (HostSlot& sl : h.slot) {
+        const int r = sync_status(sl.s, sl.err, true);
+        if (!rc) rc = r;
+    }
+    return rc;
 }
 
 int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out) { return nzgpu_decompress_host_batch(t, 1, &out); }

@@ -490,6 +490,7 @@ uint32_t decode_smem_for(int log2k, uint32_t win_cap) {
 }
 
 uint64_t decode_tiles_for(uint64_t nsub) { return ceil_div(nsub, kTileSubs); }
+uint64_t decode_tile_subs() { return kTileSubs; }
 
 cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s) {
     switch (log2k) {
