@@ -248,7 +248,9 @@ def run_gpu(args):
         with open(tp) as fh:
             tj = json.load(fh)
         if tj.get("precision") == args.precision:
-            traffic = tj.get("dram_bytes_per_algo_byte")
+            # ncu DRAM bytes (read + write) per launch, over the same launch
+            # time as `achieved`: directly comparable with it.
+            traffic = round(achieved * float(tj["dram_bytes_per_algo_byte"]), 2)
 
     # ---- e2e through the reference-facing host API (host buffers in/out)
     e2e = run_e2e(args, nz, blobs, torch) if rank == 0 else None
