@@ -12,6 +12,14 @@ namespace nzgpu {
 #define NZ_WINDOW 1  // renormalisation bytes from a per-lane register window
 #endif
 
+#ifndef NZ_MINBLOCKS
+#define NZ_MINBLOCKS 1
+#endif
+
+#ifndef NZ_PF
+#define NZ_PF 8  // 8-element groups of the mantissa plane prefetched into registers
+#endif
+
 #ifndef NZ_THREADS
 #define NZ_THREADS 256
 #endif

@@ -152,7 +152,7 @@ __device__ __forceinline__ uint32_t mbar_wait_token(uint64_t* bar, uint32_t pari
     } while (0)
 
 template <int LOG2K, int P>
-__global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const DecodeDesc* __restrict__ descs,
+__global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_kernel(const DecodeDesc* __restrict__ descs,
                                                                       int ndesc,
                                                                       const uint64_t* __restrict__ tile_prefix,
                                                                       DecodeDesc one, uint32_t win_cap) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kDecodeThreads) decode_tiles_kernel(const Deco
     constexpr uint32_t RW = exps_row_words(LOG2K);
     constexpr uint32_t kWinOff = win_off<LOG2K>();
     constexpr int G = TS * K / 8 / T;           // 8-element merge groups per thread
-    constexpr int PF = G < 8 ? G : 8;           // groups prefetched into registers
+    constexpr int PF = G < NZ_PF ? G : NZ_PF;   // groups prefetched into registers
     using GB = typename GroupBits<P>::T;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
