@@ -102,6 +102,10 @@ int nzgpu_version(void);                       /* 10000 * major + 100 * minor */
 int nzgpu_device_check(int* device_count);
 /* Last CUDA error text recorded by the library (thread-local). */
 const char* nzgpu_last_error_message(void);
+/* Decode schedule for plans/decompress created afterwards: 0 = persistent
+ * warp-pipelined kernel (default), 1 = one tile per CTA.  Both are
+ * bit-identical; this exists for A/B measurement. */
+int nzgpu_set_decode_kernel(int which);
 
 /* ---- device tier: device pointers, stream-ordered ---------------------- */
 /* Compress n bf16 values resident on the device (compress_lossless,

@@ -8,7 +8,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -43,7 +45,26 @@ cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cud
 uint32_t decode_smem_for(int log2k, uint32_t win_cap);
 uint64_t decode_tiles_for(uint64_t nsub);
 uint64_t decode_tile_subs();
+cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* descs, int ndesc,
+                                  const uint32_t* cta_prefix, const DecodeDesc& one, uint32_t ctas, uint32_t upc,
+                                  uint32_t win_cap, cudaStream_t s);
+uint32_t persist_resident_ctas(int log2k, uint32_t win_cap);
+bool persist_fits(int log2k, uint32_t win_cap);
+cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
 }  // namespace nzgpu
+
+namespace {
+// Decode schedule: the persistent warp-pipelined kernel (default) or the
+// one-tile-per-CTA kernel (NZGPU_KERNEL=tiles, or nzgpu_set_decode_kernel).
+int g_kernel = -1;  // -1: from the environment
+bool use_persist() {
+    if (g_kernel < 0) {
+        const char* e = std::getenv("NZGPU_KERNEL");
+        g_kernel = (e && std::string(e) == "tiles") ? 1 : 0;
+    }
+    return g_kernel == 0;
+}
+}  // namespace
 
 using namespace nzgpu;
 
@@ -146,7 +167,8 @@ struct nzgpu_blob_s {
     uint64_t nsub = 0;
     uint32_t flags = 0;
     uint32_t single_symbol = 0;
-    uint32_t max_window = 0;
+    uint32_t max_window = 0;       // per 256-sub-range tile (decode_tiles_kernel)
+    uint32_t max_window_unit = 0;  // per 32-sub-range warp unit (decode_persist_kernel)
     // main allocation
     void* base = nullptr;
     uint16_t* freqs = nullptr;
@@ -272,13 +294,31 @@ int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
 }
 
 int compute_window(nzgpu_blob_s* b, cudaStream_t s) {
-    b->max_window = 0;
+    b->max_window = b->max_window_unit = 0;
     if ((b->flags & kFlagIrregular) || b->nsub == 0 || (b->flags & kFlagSingleSymbol)) return NZGPU_OK;
-    CK(cudaMemsetAsync(b->scratch_u32 + 3, 0, 4, s));
+    CK(cudaMemsetAsync(b->scratch_u32 + 2, 0, 8, s));
     CK(launch_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 3, s));
-    CK(cudaMemcpyAsync(&b->max_window, b->scratch_u32 + 3, 4, cudaMemcpyDeviceToHost, s));
+    CK(launch_unit_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 2, s));
+    uint32_t w[2];
+    CK(cudaMemcpyAsync(w, b->scratch_u32 + 2, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    b->max_window_unit = w[0];
+    b->max_window = w[1];
     return NZGPU_OK;
+}
+
+// Persistent-kernel geometry: 32-sub-range units, `upc` units per CTA so
+// that the grid is about one resident wave.
+struct PersistGeom {
+    uint32_t ctas = 0, upc = 1;
+};
+PersistGeom persist_geom(uint64_t units, int log2k, uint32_t win_cap) {
+    PersistGeom g;
+    if (!units) return g;
+    const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(log2k, win_cap));
+    g.upc = (uint32_t)std::max<uint64_t>(1, ceil_div(units, resident));
+    g.ctas = (uint32_t)ceil_div(units, g.upc);
+    return g;
 }
 
 int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
@@ -297,7 +337,13 @@ int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
         CK(cudaFreeAsync(exps, s));
         return NZGPU_OK;
     }
-    CK(launch_decode(b->log2k, b->precision, nullptr, 0, nullptr, b->desc(d_out), b->tiles(), b->max_window, s));
+    if (use_persist() && persist_fits(b->log2k, b->max_window_unit)) {
+        const PersistGeom g = persist_geom(ceil_div(b->nsub, 32), b->log2k, b->max_window_unit);
+        CK(launch_decode_persist(b->log2k, b->precision, nullptr, 0, nullptr, b->desc(d_out), g.ctas, g.upc,
+                                 b->max_window_unit, s));
+    } else {
+        CK(launch_decode(b->log2k, b->precision, nullptr, 0, nullptr, b->desc(d_out), b->tiles(), b->max_window, s));
+    }
     return NZGPU_OK;
 }
 
@@ -513,10 +559,14 @@ struct nzgpu_plan_s {
     DecodeDesc* d_descs = nullptr;
     uint64_t* d_prefix = nullptr;
     uint32_t* d_err = nullptr;
+    // persistent schedule
+    uint32_t ctas = 0, upc = 1, win_cap_unit = 0;
+    uint32_t* d_cta_prefix = nullptr;
     ~nzgpu_plan_s() {
         if (d_descs) cudaFree(d_descs);
         if (d_prefix) cudaFree(d_prefix);
         if (d_err) cudaFree(d_err);
+        if (d_cta_prefix) cudaFree(d_cta_prefix);
     }
 };
 
@@ -540,6 +590,12 @@ const char* nzgpu_status_string(int status) {
 }
 
 int nzgpu_version(void) { return 100; }
+
+int nzgpu_set_decode_kernel(int which) {
+    if (which != 0 && which != 1) return NZGPU_INVALID_ARGUMENT;
+    g_kernel = which;
+    return NZGPU_OK;
+}
 
 const char* nzgpu_last_error_message(void) { return g_msg; }
 
@@ -664,14 +720,33 @@ int nzgpu_plan_create(const nzgpu_blob* blobs, uint16_t* const* d_outs, int coun
         prefix.push_back(tiles);
         tiles += b->tiles();
         p->win_cap = std::max(p->win_cap, b->max_window);
+        p->win_cap_unit = std::max(p->win_cap_unit, b->max_window_unit);
     }
     p->tiles = tiles;
     p->count = (int)descs.size();
+    // Persistent schedule: every CTA owns `upc` units of one tensor; the
+    // number of CTAs per tensor is proportional to its units (one wave).
+    std::vector<uint32_t> cta_prefix;
+    uint64_t units = 0;
+    for (const DecodeDesc& d : descs) units += ceil_div(ceil_div(d.n, 1ull << p->log2k), 32);
+    if (units) {
+        const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
+        p->upc = (uint32_t)std::max<uint64_t>(1, ceil_div(units, resident));
+        uint32_t ctas = 0;
+        for (const DecodeDesc& d : descs) {
+            cta_prefix.push_back(ctas);
+            ctas += (uint32_t)ceil_div(ceil_div(ceil_div(d.n, 1ull << p->log2k), 32), p->upc);
+        }
+        p->ctas = ctas;
+    }
     if (!descs.empty()) {
         CK(cudaMalloc(&p->d_descs, descs.size() * sizeof(DecodeDesc)));
         CK(cudaMalloc(&p->d_prefix, prefix.size() * sizeof(uint64_t)));
+        CK(cudaMalloc(&p->d_cta_prefix, cta_prefix.size() * sizeof(uint32_t)));
         CK(cudaMemcpy(p->d_descs, descs.data(), descs.size() * sizeof(DecodeDesc), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(p->d_prefix, prefix.data(), prefix.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_cta_prefix, cta_prefix.data(), cta_prefix.size() * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
     }
     *out = p.release();
     return NZGPU_OK;
@@ -681,8 +756,13 @@ int nzgpu_plan_launch(nzgpu_plan p, void* cuda_stream) {
     if (!p) return NZGPU_INVALID_ARGUMENT;
     if (!p->tiles) return NZGPU_OK;
     DecodeDesc none{};
-    CK(launch_decode(p->log2k, p->precision, p->d_descs, p->count, p->d_prefix, none, p->tiles, p->win_cap,
-                     static_cast<cudaStream_t>(cuda_stream)));
+    if (use_persist() && persist_fits(p->log2k, p->win_cap_unit)) {
+        CK(launch_decode_persist(p->log2k, p->precision, p->d_descs, p->count, p->d_cta_prefix, none, p->ctas, p->upc,
+                                 p->win_cap_unit, static_cast<cudaStream_t>(cuda_stream)));
+    } else {
+        CK(launch_decode(p->log2k, p->precision, p->d_descs, p->count, p->d_prefix, none, p->tiles, p->win_cap,
+                         static_cast<cudaStream_t>(cuda_stream)));
+    }
     return NZGPU_OK;
 }
 
@@ -767,8 +847,9 @@ thread_local std::unique_ptr<HostCtx> g_host;
 
 // Host replica of tile_window() over the host copy of the index: the decode
 // kernel's shared-memory window size without a device round trip.
-uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint64_t nsub, uint32_t S, int log2k) {
-    const uint64_t spc = S >> log2k, ts = decode_tile_subs();
+uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint64_t nsub, uint32_t S, int log2k,
+                         uint64_t ts) {
+    const uint64_t spc = S >> log2k;
     uint64_t best = 0;
     for (uint64_t sub0 = 0; sub0 < nsub; sub0 += ts) {
         const uint64_t subs = std::min<uint64_t>(ts, nsub - sub0);
@@ -859,7 +940,10 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     CK(cudaMemcpyAsync(b.ckpt, ck, b.nsub * sizeof(uint2), cudaMemcpyHostToDevice, s));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
-    b.max_window = (b.flags & kFlagSingleSymbol) ? 0 : host_max_window(info, ck, b.nsub, S, log2k);
+    if (!(b.flags & kFlagSingleSymbol)) {
+        b.max_window_unit = host_max_window(info, ck, b.nsub, S, log2k, 32);
+        b.max_window = host_max_window(info, ck, b.nsub, S, log2k, decode_tile_subs());
+    }
     if (int rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), s)) return rc;
     if (t->n) CK(cudaMemcpyAsync(host_out, sl.out.p, t->n * 2, cudaMemcpyDeviceToHost, s));
     return NZGPU_OK;

@@ -1,0 +1,486 @@
+// decode_persist.cu -- K5/K7, persistent warp-pipelined variant (default).
+//
+// Same contract and bit-exact output as decode_tiles.cu, different schedule:
+//
+//  * a CTA owns a contiguous range of work units of ONE tensor, so the
+//    16 KiB packed decode LUT is TMA-loaded once per CTA (not per tile);
+//  * a work unit is one warp's worth of sub-ranges: 32 lanes x K symbols;
+//    every warp runs its own pipeline with no CTA-wide barrier: while it
+//    decodes unit i from shared memory, the TMA bulk copy (UBLKCP, own
+//    mbarrier per buffer) of unit i+1's payload window is already in flight
+//    and the unit's sign/mantissa words are in registers;
+//  * each lane decodes one sub-range (ANS lane) from a register byte window,
+//    checks it lands on the next checkpoint (ans.hpp:252 applied per
+//    sub-range), writes exponents into the warp's padded smem tile, and the
+//    same warp then merges the unit with coalesced 16-byte stores -- so
+//    decode (ALU/shared) of some warps overlaps merge (HBM) of others.
+#include "decode_common.cuh"
+
+#ifndef NZ_PWARPS
+#define NZ_PWARPS 32  // warps per persistent CTA (one CTA per SM)
+#endif
+#ifndef NZ_PMINB
+#define NZ_PMINB 1  // resident CTAs per SM the register budget must allow
+#endif
+
+namespace nzgpu {
+
+namespace {
+
+constexpr int kPWarps = NZ_PWARPS;
+constexpr int kPThreads = kPWarps * 32;
+constexpr uint32_t kPHeader = 128 + 2 * 8 * kPWarps;  // LUT barrier + 2 mbarriers per warp
+
+__host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(log2k); }
+
+// Per-warp region: exponent tile (32 padded rows) + 2 payload windows.
+__host__ __device__ constexpr uint32_t warp_region(int log2k, uint32_t win_cap) {
+    return (unit_words(log2k) * 4 + 2 * (win_cap + 2 * (1u << log2k) + 64) + 127) & ~127u;
+}
+
+__host__ __device__ constexpr uint32_t persist_smem(int log2k, uint32_t win_cap) {
+    return kPHeader + kLutBytes + kPWarps * warp_region(log2k, win_cap);
+}
+
+template <int P>
+struct HalfBits;
+template <>
+struct HalfBits<7> {
+    using T = uint2;
+};
+template <>
+struct HalfBits<3> {
+    using T = uint32_t;
+};
+template <>
+struct HalfBits<1> {
+    using T = unsigned short;
+};
+template <>
+struct HalfBits<0> {
+    using T = unsigned char;
+};
+
+}  // namespace
+
+__device__ __forceinline__ uint32_t p_lds32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t p_lds8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t p_wait_token(uint32_t bar, uint32_t parity) {
+    uint32_t tok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "PWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "@!p bra PWAIT_%=;\n"
+        "mov.u32 %0, 0;\n"
+        "}\n"
+        : "=r"(tok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return tok;
+}
+__device__ __forceinline__ void p_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void p_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// The ANS step of decode_tiles.cu (register byte window variant).
+#define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
+    do {                                                                                     \
+        uint32_t a_;                                                                         \
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"((x) & 0xFFFu), "r"(lut));           \
+        v = p_lds32(a_);                                                                     \
+        x = ((v) >> 20) * (((x) >> kProbBits) - kProbScale) + ((v) >> 8);                    \
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 t, u;\n\t"                                      \
+            "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
+            "shf.r.clamp.b32 t, %3, %4, %2;\n\t"                                             \
+            "@q prmt.b32 %0, %0, t, 0x2104;\n\t"                                             \
+            "@q add.u32 %2, %2, 8;\n\t"                                                      \
+            "setp.lt.and.u32 q, %0, 8388608, q;\n\t"                                         \
+            "shf.r.clamp.b32 u, %3, %4, %2;\n\t"                                             \
+            "@q prmt.b32 %0, %0, u, 0x2104;\n\t"                                             \
+            "@q add.u32 %2, %2, 8;\n\t"                                                      \
+            "setp.ge.u32 q, %2, 32;\n\t"                                                     \
+            "@q mov.b32 %3, %4;\n\t"                                                         \
+            "@q add.u32 %1, %1, 4;\n\t"                                                      \
+            "@q sub.u32 %2, %2, 32;\n\t"                                                     \
+            "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
+            : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
+    } while (0)
+
+// Lane setup for one unit: the lane's sub-range (start state/position, end
+// state/position, symbol count) and the unit's payload window.
+struct LaneJob {
+    uint32_t x0, xe, cnt, err;
+    int64_t p0, pe;  // absolute stream offsets
+};
+
+// Raw index records of a lane's sub-range, loaded one unit ahead so the
+// global-memory latency never sits on a warp's critical path.
+struct RawRec {
+    uint4 ci;
+    uint2 rec, nxt;
+};
+
+template <int LOG2K>
+__device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint32_t nsub) {
+    RawRec r{make_uint4(0, 0, 0, 0), make_uint2(0, 0), make_uint2(0, 0)};
+    if (j >= nsub) return r;
+    uint32_t ch, jin;
+    sub_to_chunk(d, LOG2K, j, ch, jin);
+    r.ci = d.chunk_info[ch];
+    r.rec = d.ckpt[j];
+    if (j + 1 < nsub) r.nxt = d.ckpt[j + 1];
+    return r;
+}
+
+template <int LOG2K>
+__device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uint32_t nsub, bool single,
+                                            const RawRec& raw) {
+    constexpr int K = 1 << LOG2K;
+    LaneJob L{kStateLow, kStateLow, 0u, 0u, 0, 0};
+    if (j >= nsub) return L;
+    uint32_t ch, jin;
+    sub_to_chunk(d, LOG2K, j, ch, jin);
+    const uint4 ci = raw.ci;
+    const uint64_t off = chunk_offset(ci);
+    const uint32_t len = ci.z, nsym = ci.w;
+    const uint32_t sym_in = jin << LOG2K;
+    L.cnt = nsym > sym_in ? min((uint32_t)K, nsym - sym_in) : 0u;
+    if (len < 4) L.err |= kErrTruncated;  // ans.hpp:231-233
+    const uint32_t limit = len >= 4 ? len - 4 : 0;
+    if (jin == 0) {
+        // framing must agree with the index (ans.hpp:332-340); the chunk's first
+        // lane starts from the stream's own final state (ans.hpp:235-236)
+        if (ld_u32le_bytes(d.stream + off - 8) != nsym || ld_u32le_bytes(d.stream + off - 4) != len)
+            L.err |= kErrLength;
+        L.x0 = ld_u32le_bytes(d.stream + off + limit);
+    }
+    if (single) {
+        if (jin == 0 && len >= 4 && (L.x0 != kStateLow || len != 4)) L.err |= L.x0 < kStateLow ? kErrTruncated : kErrDesync;
+        L.p0 = L.pe = (int64_t)(off + limit);
+        return L;
+    }
+    const uint2 rec = raw.rec;
+    const bool last = sym_in + K >= nsym;
+    const uint2 end = last ? make_uint2(kStateLow, 0u) : raw.nxt;
+    const uint32_t e_start = jin == 0 ? limit : rec.y;
+    if (jin != 0) L.x0 = rec.x;
+    L.xe = end.x;
+    if (e_start > limit || end.y > limit) L.err |= kErrDesync;
+    L.p0 = (int64_t)(off + limit - min(e_start, limit));
+    L.pe = (int64_t)(off + limit - min(end.y, limit));
+    if (L.pe < L.p0) L.err |= kErrDesync;
+    return L;
+}
+
+template <int LOG2K, int P>
+__global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(const DecodeDesc* __restrict__ descs,
+                                                                      int ndesc,
+                                                                      const uint32_t* __restrict__ cta_prefix,
+                                                                      DecodeDesc one, uint32_t upc,
+                                                                      uint32_t win_cap) {
+    constexpr int K = 1 << LOG2K;
+    constexpr uint32_t RW = exps_row_words(LOG2K);
+    constexpr int G = K / 8;  // 8-element merge groups per lane per unit
+    using HB = typename HalfBits<P>::T;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t lut_bar = sbase;
+    const uint32_t my_bar0 = sbase + 128 + 16 * warp;  // two mbarriers per warp
+    const uint32_t lut = sbase + kPHeader;
+    const uint32_t region = sbase + kPHeader + kLutBytes + warp * warp_region(LOG2K, win_cap);
+    uint32_t* exps = reinterpret_cast<uint32_t*>(smem + (region - sbase));
+    const uint32_t winbuf0 = region + unit_words(LOG2K) * 4;
+    const uint32_t winstride = win_cap + 2 * K + 64;
+
+    // ---- which tensor / unit range this CTA owns
+    uint32_t cta = blockIdx.x;
+    const DecodeDesc* dp = &one;
+    if (descs) {
+        int lo = 0, hi = ndesc - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(cta_prefix + mid) <= cta) lo = mid; else hi = mid - 1;
+        }
+        dp = descs + lo;
+        cta -= __ldg(cta_prefix + lo);
+    }
+    const DecodeDesc d = *dp;
+    const uint32_t nsub = (uint32_t)ceil_div(d.n, K);
+    const uint32_t units = (nsub + 31) / 32;
+    const uint32_t ubeg = cta * upc, uend = min(units, ubeg + upc);
+    const bool single = d.flags & kFlagSingleSymbol;
+
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lut_bar));
+        for (int w = 0; w < kPWarps; ++w) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + 128 + 16 * w));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + 128 + 16 * w + 8));
+        }
+        fence_mbar_init();
+        if (!single) {
+            p_expect_tx(lut_bar, kLutBytes);
+            p_bulk(lut, d.lut, kLutBytes, lut_bar);
+        }
+    }
+    __syncthreads();
+    if (ubeg >= uend) {
+        if (!single) p_wait_token(lut_bar, 0);
+        return;
+    }
+
+    // ---- per-warp pipeline over units u = ubeg + warp + i * kPWarps
+    uint32_t err = 0;
+    // stage unit u into buffer b: returns this lane's job, issues the window TMA
+    auto stage = [&](uint32_t u, int b, uint64_t& wa_out, const RawRec& raw) -> LaneJob {
+        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw);
+        const int64_t a = __shfl_sync(0xFFFFFFFFu, L.p0, 0);
+        const uint32_t last_lane = min(31u, nsub - u * 32 - 1);
+        const int64_t e = __shfl_sync(0xFFFFFFFFu, L.pe, last_lane);
+        const uint64_t wa = (uint64_t)a & ~15ull;
+        uint64_t bytes = single ? 0 : (((uint64_t)e + 15) & ~15ull) - wa;
+        if (!single && ((uint64_t)e < (uint64_t)a || bytes > win_cap)) {
+            L.err |= kErrDesync;
+            bytes = 0;
+        }
+        if (!single && lane == 0) {
+            const uint32_t bar = my_bar0 + 8 * b;
+            p_expect_tx(bar, (uint32_t)bytes);
+            if (bytes) p_bulk(winbuf0 + b * winstride, d.stream + wa, (uint32_t)bytes, bar);
+        }
+        wa_out = wa;
+        return L;
+    };
+
+    uint32_t u = ubeg + warp;
+    uint64_t wa_cur = 0, wa_nxt = 0;
+    LaneJob cur{}, nxt{};
+    RawRec raw_n{};  // index records of unit u + kPWarps (loaded one iteration early)
+    if (u < uend) {
+        const RawRec r0 = load_raw<LOG2K>(d, u * 32 + lane, nsub);
+        if (u + kPWarps < uend) raw_n = load_raw<LOG2K>(d, (u + kPWarps) * 32 + lane, nsub);
+        cur = stage(u, 0, wa_cur, r0);
+    }
+    uint32_t tok = 0;
+    if (!single) tok = p_wait_token(lut_bar, 0);
+    const uint32_t lutt = lut + tok;
+
+    for (uint32_t i = 0; u < uend; ++i, u += kPWarps) {
+        const int b = i & 1;
+        const uint32_t un = u + kPWarps;
+        if (un < uend) {
+            nxt = stage(un, b ^ 1, wa_nxt, raw_n);
+            if (un + kPWarps < uend) raw_n = load_raw<LOG2K>(d, (un + kPWarps) * 32 + lane, nsub);
+        }
+        const uint64_t sym0 = (uint64_t)u * 32 * K;
+        const uint32_t unit_syms = (uint32_t)min((uint64_t)32 * K, d.n - sym0);
+        const uint32_t groups = unit_syms >> 3;
+        // sign/mantissa words of this unit: in flight during the decode
+        const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
+        HB pre[G];
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi) {
+            const uint32_t g = lane + gi * 32;
+            if (g < groups) pre[gi] = __ldcs(gb + g);
+        }
+        err |= cur.err;
+        uint32_t* row = exps + lane * RW;
+        if (single) {
+            const uint32_t wv = d.single_symbol * 0x01010101u;
+            for (uint32_t k = 0; k < (cur.cnt + 3) / 4; ++k) row[k] = wv;
+        } else {
+            const uint32_t t2 = p_wait_token(my_bar0 + 8 * b, (i >> 1) & 1);
+            if (!cur.err && cur.cnt) {
+                const uint32_t wbase = winbuf0 + b * winstride + t2;
+                uint32_t x = cur.x0;
+                const uint32_t p = wbase + (uint32_t)(cur.p0 - (int64_t)wa_cur);
+                uint32_t q = p & ~3u, o8 = (p & 3u) * 8;
+                uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
+                if (cur.cnt == (uint32_t)K) {
+#pragma unroll 1
+                    for (uint32_t k = 0; k < (uint32_t)K / 4; ++k) {
+                        uint32_t v0, v1, v2, v3;
+                        NZP_STEP(lutt, x, q, o8, w0, w1, v0);
+                        NZP_STEP(lutt, x, q, o8, w0, w1, v1);
+                        NZP_STEP(lutt, x, q, o8, w0, w1, v2);
+                        NZP_STEP(lutt, x, q, o8, w0, w1, v3);
+                        row[k] = __byte_perm(__byte_perm(v0, v1, 0x0040), __byte_perm(v2, v3, 0x0040), 0x5410);
+                    }
+                } else {
+                    uint32_t word = 0;
+                    for (uint32_t k = 0; k < cur.cnt; ++k) {
+                        uint32_t v;
+                        NZP_STEP(lutt, x, q, o8, w0, w1, v);
+                        word |= (v & 0xFFu) << (8 * (k & 3));
+                        if ((k & 3) == 3 || k + 1 == cur.cnt) {
+                            row[k >> 2] = word;
+                            word = 0;
+                        }
+                    }
+                }
+                const uint32_t pend = wbase + (uint32_t)(cur.pe - (int64_t)wa_cur);
+                const uint32_t pos = q + (o8 >> 3);
+                if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
+            }
+        }
+        __syncwarp();
+        // ---- merge this unit: 8-element groups, one coalesced 16-B store per lane
+        uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi) {
+            const uint32_t g = lane + gi * 32;
+            if (g >= groups) break;
+            const HB s = pre[gi];
+            const uint32_t e = g << 3;
+            const uint32_t* er = exps + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
+            const uint32_t e0 = er[0], e1 = er[1];
+            if constexpr (P == 7) {
+                __stcs(out + g, merge8(e0, s.x, e1, s.y));
+            } else {
+                constexpr uint32_t W = P + 1;
+                uint32_t bits;
+                if constexpr (W == 4) bits = __byte_perm(s, 0, 0x0123);
+                else if constexpr (W == 2) bits = __byte_perm((uint32_t)s, 0, 0x0144);
+                else bits = (uint32_t)s << 24;
+                const uint32_t B = d.block_size;
+                const uint64_t gidx = sym0 + e;
+                const uint64_t b0 = gidx / B;
+                const float c0 = scale_coef(__ldg(d.scales + b0));
+                const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
+                const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+                const uint32_t ew[2] = {e0, e1};
+                uint32_t res[4];
+#pragma unroll
+                for (int qq = 0; qq < 8; ++qq) {
+                    const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
+                    const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
+                    float c = qq < (int)split ? c0 : c1;
+                    if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
+                    const uint32_t h = lossy_rebuild(item, ex, P, c);
+                    if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
+                }
+                __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
+            }
+        }
+        for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
+            const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
+            const uint64_t gidx = sym0 + ii;
+            if constexpr (P == 7) {
+                const uint32_t sm = __ldg(d.mant + gidx);
+                d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
+            } else {
+                d.out[gidx] = lossy_rebuild(packed_item(d.mant, gidx, P), ex, P,
+                                            scale_coef(__ldg(d.scales + gidx / d.block_size)));
+            }
+        }
+        __syncwarp();
+        cur = nxt;
+        wa_cur = wa_nxt;
+    }
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(d.err, err);
+}
+
+// Largest per-unit payload window (32 sub-ranges) of a tensor.
+template <int LOG2K>
+__global__ void unit_window_max_kernel(DecodeDesc d, uint32_t* __restrict__ out) {
+    const uint32_t nsub = (uint32_t)ceil_div(d.n, 1u << LOG2K);
+    const uint32_t units = (nsub + 31) / 32;
+    uint32_t best = 0;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < units; t += gridDim.x * blockDim.x) {
+        const uint32_t sub0 = t * 32;
+        uint64_t a, b;
+        tile_window(d, sub0, min(32u, nsub - sub0), LOG2K, nsub, a, b);
+        const uint64_t bytes = (uint64_t)(((b + 15) & ~15ull) - (a & ~15ull));
+        best = max(best, (uint32_t)min(bytes, (uint64_t)0xFFFFFFFFu));
+    }
+    atomicMax(out, best);
+}
+
+// ------------------------------------------------------------ launchers --
+template <int LOG2K, int P>
+static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* cta_prefix, const DecodeDesc& one,
+                            uint32_t ctas, uint32_t upc, uint32_t win_cap, cudaStream_t s) {
+    const uint32_t smem = persist_smem(LOG2K, win_cap);
+    static uint32_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(decode_persist_kernel<LOG2K, P>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap);
+    return cudaGetLastError();
+}
+
+template <int LOG2K>
+static cudaError_t launch_pk(int precision, const DecodeDesc* descs, int ndesc, const uint32_t* cta_prefix,
+                             const DecodeDesc& one, uint32_t ctas, uint32_t upc, uint32_t win_cap, cudaStream_t s) {
+    switch (precision) {
+        case 7: return launch_p<LOG2K, 7>(descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        case 3: return launch_p<LOG2K, 3>(descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        case 1: return launch_p<LOG2K, 1>(descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        case 0: return launch_p<LOG2K, 0>(descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* descs, int ndesc,
+                                  const uint32_t* cta_prefix, const DecodeDesc& one, uint32_t ctas, uint32_t upc,
+                                  uint32_t win_cap, cudaStream_t s) {
+    if (ctas == 0) return cudaSuccess;
+    switch (log2k) {
+        case 6: return launch_pk<6>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        case 7: return launch_pk<7>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        case 8: return launch_pk<8>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool persist_fits(int log2k, uint32_t win_cap) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return persist_smem(log2k, win_cap) <= (uint32_t)optin;
+}
+
+// CTAs of the persistent kernel that fit on the device at once.
+uint32_t persist_resident_ctas(int log2k, uint32_t win_cap) {
+    const uint32_t smem = persist_smem(log2k, win_cap);
+    int dev = 0, sms = 148, per_sm_smem = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    uint32_t per_sm = smem ? (uint32_t)per_sm_smem / (smem + 1024) : 1;
+    const uint32_t by_threads = 2048u / (uint32_t)kPThreads;
+    if (per_sm > by_threads) per_sm = by_threads;
+    if (per_sm < 1) per_sm = 1;
+    return (uint32_t)sms * per_sm;
+}
+
+cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s) {
+    switch (log2k) {
+        case 6: unit_window_max_kernel<6><<<148, 256, 0, s>>>(d, out); break;
+        case 7: unit_window_max_kernel<7><<<148, 256, 0, s>>>(d, out); break;
+        case 8: unit_window_max_kernel<8><<<148, 256, 0, s>>>(d, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace nzgpu

@@ -113,6 +113,7 @@ SIGNATURES = {
     "nzgpu_version": (_i, []),
     "nzgpu_device_check": (_i, [_p(_i)]),
     "nzgpu_last_error_message": (C.c_char_p, []),
+    "nzgpu_set_decode_kernel": (_i, [_i]),
     "nzgpu_compress": (_i, [_vp, _u64, _i, _u32, _u32, _u32, _vp, _p(_vp)]),
     "nzgpu_decompress": (_i, [_vp, _vp, _vp]),
     "nzgpu_blob_status": (_i, [_vp, _vp]),
