@@ -97,13 +97,48 @@ __device__ __forceinline__ void p_bulk(uint32_t dst, const void* src, uint32_t b
                  : "memory");
 }
 
-// The ANS step of decode_tiles.cu (register byte window variant).
-#define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
+// Multiplier constants for the FMA-pipe state transition, passed as a kernel
+// parameter so ptxas cannot strength-reduce the mul.hi back to ALU shifts.
+struct MulConsts {
+    uint32_t two20, two12, two24, m4096, m16384;
+};
+
+#ifndef NZ_FMA
+#define NZ_FMA 0  // measured: 281 us vs 245 us (IMAD.HI costs more than the shifts it replaces)
+#endif
+
+// The ANS step of decode_tiles.cu (register byte window variant).  With
+// NZ_FMA the state transition runs entirely on the FMA pipe:
+//   h = mul.hi(x, 2^20) = x >> 12,  a = lut + 4x - 16384 h = lut + 4 (x & 0xFFF),
+//   f = mul.hi(v, 2^12) = v >> 20,  x = f h + (mul.hi(v, 2^24) - 4096 f)
+// leaving the (half-rate) ALU pipe to the renormalisation -- ncu showed the
+// ALU pipe 89% busy and the FMA pipe 25% with shifts/masks.
+#if NZ_FMA
+#define NZP_TRANSITION(lut, x, v)                                                            \
+    do {                                                                                     \
+        uint32_t h_, a_, f_, t_;                                                             \
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(h_) : "r"(x), "r"(mc.two20));                    \
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"(x), "r"(lut));                      \
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a_) : "r"(h_), "r"(mc.m16384), "r"(a_));      \
+        v = p_lds32(a_);                                                                     \
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(f_) : "r"(v), "r"(mc.two12));                    \
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(t_) : "r"(v), "r"(mc.two24));                    \
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t_) : "r"(f_), "r"(mc.m4096), "r"(t_));       \
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(f_), "r"(h_), "r"(t_));             \
+    } while (0)
+#else
+#define NZP_TRANSITION(lut, x, v)                                                            \
     do {                                                                                     \
         uint32_t a_;                                                                         \
         asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"((x) & 0xFFFu), "r"(lut));           \
         v = p_lds32(a_);                                                                     \
         x = ((v) >> 20) * (((x) >> kProbBits) - kProbScale) + ((v) >> 8);                    \
+    } while (0)
+#endif
+
+#define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
+    do {                                                                                     \
+        NZP_TRANSITION(lut, x, v);                                                           \
         asm("{\n\t.reg .pred q;\n\t.reg .b32 t, u;\n\t"                                      \
             "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
             "shf.r.clamp.b32 t, %3, %4, %2;\n\t"                                             \
@@ -192,7 +227,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                                                                       int ndesc,
                                                                       const uint32_t* __restrict__ cta_prefix,
                                                                       DecodeDesc one, uint32_t upc,
-                                                                      uint32_t win_cap) {
+                                                                      uint32_t win_cap, MulConsts mc) {
     constexpr int K = 1 << LOG2K;
     constexpr uint32_t RW = exps_row_words(LOG2K);
     constexpr int G = K / 8;  // 8-element merge groups per lane per unit
@@ -424,7 +459,8 @@ static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* 
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap);
+    const MulConsts mc{1u << 20, 1u << 12, 1u << 24, 0xFFFFF000u, 0xFFFFC000u};
+    decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap, mc);
     return cudaGetLastError();
 }
 
