@@ -91,7 +91,9 @@ typedef struct nzgpu_blob_info {
     const uint16_t* d_freqs;
     const uint8_t* d_mantissas;
     const uint8_t* d_scales;
-    uint32_t flags;           /* bit0: single-symbol table; bit1: irregular framing (sequential decode) */
+    uint32_t flags;           /* bit0: single-symbol table; bit1: irregular framing (sequential
+                                 decode); bit2: table codes exponent 255; bit3: a lossy scale
+                                 byte >= 128 (bits 2-3 select the float lossy merge) */
     uint32_t max_window;      /* largest per-tile payload window (bytes)        */
 } nzgpu_blob_info;
 

@@ -207,12 +207,13 @@ struct nzgpu_blob_s {
         d.err = err;
         d.n = n;
         d.chunk_syms = chunk_syms;
-        d.flags = flags & kFlagSingleSymbol;
+        d.flags = flags & (kFlagSingleSymbol | kFlagSlowLossy);
         d.single_symbol = single_symbol;
         d.precision = precision;
         d.block_size = block ? block : 1;
         const uint32_t spc = interval ? chunk_syms / interval : 0;
         d.log2_spc = (spc && !(spc & (spc - 1))) ? (uint32_t)__builtin_ctz(spc) : 0xFFFFFFFFu;
+        d.log2_block = !(d.block_size & (d.block_size - 1)) ? (uint32_t)__builtin_ctz(d.block_size) : 0xFFFFFFFFu;
         return d;
     }
     uint64_t tiles() const { return decode_tiles_for(nsub); }
@@ -277,6 +278,14 @@ int walk_stream(const uint8_t* s, uint64_t len, std::vector<uint4>& info, uint64
     return NZGPU_OK;
 }
 
+// kFlagWideScale when an imported lossy blob has a scale byte >= 128.
+uint32_t wide_scale_flag(const nzgpu_host_tensor* t) {
+    if (t->precision == 7 || !t->scales) return 0u;
+    for (uint64_t i = 0; i < t->scales_len; ++i)
+        if (t->scales[i] & 0x80u) return kFlagWideScale;
+    return 0u;
+}
+
 // Exponent-table upload + validation (deserialize_table, ans.hpp:120-130)
 // + packed decode LUT; reads back flags.
 int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
@@ -288,7 +297,7 @@ int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
     CK(cudaMemcpyAsync(info, b->scratch_u32, 12, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (info[2]) return status_from_bits(info[2]);
-    b->flags |= info[0] & kFlagSingleSymbol;
+    b->flags |= info[0] & (kFlagSingleSymbol | kFlagHas255);
     b->single_symbol = info[1];
     return NZGPU_OK;
 }
@@ -396,7 +405,7 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
         if (c + 1 < info.size() ? info[c].w != S : (info[c].w == 0 || info[c].w > S)) uniform = false;
     }
     b->chunk_syms = S;
-    b->flags = uniform || t->n == 0 ? 0u : kFlagIrregular;
+    b->flags = (uniform || t->n == 0 ? 0u : kFlagIrregular) | wide_scale_flag(t);
     rc = blob_alloc(b, !uniform);
     if (rc) return rc;
     CK(cudaMalloc(&b->stream, align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32));
@@ -521,7 +530,7 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
         cudaFreeAsync(tmp, s);
         return status_from_bits(err_bits | info[2]);
     }
-    b->flags = (info[0] & kFlagSingleSymbol) | (irregular ? kFlagIrregular : 0u);
+    b->flags = (info[0] & (kFlagSingleSymbol | kFlagHas255)) | (irregular ? kFlagIrregular : 0u);
     b->single_symbol = info[1];
     b->stream_len = stream_len;
     CK(cudaMalloc(reinterpret_cast<void**>(&b->stream), align_up(stream_len, 16) + 32));
@@ -911,7 +920,8 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     b.mant_len = t->mantissa_len;
     b.scales_len = t->precision == 7 ? 0 : t->scales_len;
     b.stream_len = t->stream_len;
-    b.flags = single != 0xFFFFFFFFu ? kFlagSingleSymbol : 0u;
+    b.flags = (single != 0xFFFFFFFFu ? kFlagSingleSymbol : 0u) | (t->freqs[255] ? kFlagHas255 : 0u) |
+              wide_scale_flag(t);
     b.single_symbol = single != 0xFFFFFFFFu ? single : 0u;
     Carve cv;
     const uint64_t o_freqs = cv.take(512), o_lut = cv.take(16384), o_mant = cv.take(b.mant_len + 16);

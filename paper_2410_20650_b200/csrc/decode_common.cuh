@@ -96,10 +96,70 @@ __device__ __forceinline__ uint16_t lossy_rebuild(uint32_t item, uint32_t e, int
     const uint32_t sgn = item >> k;
     const uint32_t m = item & ((1u << k) - 1u);
     const uint32_t normalized = (sgn << 15) | (e << 7) | (m << (7 - k));
+    // Inf * c stays Inf; a NaN keeps its payload with the quiet bit set (what
+    // the reference's double multiply does on the host, where the GPU would
+    // return the canonical NaN).
+    if (e == 255) return (uint16_t)(m ? normalized | 0x40u : normalized);
     return bf16_from_float(__fmul_rn(__uint_as_float(normalized << 16), c));
 }
 
 __device__ __forceinline__ float scale_coef(uint32_t s) { return 1.0f + (float)s * (1.0f / 128.0f); }
+
+// Two bf16 lanes times two bf16 lanes, one correctly rounded (RNE) multiply.
+__device__ __forceinline__ uint32_t bf16x2_mul(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// The lossy block coefficient 1 + s/128 (tensorstore.hpp:231) is exactly the
+// bf16 with exponent 127 and mantissa s: 0x3F80 | s.
+__device__ __forceinline__ uint32_t scale_coef_bf16(uint32_t s) { return 0x3F80u | s; }
+
+// Eight lossy elements (decompress_lossy, tensorstore.hpp:229-236) on the
+// bf16x2 pipe.  The reference multiplies the normalized bf16 (8 significant
+// bits) by c (8 significant bits) in double and rounds once to bf16 through
+// float; the product is exact in both, so a single RNE bf16 multiply gives
+// the same bits for every finite and infinite operand.  NaN payloads differ
+// (the hardware returns the canonical NaN) -- callers take the float path
+// when the table can produce exponent 255 (kFlagHas255).
+//
+// raw holds the 8 packed (k+1)-bit items as loaded (first item in the MSBs
+// of byte 0).  Each item (s<<k | m) becomes the byte s<<7 | m<<(7-k), the
+// lossless sign/mantissa layout, so merge4 rebuilds the normalized values:
+//   k=3: even/odd nibbles masked in place, interleaved by two PRMTs;
+//   k=1: x * (1 + 2^10 + 2^20 + 2^30) moves 2-bit field j of byte x to bits
+//        6-7 of byte j (the shifted copies do not overlap, so no carries);
+//   k=0: x * (1 + 2^9 + 2^18 + 2^27) moves bit 7-j to bit 7 of byte j.
+// Elements [0, split) take coefficient c0, the rest c1 (bf16 bits).
+template <int P>
+__device__ __forceinline__ uint4 lossy_merge8(uint32_t e0, uint32_t e1, uint32_t raw, uint32_t c0, uint32_t c1,
+                                              uint32_t split) {
+    uint32_t sa, sb;
+    if constexpr (P == 3) {
+        const uint32_t ev = raw & 0xF0F0F0F0u, od = (raw << 4) & 0xF0F0F0F0u;
+        sa = __byte_perm(ev, od, 0x5140);
+        sb = __byte_perm(ev, od, 0x7362);
+    } else if constexpr (P == 1) {
+        sa = ((raw & 0xFFu) * 0x40100401u) & 0xC0C0C0C0u;
+        sb = (((raw >> 8) & 0xFFu) * 0x40100401u) & 0xC0C0C0C0u;
+    } else {
+        static_assert(P == 0, "lossy precision");
+        sa = ((raw & 0xFFu) * 0x08040201u) & 0x80808080u;
+        sb = (((raw << 4) & 0xF0u) * 0x08040201u) & 0x80808080u;
+    }
+    const uint2 a = merge4(e0, sa), b = merge4(e1, sb);
+    uint32_t cp[4];
+    if (split >= 8) {
+        cp[0] = cp[1] = cp[2] = cp[3] = c0 | (c0 << 16);
+    } else {
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            cp[p] = ((uint32_t)(2 * p) < split ? c0 : c1) | (((uint32_t)(2 * p + 1) < split ? c0 : c1) << 16);
+    }
+    return make_uint4(bf16x2_mul(a.x, cp[0]), bf16x2_mul(a.y, cp[1]), bf16x2_mul(b.x, cp[2]),
+                      bf16x2_mul(b.y, cp[3]));
+}
 
 // (k+1)-bit item i of a packed MSB-first stream (bitfloat.hpp:156-162).
 __device__ __forceinline__ uint32_t packed_item(const uint8_t* packed, uint64_t i, int k) {

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const uint32_t units = (nsub + 31) / 32;
     const uint32_t ubeg = cta * upc, uend = min(units, ubeg + upc);
     const bool single = d.flags & kFlagSingleSymbol;
+    const bool fast_lossy = d.block_size >= 8 && !(d.flags & kFlagSlowLossy);
 
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lut_bar));
@@ -386,6 +387,19 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
             const uint32_t e0 = er[0], e1 = er[1];
             if constexpr (P == 7) {
                 __stcs(out + g, merge8(e0, s.x, e1, s.y));
+            } else if (fast_lossy) {
+                const uint64_t gidx = sym0 + e;
+                uint32_t b0, split;
+                if (d.log2_block != 0xFFFFFFFFu) {
+                    b0 = (uint32_t)(gidx >> d.log2_block);
+                    split = min(8u, d.block_size - ((uint32_t)gidx & (d.block_size - 1u)));
+                } else {
+                    b0 = (uint32_t)(gidx / d.block_size);
+                    split = (uint32_t)min((uint64_t)8, (uint64_t)(b0 + 1) * d.block_size - gidx);
+                }
+                const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
+                const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
+                __stcs(out + g, lossy_merge8<P>(e0, e1, (uint32_t)s, c0, c1, split));
             } else {
                 constexpr uint32_t W = P + 1;
                 uint32_t bits;

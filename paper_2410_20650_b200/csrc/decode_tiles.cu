@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
     const uint32_t tile_syms = (uint32_t)min((uint64_t)TS * K, d.n - sym0);
     const uint32_t groups = tile_syms >> 3;
     const bool single = d.flags & kFlagSingleSymbol;
+    const bool fast_lossy = d.block_size >= 8 && !(d.flags & kFlagSlowLossy);
 
     if (tid == 0) {
         mbar_init(bar, 1);
@@ -382,6 +383,19 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
         const uint32_t e0 = er[0], e1 = er[1];
         if constexpr (P == 7) {
             __stcs(out + g, merge8(e0, s.x, e1, s.y));
+        } else if (fast_lossy) {
+            const uint64_t gi = sym0 + e;
+            uint32_t b0, split;
+            if (d.log2_block != 0xFFFFFFFFu) {
+                b0 = (uint32_t)(gi >> d.log2_block);
+                split = min(8u, B - ((uint32_t)gi & (B - 1u)));
+            } else {
+                b0 = (uint32_t)(gi / B);
+                split = (uint32_t)min((uint64_t)8, (uint64_t)(b0 + 1) * B - gi);
+            }
+            const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
+            const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
+            __stcs(out + g, lossy_merge8<P>(e0, e1, (uint32_t)s, c0, c1, split));
         } else {
             constexpr uint32_t W = P + 1;
             // 8 items of W bits, MSB-first: gather big-endian into the top bits.

@@ -41,7 +41,13 @@ __host__ __device__ inline uint32_t lut_entry(uint32_t sym, uint32_t bias, uint3
     return sym | (bias << 8) | (freq << 20);
 }
 
-enum : uint32_t { kFlagSingleSymbol = 1u };
+// kFlagHas255: the table gives symbol 255 (exponent of Inf/NaN) a nonzero
+// frequency, so decoded values may be non-finite; kFlagWideScale: a lossy
+// scale byte >= 128 (never produced by compress_lossy, whose scales are 7-bit
+// mantissas, but legal in an imported blob).  Either sends the lossy merge to
+// the float path.
+enum : uint32_t { kFlagSingleSymbol = 1u, kFlagHas255 = 4u, kFlagWideScale = 8u };
+constexpr uint32_t kFlagSlowLossy = kFlagHas255 | kFlagWideScale;
 
 // Per-symbol encoder constants (ans.hpp:209-219):
 // rcp = floor(2^32 / f) (f == 1: 0xFFFFFFFF), used with one correction step.
@@ -64,11 +70,12 @@ struct DecodeDesc {
     uint32_t* err;                // sticky error word
     uint64_t n;                   // elements
     uint32_t chunk_syms;          // uniform chunk size S (multiple of K)
-    uint32_t flags;               // kFlagSingleSymbol
+    uint32_t flags;               // kFlagSingleSymbol | kFlagHas255
     uint32_t single_symbol;       // the exponent when kFlagSingleSymbol
     int32_t precision;            // 7 lossless, 0/1/3 lossy
     uint32_t block_size;          // lossy block size B
     uint32_t log2_spc;            // log2(S/K) when S/K is a power of two, else 0xFFFFFFFF
+    uint32_t log2_block;          // log2(B) when B is a power of two, else 0xFFFFFFFF
 };
 
 // ------------------------------------------------------------------ PTX --

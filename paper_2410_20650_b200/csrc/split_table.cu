@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(256) build_table_kernel(const unsigned long lo
         e.pad = 0;
         enc[s] = e;
     }
+    if (s == 255 && f > 0) atomicOr(info, kFlagHas255);
     if (f == kProbScale) {
-        info[0] = kFlagSingleSymbol;
+        atomicOr(info, kFlagSingleSymbol);
         info[1] = (uint32_t)s;
     }
     // Decode LUT: thread s fills slots s*16 .. s*16+15 (binary search in cum).

@@ -125,6 +125,41 @@ def test_gpu_lossy_elementwise_exhaustive(nz, port, k):
     assert (got == want).all(), int((got != want).sum())
 
 
+@pytest.mark.parametrize("k", [0, 1, 3])
+@pytest.mark.parametrize("variant", ["fast", "wide_scales", "exp255"])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_gpu_lossy_decode_merge_exhaustive(nz, port, k, variant, kernel):
+    """Every (scale byte, exponent, packed item) triple through the decode
+    kernels' merge (block b holds every (exponent, item) pair under scale b).
+    'fast' takes the bf16x2 multiply; a scale byte >= 128 or a table that can
+    decode exponent 255 (Inf/NaN payloads) must take the float path and still
+    match the oracle bit for bit."""
+    import torch
+
+    ne = 256 if variant == "exp255" else 255
+    ns = 256 if variant == "wide_scales" else 128
+    w = 1 << (k + 1)
+    e = np.tile(np.arange(ne, dtype=np.uint8), w)
+    it = np.repeat(np.arange(w, dtype=np.uint8), ne)
+    B = e.size
+    exps, items = np.tile(e, ns), np.tile(it, ns)
+    scales = np.arange(ns, dtype=np.uint8)
+    n = exps.size
+    freqs = port.build_table(np.bincount(exps, minlength=256).astype(np.uint64))
+    stream = port.encode_stream(exps, freqs)
+    packed = port.pack(items >> k, items & ((1 << k) - 1), k)
+    want = port.decompress_lossy(freqs, scales, stream, packed, k, B, n)
+    blob = nz.LossyBlob(nz.TensorMeta((n,)), k, B, scales, freqs, stream, packed)
+    nz.nzgpu.lib.nzgpu_set_decode_kernel(kernel)
+    try:
+        got = nz.DeviceBlob.from_host(blob).decompress().view(torch.int16).cpu().numpy().view(np.uint16)
+        host = nz.decompress_lossy(blob)
+    finally:
+        nz.nzgpu.lib.nzgpu_set_decode_kernel(0)
+    assert (got == want).all(), int((got != want).sum())
+    assert (host == want).all(), int((host != want).sum())
+
+
 def test_gpu_lossy_decodes_reference_produced_blobs(nz, port):
     v = port.gaussian_bf16(31, 200003, 0.02)
     for k, B in ((0, 512), (1, 7), (3, 64)):
