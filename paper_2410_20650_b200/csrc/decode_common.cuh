@@ -74,14 +74,21 @@ __device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, 
     if (b < a) b = a;
 }
 
+// bitwise c ? a : b in one LOP3
+__device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 // Four bf16 from four exponent bytes E and four sign/mantissa bytes S
 // (merge, bitfloat.hpp:64-71, on the tensorstore.hpp:119-123 fields):
 // bf16 = s<<15 | e<<7 | m has high byte s<<7 | e>>1 and low byte
 // (e&1)<<7 | m, so build all four high bytes and all four low bytes with
-// one shift + one LOP3 each, then interleave them with two PRMTs.
+// one shift + one bit-select LOP3 each, then interleave them with two PRMTs.
 __device__ __forceinline__ uint2 merge4(uint32_t e4, uint32_t s4) {
-    const uint32_t hi = ((e4 >> 1) & 0x7F7F7F7Fu) | (s4 & 0x80808080u);
-    const uint32_t lo = ((e4 << 7) & 0x80808080u) | (s4 & 0x7F7F7F7Fu);
+    const uint32_t hi = bitsel(e4 >> 1, s4, 0x7F7F7F7Fu);
+    const uint32_t lo = bitsel(e4 << 7, s4, 0x80808080u);
     return make_uint2(__byte_perm(lo, hi, 0x5140), __byte_perm(lo, hi, 0x7362));
 }
 

@@ -19,6 +19,10 @@
 #ifndef NZ_PWARPS
 #define NZ_PWARPS 32  // warps per persistent CTA (one CTA per SM)
 #endif
+#ifndef NZ_PUNROLL
+#define NZ_PUNROLL 16  // 4-step groups of the full-sub-range decode loop unrolled (16 = all of K=64)
+#endif
+
 #ifndef NZ_PMINB
 #define NZ_PMINB 1  // resident CTAs per SM the register budget must allow
 #endif
@@ -28,6 +32,7 @@ namespace nzgpu {
 namespace {
 
 constexpr int kPWarps = NZ_PWARPS;
+constexpr int kPUnroll = NZ_PUNROLL;
 constexpr int kPThreads = kPWarps * 32;
 constexpr uint32_t kPHeader = 128 + 2 * 8 * kPWarps;  // LUT barrier + 2 mbarriers per warp
 
@@ -136,6 +141,31 @@ struct MulConsts {
     } while (0)
 #endif
 
+#ifndef NZ_PBYTES
+#define NZ_PBYTES 0
+#endif
+
+#if NZ_PBYTES
+// Renormalisation bytes loaded from shared memory one at a time (q is the
+// byte pointer): both "need a byte" predicates are known right after the
+// transition (x < 2^23, x < 2^15), so the two loads issue together and the
+// byte insertion runs on the FMA pipe (x*256 + b) -- 2 ALU ops per step
+// instead of the window's 8.
+#define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
+    do {                                                                                     \
+        NZP_TRANSITION(lut, x, v);                                                           \
+        asm("{\n\t.reg .pred p1, p2;\n\t.reg .b32 b0, b1;\n\t"                                 \
+            "setp.lt.u32 p1, %0, 8388608;\n\t"                                               \
+            "setp.lt.u32 p2, %0, 32768;\n\t"                                                 \
+            "@p1 ld.shared.u8 b0, [%1];\n\t"                                                 \
+            "@p2 ld.shared.u8 b1, [%1+1];\n\t"                                               \
+            "@p1 mad.lo.u32 %0, %0, 256, b0;\n\t"                                            \
+            "@p1 add.u32 %1, %1, 1;\n\t"                                                     \
+            "@p2 mad.lo.u32 %0, %0, 256, b1;\n\t"                                            \
+            "@p2 add.u32 %1, %1, 1;\n\t}"                                                    \
+            : "+r"(x), "+r"(q));                                                             \
+    } while (0)
+#else
 #define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
     do {                                                                                     \
         NZP_TRANSITION(lut, x, v);                                                           \
@@ -155,6 +185,7 @@ struct MulConsts {
             "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
             : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
     } while (0)
+#endif
 
 // Lane setup for one unit: the lane's sub-range (start state/position, end
 // state/position, symbol count) and the unit's payload window.
@@ -328,11 +359,17 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         const uint32_t groups = unit_syms >> 3;
         // sign/mantissa words of this unit: in flight during the decode
         const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
+        const bool full = unit_syms == 32u * K;  // every unit but a tensor's last
         HB pre[G];
+        if (full) {
 #pragma unroll
-        for (int gi = 0; gi < G; ++gi) {
-            const uint32_t g = lane + gi * 32;
-            if (g < groups) pre[gi] = __ldcs(gb + g);
+            for (int gi = 0; gi < G; ++gi) pre[gi] = __ldcs(gb + lane + gi * 32);
+        } else {
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+                const uint32_t g = lane + gi * 32;
+                if (g < groups) pre[gi] = __ldcs(gb + g);
+            }
         }
         err |= cur.err;
         uint32_t* row = exps + lane * RW;
@@ -345,10 +382,14 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                 const uint32_t wbase = winbuf0 + b * winstride + t2;
                 uint32_t x = cur.x0;
                 const uint32_t p = wbase + (uint32_t)(cur.p0 - (int64_t)wa_cur);
+#if NZ_PBYTES
+                uint32_t q = p, o8 = 0, w0 = 0, w1 = 0;
+#else
                 uint32_t q = p & ~3u, o8 = (p & 3u) * 8;
                 uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
+#endif
                 if (cur.cnt == (uint32_t)K) {
-#pragma unroll 1
+#pragma unroll kPUnroll
                     for (uint32_t k = 0; k < (uint32_t)K / 4; ++k) {
                         uint32_t v0, v1, v2, v3;
                         NZP_STEP(lutt, x, q, o8, w0, w1, v0);
@@ -376,14 +417,17 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         }
         __syncwarp();
         // ---- merge this unit: 8-element groups, one coalesced 16-B store per lane
+        // group g = lane + 32 gi starts at element 8g: row (8g) / K, word ((8g) % K) / 4,
+        // i.e. a per-lane base plus a compile-time stride per gi (K <= 256)
         uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
+        const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
 #pragma unroll
         for (int gi = 0; gi < G; ++gi) {
             const uint32_t g = lane + gi * 32;
-            if (g >= groups) break;
+            if (!full && g >= groups) break;
             const HB s = pre[gi];
             const uint32_t e = g << 3;
-            const uint32_t* er = exps + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
+            const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
             const uint32_t e0 = er[0], e1 = er[1];
             if constexpr (P == 7) {
                 __stcs(out + g, merge8(e0, s.x, e1, s.y));
