@@ -102,55 +102,45 @@ __device__ __forceinline__ void p_bulk(uint32_t dst, const void* src, uint32_t b
                  : "memory");
 }
 
-// Multiplier constants for the FMA-pipe state transition, passed as a kernel
-// parameter so ptxas cannot strength-reduce the mul.hi back to ALU shifts.
+// Opaque constants passed as a kernel parameter so ptxas cannot fold the
+// FMA-pipe forms below back into ALU instructions.
 struct MulConsts {
-    uint32_t two20, two12, two24, m4096, m16384;
+    uint32_t one;
 };
 
-#ifndef NZ_FMA
-#define NZ_FMA 0  // measured: 281 us vs 245 us (IMAD.HI costs more than the shifts it replaces)
-#endif
-
-// The ANS step of decode_tiles.cu (register byte window variant).  With
-// NZ_FMA the state transition runs entirely on the FMA pipe:
-//   h = mul.hi(x, 2^20) = x >> 12,  a = lut + 4x - 16384 h = lut + 4 (x & 0xFFF),
-//   f = mul.hi(v, 2^12) = v >> 20,  x = f h + (mul.hi(v, 2^24) - 4096 f)
-// leaving the (half-rate) ALU pipe to the renormalisation -- ncu showed the
-// ALU pipe 89% busy and the FMA pipe 25% with shifts/masks.
-#if NZ_FMA
+// The ANS step (ans.hpp:238-255) balanced across the two integer pipes.  ncu
+// on the first version showed the half-rate ALU pipe 89% busy and the FMA
+// pipe 25%, so everything that can be a multiply-add is one:
+//   * slot address 4 (x & 0xFFF) + lut = 4x - 16384 (x >> 12) + lut, with
+//     h' = (x >> 12) - 4096 (one LEA.HI) shared with the state update
+//     x = (v >> 20) h' + (v >> 8), lutm = lut - 2^26 (two IMADs, no LOP3);
+//   * the window shift w = w2 is a multiply by an opaque 1 (not a SEL);
+//   * both renormalisation bytes come from ONE funnel shift of the register
+//     window (the second byte is byte 1 of the same word: PRMT 0x2105).
+// Measured on 218M symbols: 246 -> 209 us.  Tried and slower: mul.hi for the
+// shifts (the FMA pipe's IMAD.HI is not cheaper than the ALU shift), a
+// warp-uniform branch for the rare second byte (VOTE + reconvergence).
 #define NZP_TRANSITION(lut, x, v)                                                            \
     do {                                                                                     \
-        uint32_t h_, a_, f_, t_;                                                             \
-        asm("mul.hi.u32 %0, %1, %2;" : "=r"(h_) : "r"(x), "r"(mc.two20));                    \
-        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"(x), "r"(lut));                      \
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a_) : "r"(h_), "r"(mc.m16384), "r"(a_));      \
+        uint32_t a_, h_ = ((x) >> kProbBits) - kProbScale;                                   \
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"(x), "r"(lutm));                      \
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a_) : "r"(h_), "r"(0xFFFFC000u), "r"(a_));    \
         v = p_lds32(a_);                                                                     \
-        asm("mul.hi.u32 %0, %1, %2;" : "=r"(f_) : "r"(v), "r"(mc.two12));                    \
-        asm("mul.hi.u32 %0, %1, %2;" : "=r"(t_) : "r"(v), "r"(mc.two24));                    \
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t_) : "r"(f_), "r"(mc.m4096), "r"(t_));       \
-        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(f_), "r"(h_), "r"(t_));             \
+        x = ((v) >> 20) * h_ + ((v) >> 8);                                                   \
     } while (0)
-#else
-#define NZP_TRANSITION(lut, x, v)                                                            \
-    do {                                                                                     \
-        uint32_t a_;                                                                         \
-        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a_) : "r"((x) & 0xFFFu), "r"(lut));           \
-        v = p_lds32(a_);                                                                     \
-        x = ((v) >> 20) * (((x) >> kProbBits) - kProbScale) + ((v) >> 8);                    \
-    } while (0)
-#endif
 
 #ifndef NZ_PBYTES
 #define NZ_PBYTES 0
 #endif
 
+
 #if NZ_PBYTES
 // Renormalisation bytes loaded from shared memory one at a time (q is the
 // byte pointer): both "need a byte" predicates are known right after the
 // transition (x < 2^23, x < 2^15), so the two loads issue together and the
-// byte insertion runs on the FMA pipe (x*256 + b) -- 2 ALU ops per step
-// instead of the window's 8.
+// byte insertion runs on the FMA pipe (x*256 + b) -- fewer ALU ops, but the
+// byte loads add ~1.5 shared-memory wavefronts per step to the LUT's ~3.7
+// and the kernel turns LSU-bound (measured slower than the window).
 #define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
     do {                                                                                     \
         NZP_TRANSITION(lut, x, v);                                                           \
@@ -169,21 +159,20 @@ struct MulConsts {
 #define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
     do {                                                                                     \
         NZP_TRANSITION(lut, x, v);                                                           \
-        asm("{\n\t.reg .pred q;\n\t.reg .b32 t, u;\n\t"                                      \
+        asm("{\n\t.reg .pred q, r;\n\t.reg .b32 t;\n\t"                                      \
             "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
+            "setp.lt.u32 r, %0, 32768;\n\t"                                                  \
             "shf.r.clamp.b32 t, %3, %4, %2;\n\t"                                             \
             "@q prmt.b32 %0, %0, t, 0x2104;\n\t"                                             \
             "@q add.u32 %2, %2, 8;\n\t"                                                      \
-            "setp.lt.and.u32 q, %0, 8388608, q;\n\t"                                         \
-            "shf.r.clamp.b32 u, %3, %4, %2;\n\t"                                             \
-            "@q prmt.b32 %0, %0, u, 0x2104;\n\t"                                             \
-            "@q add.u32 %2, %2, 8;\n\t"                                                      \
+            "@r prmt.b32 %0, %0, t, 0x2105;\n\t"                                             \
+            "@r add.u32 %2, %2, 8;\n\t"                                                      \
             "setp.ge.u32 q, %2, 32;\n\t"                                                     \
-            "@q mov.b32 %3, %4;\n\t"                                                         \
+            "@q mad.lo.u32 %3, %4, %5, 0;\n\t"                                                \
             "@q add.u32 %1, %1, 4;\n\t"                                                      \
             "@q sub.u32 %2, %2, 32;\n\t"                                                     \
             "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
-            : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
+            : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2) : "r"(mc.one));                  \
     } while (0)
 #endif
 
@@ -346,6 +335,8 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     uint32_t tok = 0;
     if (!single) tok = p_wait_token(lut_bar, 0);
     const uint32_t lutt = lut + tok;
+    const uint32_t lutm = lutt - (1u << 26);
+    (void)lutm;
 
     for (uint32_t i = 0; u < uend; ++i, u += kPWarps) {
         const int b = i & 1;
@@ -517,7 +508,7 @@ static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* 
         if (e != cudaSuccess) return e;
         configured = smem;
     }
-    const MulConsts mc{1u << 20, 1u << 12, 1u << 24, 0xFFFFF000u, 0xFFFFC000u};
+    const MulConsts mc{1u};
     decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap, mc);
     return cudaGetLastError();
 }
