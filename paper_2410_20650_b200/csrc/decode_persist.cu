@@ -14,6 +14,8 @@
 //    sub-range), writes exponents into the warp's padded smem tile, and the
 //    same warp then merges the unit with coalesced 16-byte stores -- so
 //    decode (ALU/shared) of some warps overlaps merge (HBM) of others.
+#include <type_traits>
+
 #include "decode_common.cuh"
 
 #ifndef NZ_PWARPS
@@ -65,6 +67,15 @@ template <>
 struct HalfBits<0> {
     using T = unsigned char;
 };
+
+// Uniform accessors over the per-precision group words (a generic lambda
+// instantiates every flavour for every precision).
+__device__ __forceinline__ uint32_t hb_raw(uint32_t v) { return v; }
+__device__ __forceinline__ uint32_t hb_raw(uint2 v) { return v.x; }
+__device__ __forceinline__ uint32_t hb_lo(uint2 v) { return v.x; }
+__device__ __forceinline__ uint32_t hb_hi(uint2 v) { return v.y; }
+__device__ __forceinline__ uint32_t hb_lo(uint32_t) { return 0; }
+__device__ __forceinline__ uint32_t hb_hi(uint32_t) { return 0; }
 
 }  // namespace
 
@@ -412,54 +423,70 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         // i.e. a per-lane base plus a compile-time stride per gi (K <= 256)
         uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
         const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
-#pragma unroll
-        for (int gi = 0; gi < G; ++gi) {
-            const uint32_t g = lane + gi * 32;
-            if (!full && g >= groups) break;
-            const HB s = pre[gi];
-            const uint32_t e = g << 3;
-            const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
-            const uint32_t e0 = er[0], e1 = er[1];
-            if constexpr (P == 7) {
-                __stcs(out + g, merge8(e0, s.x, e1, s.y));
-            } else if (fast_lossy) {
-                const uint64_t gidx = sym0 + e;
-                uint32_t b0, split;
-                if (d.log2_block != 0xFFFFFFFFu) {
-                    b0 = (uint32_t)(gidx >> d.log2_block);
-                    split = min(8u, d.block_size - ((uint32_t)gidx & (d.block_size - 1u)));
-                } else {
-                    b0 = (uint32_t)(gidx / d.block_size);
-                    split = (uint32_t)min((uint64_t)8, (uint64_t)(b0 + 1) * d.block_size - gidx);
-                }
-                const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
-                const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
-                __stcs(out + g, lossy_merge8<P>(e0, e1, (uint32_t)s, c0, c1, split));
-            } else {
-                constexpr uint32_t W = P + 1;
-                uint32_t bits;
-                if constexpr (W == 4) bits = __byte_perm(s, 0, 0x0123);
-                else if constexpr (W == 2) bits = __byte_perm((uint32_t)s, 0, 0x0144);
-                else bits = (uint32_t)s << 24;
-                const uint32_t B = d.block_size;
-                const uint64_t gidx = sym0 + e;
-                const uint64_t b0 = gidx / B;
-                const float c0 = scale_coef(__ldg(d.scales + b0));
-                const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
-                const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
-                const uint32_t ew[2] = {e0, e1};
-                uint32_t res[4];
-#pragma unroll
-                for (int qq = 0; qq < 8; ++qq) {
-                    const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
-                    const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
-                    float c = qq < (int)split ? c0 : c1;
-                    if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
-                    const uint32_t h = lossy_rebuild(item, ex, P, c);
-                    if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
-                }
-                __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
+        // one fully unrolled loop per merge flavour, chosen once per unit
+        auto merge_groups = [&](auto flavour) {
+            constexpr int M = decltype(flavour)::value;  // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path
+            uint32_t blk0 = 0, rem0 = 0;
+            if constexpr (M == 1) {
+                blk0 = (uint32_t)(sym0 >> d.log2_block);
+                rem0 = (uint32_t)sym0 & (d.block_size - 1u);
             }
+#pragma unroll
+            for (int gi = 0; gi < G; ++gi) {
+                const uint32_t g = lane + gi * 32;
+                if (!full && g >= groups) break;
+                const HB s = pre[gi];
+                const uint32_t e = g << 3;
+                const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
+                const uint32_t e0 = er[0], e1 = er[1];
+                if constexpr (M == 0) {
+                    __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                } else if constexpr (M == 1) {
+                    // power-of-two B >= 8: an aligned 8-group never straddles a block
+                    const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
+                    __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c, c, 8));
+                } else if constexpr (M == 2) {
+                    const uint64_t gidx = sym0 + e;
+                    const uint64_t b0 = gidx / d.block_size;
+                    const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * d.block_size - gidx);
+                    const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
+                    const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
+                    __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c0, c1, split));
+                } else {
+                    constexpr uint32_t W = P + 1;
+                    uint32_t bits;
+                    if constexpr (W == 4) bits = __byte_perm(hb_raw(s), 0, 0x0123);
+                    else if constexpr (W == 2) bits = __byte_perm(hb_raw(s), 0, 0x0144);
+                    else bits = hb_raw(s) << 24;
+                    const uint32_t B = d.block_size;
+                    const uint64_t gidx = sym0 + e;
+                    const uint64_t b0 = gidx / B;
+                    const float c0 = scale_coef(__ldg(d.scales + b0));
+                    const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
+                    const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+                    const uint32_t ew[2] = {e0, e1};
+                    uint32_t res[4];
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
+                        const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
+                        float c = qq < (int)split ? c0 : c1;
+                        if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
+                        const uint32_t h = lossy_rebuild(item, ex, P, c);
+                        if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
+                    }
+                    __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
+                }
+            }
+        };
+        if constexpr (P == 7) {
+            merge_groups(std::integral_constant<int, 0>{});
+        } else if (!fast_lossy) {
+            merge_groups(std::integral_constant<int, 3>{});
+        } else if (d.log2_block != 0xFFFFFFFFu) {
+            merge_groups(std::integral_constant<int, 1>{});
+        } else {
+            merge_groups(std::integral_constant<int, 2>{});
         }
         for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
             const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
