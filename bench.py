@@ -268,7 +268,7 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u8" if args.precision == 7 else "u8+f32",
+        "dtype": "u8" if args.precision == 7 else "u8+bf16",
         "data": "synthetic: random-init N(0,0.02^2) bf16 weights (torch.randn on GPU), RMSNorm=1.0",
         "config": {
             "workload": "Llama-3-8B-shaped per-layer decode" + ("" if args.precision == 7 else f" lossy k={args.precision} B={args.block}"),
@@ -287,7 +287,7 @@ def run_gpu(args):
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": "decode_tiles_kernel (one launch per layer)"},
+                     "kernel": f"{plans[0].kernel} (one launch per layer)"},
         "clocks": clocks.summary(),
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,

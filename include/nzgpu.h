@@ -145,6 +145,9 @@ int nzgpu_plan_status(nzgpu_plan plan, void* cuda_stream);
 int nzgpu_plan_free(nzgpu_plan plan);
 /* Number of kernel launches nzgpu_plan_launch / nzgpu_decompress issue. */
 int nzgpu_plan_launch_count(nzgpu_plan plan);
+/* Decode kernel nzgpu_plan_launch uses now: 0 persistent, 1 tiles, -1 none
+ * (empty plan). */
+int nzgpu_plan_kernel(nzgpu_plan plan);
 
 /* ---- host tier: the reference-facing calls (host buffers, synchronous) --- */
 /* Compress host values; returns a device blob (export its sections with

@@ -443,6 +443,12 @@ class DecodePlan:
     def launches(self) -> int:
         return int(N.lib.nzgpu_plan_launch_count(self._h))
 
+    @property
+    def kernel(self) -> str:
+        """Decode kernel the next launch uses."""
+        return {0: "decode_persist_kernel", 1: "decode_tiles_kernel"}.get(
+            int(N.lib.nzgpu_plan_kernel(self._h)), "none")
+
     def free(self) -> None:
         if self._h:
             N.lib.nzgpu_plan_free(self._h)

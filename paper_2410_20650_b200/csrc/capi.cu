@@ -787,6 +787,11 @@ int nzgpu_plan_free(nzgpu_plan p) {
 
 int nzgpu_plan_launch_count(nzgpu_plan p) { return p && p->tiles ? 1 : 0; }
 
+int nzgpu_plan_kernel(nzgpu_plan p) {
+    if (!p || !p->tiles) return -1;
+    return use_persist() && persist_fits(p->log2k, p->win_cap_unit) ? 0 : 1;
+}
+
 // ---------------------------------------------------------------- host tier
 int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint32_t block_size,
                         uint32_t chunk_symbols, uint32_t interval, nzgpu_blob* out) {

@@ -565,9 +565,13 @@ cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* de
 }
 
 bool persist_fits(int log2k, uint32_t win_cap) {
-    int dev = 0, optin = 0;
+    static thread_local int dev_cached = -1, optin = 0;  // queried once per device, not per launch
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (dev != dev_cached) {
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        dev_cached = dev;
+    }
     return persist_smem(log2k, win_cap) <= (uint32_t)optin;
 }
 
