@@ -733,14 +733,33 @@ int nzgpu_plan_create(const nzgpu_blob* blobs, uint16_t* const* d_outs, int coun
     }
     p->tiles = tiles;
     p->count = (int)descs.size();
-    // Persistent schedule: every CTA owns `upc` units of one tensor; the
-    // number of CTAs per tensor is proportional to its units (one wave).
+    // Persistent schedule: every CTA owns `upc` units of one tensor.  The
+    // per-tensor round-up must not push the CTA count past one resident wave
+    // (a second wave of a few CTAs doubles the launch time), so upc is the
+    // smallest value with sum_i ceil(units_i / upc) <= resident CTAs.
     std::vector<uint32_t> cta_prefix;
+    std::vector<uint64_t> tunits;
     uint64_t units = 0;
-    for (const DecodeDesc& d : descs) units += ceil_div(ceil_div(d.n, 1ull << p->log2k), 32);
+    for (const DecodeDesc& d : descs) {
+        tunits.push_back(ceil_div(ceil_div(d.n, 1ull << p->log2k), 32));
+        units += tunits.back();
+    }
     if (units) {
         const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
-        p->upc = (uint32_t)std::max<uint64_t>(1, ceil_div(units, resident));
+        auto ctas_for = [&](uint64_t upc) {
+            uint64_t c = 0;
+            for (uint64_t u : tunits) c += ceil_div(u, upc);
+            return c;
+        };
+        const uint64_t umax = *std::max_element(tunits.begin(), tunits.end());
+        uint64_t lo = std::max<uint64_t>(1, ceil_div(units, resident)), hi = lo;
+        while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
+        hi = std::max(lo, std::min(hi, umax));
+        while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
+            const uint64_t mid = (lo + hi) / 2;
+            if (ctas_for(mid) > resident) lo = mid + 1; else hi = mid;
+        }
+        p->upc = (uint32_t)lo;
         uint32_t ctas = 0;
         for (const DecodeDesc& d : descs) {
             cta_prefix.push_back(ctas);
