@@ -56,6 +56,13 @@ cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out
 namespace {
 // Decode schedule: the persistent warp-pipelined kernel (default) or the
 // one-tile-per-CTA kernel (NZGPU_KERNEL=tiles, or nzgpu_set_decode_kernel).
+// K3 chains are latency-bound and their byte stores cost one transaction per
+// active lane (every lane writes a different chunk): few lanes per warp,
+// spread over many SMs.
+#ifndef NZ_ENC_THREADS
+#define NZ_ENC_THREADS 32
+#endif
+
 int g_kernel = -1;  // -1: from the environment
 bool use_persist() {
     if (g_kernel < 0) {
@@ -515,7 +522,7 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
         pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
     }
     build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
-    ans_encode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
+    ans_encode_kernel<<<grid_for(b->nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(
         exps, n, chunk_syms, (uint32_t)log2k, enc, scratch, slot, plen, irregular ? nullptr : b->ckpt, b->err);
     stream_scan_kernel<<<1, 1024, 0, s>>>(plen, b->nchunks, n, chunk_syms, b->chunk_info, hdr, total);
     CK(cudaGetLastError());
@@ -1104,7 +1111,7 @@ int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* fr
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, reinterpret_cast<uint16_t*>(tmp + o_fr), nullptr,
                                          reinterpret_cast<EncSym*>(tmp + o_enc), nullptr, meta);
     // The raw coder needs no side index: checkpoints off.
-    ans_encode_kernel<<<grid_for(nchunks, 128, 1u << 30), 128, 0, s>>>(
+    ans_encode_kernel<<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(
         tmp + o_sym, n, chunk_symbols, 0u, reinterpret_cast<EncSym*>(tmp + o_enc), tmp + o_scr, slot,
         reinterpret_cast<uint32_t*>(tmp + o_plen), nullptr, meta + 4);
     stream_scan_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<uint32_t*>(tmp + o_plen), nchunks, n, chunk_symbols,

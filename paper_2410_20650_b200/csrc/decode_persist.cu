@@ -140,6 +140,26 @@ struct MulConsts {
         x = ((v) >> 20) * h_ + ((v) >> 8);                                                   \
     } while (0)
 
+// Window shift when o8 passes 32: w = w2 (a multiply by an opaque 1, kept on
+// the FMA pipe) and w2 reloaded, or (NZ_WRELOAD) both words reloaded from
+// shared memory (no register rotation for ptxas to resolve with moves).
+#ifndef NZ_WRELOAD
+#define NZ_WRELOAD 0
+#endif
+#if NZ_WRELOAD
+#define NZP_WSHIFT                                                                           \
+    "@q add.u32 %1, %1, 4;\n\t"                                                              \
+    "@q sub.u32 %2, %2, 32;\n\t"                                                             \
+    "@q ld.shared.u32 %3, [%1];\n\t"                                                         \
+    "@q ld.shared.u32 %4, [%1+4];\n\t}"
+#else
+#define NZP_WSHIFT                                                                           \
+    "@q mad.lo.u32 %3, %4, %5, 0;\n\t"                                                       \
+    "@q add.u32 %1, %1, 4;\n\t"                                                              \
+    "@q sub.u32 %2, %2, 32;\n\t"                                                             \
+    "@q ld.shared.u32 %4, [%1+4];\n\t}"
+#endif
+
 #ifndef NZ_PBYTES
 #define NZ_PBYTES 0
 #endif
@@ -179,10 +199,7 @@ struct MulConsts {
             "@r prmt.b32 %0, %0, t, 0x2105;\n\t"                                             \
             "@r add.u32 %2, %2, 8;\n\t"                                                      \
             "setp.ge.u32 q, %2, 32;\n\t"                                                     \
-            "@q mad.lo.u32 %3, %4, %5, 0;\n\t"                                                \
-            "@q add.u32 %1, %1, 4;\n\t"                                                      \
-            "@q sub.u32 %2, %2, 32;\n\t"                                                     \
-            "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
+            NZP_WSHIFT                                                                       \
             : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2) : "r"(mc.one));                  \
     } while (0)
 #endif

@@ -3,10 +3,11 @@
 //
 // K3 restates ans_encode_chunk (ans.hpp:202-225) one chunk per thread: the
 // state is a single serial chain per chunk (format-inherent: one 32-bit
-// state per 65,536-symbol chunk), so parallelism comes from chunks.  The
-// reference's `state / f` and `state % f` become a reciprocal multiply
-// (umulhi with floor(2^32/f)) plus one correction step, exact for every
-// x < 2^32 (tests/test_oracle.py::test_encoder_reciprocal_division_identity).
+// state per 65,536-symbol chunk), so parallelism comes from chunks and the
+// step is built for latency.  The reference's `state / f` and `state % f`
+// become one exact Granlund-Montgomery division, q = (x m) >> (31 + l) for
+// x < 2^31 (tests/test_oracle.py::test_encoder_exact_division_identity), and
+// x/f << 12 + x%f = x + q (4096 - f).
 // Renormalisation bytes are emitted in reverse consumption order, so they
 // are written backwards from the end of a per-chunk scratch slot; the
 // payload (ans.hpp:222-223) is then contiguous and in decoder order.
@@ -37,34 +38,67 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const uint8_t* __restri
     const uint64_t begin = c * chunk_syms;
     const uint32_t len = (uint32_t)min((uint64_t)chunk_syms, n - begin);
     uint8_t* const slot_end = scratch + (c + 1) * slot_bytes;  // 16-byte aligned
-    uint8_t* out = slot_end - 4;
     const uint8_t* src = exps + begin;
 
     uint32_t x = kStateLow;
     uint32_t emitted = 0;
-    for (uint32_t i = len; i-- > 0;) {
-        const uint32_t s = __ldg(src + i);
-        const EncSym e = enc[s];
-        if (e.freq == 0) {  // ans.hpp:210-212
-            atomicOr(err, kErrZeroFreq);
-            return;
-        }
-        // ans.hpp:214-218: at most two renormalisation bytes per symbol.
+    uint8_t* out = slot_end - 4;  // renormalisation bytes go backwards from here
+    bool bad = false;
+    const uint32_t kmask = (1u << log2_interval) - 1u;
+    // Branch-free step (lanes of a warp encode different chunks, so any
+    // data-dependent branch diverges).  The serial chain is
+    // x -> compare -> select -> IMAD.WIDE -> shift -> IMAD -> x; the byte
+    // stores and the checkpoint record hang off it.
+    auto step = [&](const EncSym& e, uint32_t i, bool may_ckpt) {
         const uint32_t limit = e.freq << 19;
-        while (x >= limit) {
-            *--out = (uint8_t)(x & 0xFFu);
-            x >>= 8;
-            ++emitted;
+        bad |= e.freq == 0;  // ans.hpp:210-212
+        // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
+        const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
+        if (n1) out[-1] = (uint8_t)x;
+        if (n2) out[-2] = (uint8_t)(x >> 8);
+        const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
+        out -= nb;
+        emitted += nb;
+        x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
+        // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
+        // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
+        const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
+        x = q * (kProbScale - e.freq) + (x + e.cum);
+        if (may_ckpt && ckpt && (i & kmask) == 0) ckpt[(begin + i) >> log2_interval] = make_uint2(x, emitted);
+    };
+    uint32_t i = len;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (!ckpt || (kmask & 15) == 15)) {
+        // 16 symbols per aligned load, walked backwards in registers; with
+        // K a multiple of 16 only the block's first symbol can be a checkpoint
+        for (const uint32_t top = len & ~15u; i > top;) {
+            --i;
+            step(enc[__ldg(src + i)], i, true);
         }
-        // ans.hpp:219: x = (x/f << 12) + x%f + cum
-        uint32_t q = __umulhi(x, e.rcp);
-        uint32_t r = x - q * e.freq;
-        if (r >= e.freq) {
-            q += 1;
-            r -= e.freq;
+        // table entries are loaded one step ahead so the shared-memory
+        // latency stays off the state chain
+        uint4 blk = i ? __ldg(reinterpret_cast<const uint4*>(src + i - 16)) : make_uint4(0, 0, 0, 0);
+        while (i) {
+            i -= 16;
+            const uint32_t w[4] = {blk.x, blk.y, blk.z, blk.w};
+            if (i) blk = __ldg(reinterpret_cast<const uint4*>(src + i - 16));
+            EncSym cur = enc[w[3] >> 24];
+#pragma unroll
+            for (int b = 15; b >= 0; --b) {
+                EncSym nxt;
+                if (b > 0) nxt = enc[(w[(b - 1) >> 2] >> (8 * ((b - 1) & 3))) & 0xFFu];
+                step(cur, i + b, b == 0);
+                if (b > 0) cur = nxt;
+            }
         }
-        x = (q << kProbBits) + r + e.cum;
-        if (ckpt && (i & ((1u << log2_interval) - 1)) == 0) ckpt[(begin + i) >> log2_interval] = make_uint2(x, emitted);
+    } else {
+        while (i) {
+            --i;
+            step(enc[__ldg(src + i)], i, true);
+        }
+    }
+    if (bad) {
+        atomicOr(err, kErrZeroFreq);
+        return;
     }
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;

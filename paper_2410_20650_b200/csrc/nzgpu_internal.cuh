@@ -54,8 +54,8 @@ constexpr uint32_t kFlagSlowLossy = kFlagHas255 | kFlagWideScale;
 struct EncSym {
     uint32_t freq;
     uint32_t cum;
-    uint32_t rcp;
-    uint32_t pad;
+    uint32_t rcp;  // m = ceil(2^(31+l) / f), l = ceil(log2 f)
+    uint32_t pad;  // shift 31 + l: x / f = (x * m) >> shift for x < 2^31
 };
 
 // Device view of one compressed tensor, as the decode kernels consume it.

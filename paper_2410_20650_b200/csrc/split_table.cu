@@ -231,8 +231,12 @@ __global__ void __launch_bounds__(256) build_table_kernel(const unsigned long lo
         EncSym e;
         e.freq = f;
         e.cum = cum[s];
-        e.rcp = f <= 1 ? 0xFFFFFFFFu : (uint32_t)((1ull << 32) / f);
-        e.pad = 0;
+        // Exact division for the encoder's x < 2^31 (Granlund-Montgomery):
+        // l = ceil(log2 f), m = ceil(2^(31+l) / f) < 2^32, x / f = (x m) >> (31+l).
+        uint32_t l = 0;
+        while ((1u << l) < (uint32_t)f) ++l;
+        e.rcp = f ? (uint32_t)(((1ull << (31 + l)) + (uint64_t)f - 1) / (uint64_t)f) : 0u;
+        e.pad = 31 + l;
         enc[s] = e;
     }
     if (s == 255 && f > 0) atomicOr(info, kFlagHas255);

@@ -305,20 +305,23 @@ def test_lossy_fp32_arithmetic_is_exact_vs_double(port):
         assert (m32 == m64).all(), s
 
 
-def test_encoder_reciprocal_division_identity():
-    """The CUDA encoder divides by f with q = umulhi(x, floor(2^32/f)) (f=1:
-    0xFFFFFFFF) plus one correction step (SURVEY probe P11).  Check it against
-    exact division over the whole encoder domain x in [f<<11, f<<19) at edge
-    bands and a dense stride for every f in 1..4095."""
-    for f in range(1, 4096):
-        rcp = 0xFFFFFFFF if f == 1 else (1 << 32) // f
-        lo, hi = f << 11, f << 19
+def test_encoder_exact_division_identity():
+    """The CUDA encoder divides by f with q = (x m) >> (31 + l), l = ceil(log2 f),
+    m = ceil(2^(31+l)/f) (Granlund-Montgomery for x < 2^31), and forms
+    (q << 12) + r + cum as x + q (4096 - f) + cum.  Check it against exact
+    division over the encoder domain x in [f<<11, f<<19) at edge bands and a
+    dense stride for every f in 1..4096."""
+    for f in range(1, 4097):
+        l = (f - 1).bit_length()
+        m = ((1 << (31 + l)) + f - 1) // f
+        assert m < (1 << 32)
+        lo, hi = f << 11, min(f << 19, 1 << 31)
         x = np.concatenate([np.arange(lo, min(lo + 4096, hi), dtype=np.uint64),
                             np.arange(max(hi - 4096, lo), hi, dtype=np.uint64),
                             np.arange(lo, hi, max(1, (hi - lo) // 2048), dtype=np.uint64)])
-        q = (x * np.uint64(rcp)) >> np.uint64(32)
-        r = x - q * np.uint64(f)
-        fix = r >= np.uint64(f)
-        q = q + fix.astype(np.uint64)
-        r = r - np.where(fix, np.uint64(f), np.uint64(0))
-        assert (q == x // np.uint64(f)).all() and (r == x % np.uint64(f)).all(), f
+        q = (x * np.uint64(m)) >> np.uint64(31 + l)
+        assert (q == x // np.uint64(f)).all(), f
+        cum = np.uint64(4096 - f)
+        assert ((x + q * np.uint64(4096 - f) + cum) == ((x // np.uint64(f)) << np.uint64(12)) + x % np.uint64(f) + cum).all()
+
+
