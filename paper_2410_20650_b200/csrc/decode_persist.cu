@@ -126,11 +126,12 @@ struct MulConsts {
 //     h' = (x >> 12) - 4096 (one LEA.HI) shared with the state update
 //     x = (v >> 20) h' + (v >> 8), lutm = lut - 2^26 (two IMADs, no LOP3);
 //   * the window shift w = w2 is a multiply by an opaque 1 (not a SEL);
-//   * both renormalisation bytes come from ONE funnel shift of the register
-//     window (the second byte is byte 1 of the same word: PRMT 0x2105).
-// Measured on 218M symbols: 246 -> 209 us.  Tried and slower: mul.hi for the
+//   * both renormalisation bytes come from ONE PRMT of the 8-byte register
+//     window, and the window moves every second step (below).
+// Measured on 218M symbols: 246 -> 200 us.  Tried and slower: mul.hi for the
 // shifts (the FMA pipe's IMAD.HI is not cheaper than the ALU shift), a
-// warp-uniform branch for the rare second byte (VOTE + reconvergence).
+// warp-uniform branch for the rare second byte (VOTE + reconvergence),
+// reloading both window words instead of rotating them (one more LDS).
 #define NZP_TRANSITION(lut, x, v)                                                            \
     do {                                                                                     \
         uint32_t a_, h_ = ((x) >> kProbBits) - kProbScale;                                   \
@@ -140,30 +141,9 @@ struct MulConsts {
         x = ((v) >> 20) * h_ + ((v) >> 8);                                                   \
     } while (0)
 
-// Window shift when o8 passes 32: w = w2 (a multiply by an opaque 1, kept on
-// the FMA pipe) and w2 reloaded, or (NZ_WRELOAD) both words reloaded from
-// shared memory (no register rotation for ptxas to resolve with moves).
-#ifndef NZ_WRELOAD
-#define NZ_WRELOAD 0
-#endif
-#if NZ_WRELOAD
-#define NZP_WSHIFT                                                                           \
-    "@q add.u32 %1, %1, 4;\n\t"                                                              \
-    "@q sub.u32 %2, %2, 32;\n\t"                                                             \
-    "@q ld.shared.u32 %3, [%1];\n\t"                                                         \
-    "@q ld.shared.u32 %4, [%1+4];\n\t}"
-#else
-#define NZP_WSHIFT                                                                           \
-    "@q mad.lo.u32 %3, %4, %5, 0;\n\t"                                                       \
-    "@q add.u32 %1, %1, 4;\n\t"                                                              \
-    "@q sub.u32 %2, %2, 32;\n\t"                                                             \
-    "@q ld.shared.u32 %4, [%1+4];\n\t}"
-#endif
-
 #ifndef NZ_PBYTES
 #define NZ_PBYTES 0
 #endif
-
 
 #if NZ_PBYTES
 // Renormalisation bytes loaded from shared memory one at a time (q is the
@@ -186,20 +166,37 @@ struct MulConsts {
             "@p2 add.u32 %1, %1, 1;\n\t}"                                                    \
             : "+r"(x), "+r"(q));                                                             \
     } while (0)
+#define NZP_STEP_A NZP_STEP
 #else
+// The window position is a PRMT selector sel = k | (k+1) << 4 (k = byte
+// offset into the 8-byte window w:w2) instead of a bit offset: one PRMT
+// extracts the next two bytes wherever they sit in the 8 bytes, so the
+// window only has to move once every TWO steps (after a shift k <= 3, two
+// steps read at most bytes k..k+3 <= 6).  Step A has no window shift, step B
+// shifts when k >= 4.
+#define NZP_RENORM_SEL                                                                       \
+    "setp.lt.u32 q, %0, 8388608;\n\t"                                                        \
+    "setp.lt.u32 r, %0, 32768;\n\t"                                                          \
+    "prmt.b32 t, %3, %4, %2;\n\t"                                                            \
+    "@q prmt.b32 %0, %0, t, 0x2104;\n\t"                                                     \
+    "@q add.u32 %2, %2, 0x11;\n\t"                                                           \
+    "@r prmt.b32 %0, %0, t, 0x2105;\n\t"                                                     \
+    "@r add.u32 %2, %2, 0x11;\n\t"
+#define NZP_STEP_A(lut, x, q, o8, w, w2, v)                                                  \
+    do {                                                                                     \
+        NZP_TRANSITION(lut, x, v);                                                           \
+        asm("{\n\t.reg .pred q, r;\n\t.reg .b32 t;\n\t" NZP_RENORM_SEL "}"                     \
+            : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
+    } while (0)
 #define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
     do {                                                                                     \
         NZP_TRANSITION(lut, x, v);                                                           \
-        asm("{\n\t.reg .pred q, r;\n\t.reg .b32 t;\n\t"                                      \
-            "setp.lt.u32 q, %0, 8388608;\n\t"                                                \
-            "setp.lt.u32 r, %0, 32768;\n\t"                                                  \
-            "shf.r.clamp.b32 t, %3, %4, %2;\n\t"                                             \
-            "@q prmt.b32 %0, %0, t, 0x2104;\n\t"                                             \
-            "@q add.u32 %2, %2, 8;\n\t"                                                      \
-            "@r prmt.b32 %0, %0, t, 0x2105;\n\t"                                             \
-            "@r add.u32 %2, %2, 8;\n\t"                                                      \
-            "setp.ge.u32 q, %2, 32;\n\t"                                                     \
-            NZP_WSHIFT                                                                       \
+        asm("{\n\t.reg .pred q, r;\n\t.reg .b32 t;\n\t" NZP_RENORM_SEL                       \
+            "setp.ge.u32 q, %2, 0x54;\n\t"                                                   \
+            "@q mad.lo.u32 %3, %4, %5, 0;\n\t"                                                \
+            "@q add.u32 %1, %1, 4;\n\t"                                                      \
+            "@q sub.u32 %2, %2, 0x44;\n\t"                                                   \
+            "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
             : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2) : "r"(mc.one));                  \
     } while (0)
 #endif
@@ -404,16 +401,16 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
 #if NZ_PBYTES
                 uint32_t q = p, o8 = 0, w0 = 0, w1 = 0;
 #else
-                uint32_t q = p & ~3u, o8 = (p & 3u) * 8;
+                uint32_t q = p & ~3u, o8 = (p & 3u) * 0x11u + 0x10u;  // PRMT selector k | (k+1) << 4
                 uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
 #endif
                 if (cur.cnt == (uint32_t)K) {
 #pragma unroll kPUnroll
                     for (uint32_t k = 0; k < (uint32_t)K / 4; ++k) {
                         uint32_t v0, v1, v2, v3;
-                        NZP_STEP(lutt, x, q, o8, w0, w1, v0);
+                        NZP_STEP_A(lutt, x, q, o8, w0, w1, v0);
                         NZP_STEP(lutt, x, q, o8, w0, w1, v1);
-                        NZP_STEP(lutt, x, q, o8, w0, w1, v2);
+                        NZP_STEP_A(lutt, x, q, o8, w0, w1, v2);
                         NZP_STEP(lutt, x, q, o8, w0, w1, v3);
                         row[k] = __byte_perm(__byte_perm(v0, v1, 0x0040), __byte_perm(v2, v3, 0x0040), 0x5410);
                     }
@@ -430,7 +427,11 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                     }
                 }
                 const uint32_t pend = wbase + (uint32_t)(cur.pe - (int64_t)wa_cur);
-                const uint32_t pos = q + (o8 >> 3);
+#if NZ_PBYTES
+                const uint32_t pos = q;
+#else
+                const uint32_t pos = q + (o8 & 0xFu);
+#endif
                 if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
             }
         }
