@@ -36,6 +36,9 @@ HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is 
 
 # Llama-3-8B: hidden 4096, ffn 14336, 32 layers, 32 heads / 8 KV heads, vocab 128256, untied.
 LLAMA3_8B = dict(hidden=4096, ffn=14336, layers=32, kv=1024, vocab=128256)
+# Llama-3-70B: hidden 8192, ffn 28672, 80 layers, 64 heads / 8 KV heads, vocab 128256 (BASELINE configs[3]).
+LLAMA3_70B = dict(hidden=8192, ffn=28672, layers=80, kv=1024, vocab=128256)
+MODELS = {"8b": LLAMA3_8B, "70b": LLAMA3_70B}
 
 
 def llama_layout(cfg=LLAMA3_8B):
@@ -50,6 +53,15 @@ def llama_layout(cfg=LLAMA3_8B):
     groups.append(("embed_tokens", [("embed_tokens", (cfg["vocab"], h), "w")]))
     groups.append(("lm_head", [("lm_head", (cfg["vocab"], h), "w"), ("norm", (h,), "norm")]))
     return groups
+
+
+def workload_name(args, world):
+    name = f"Llama-3-{args.model.upper()}-shaped per-layer decode"
+    if args.precision != 7:
+        name += f" lossy k={args.precision} B={args.block}"
+    if args.shard == "lpt":
+        name += f", full model LPT-sharded over {world} GPU(s)"
+    return name
 
 
 def numel(shape):
@@ -153,21 +165,32 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
-    # ---- synthetic model: HF Llama init N(0, 0.02^2) weights, RMSNorm = 1.0,
-    # different tensors per rank (weak scaling: each rank owns a model).
-    groups = llama_layout()
+    # ---- synthetic model: HF Llama init N(0, 0.02^2) weights, RMSNorm = 1.0.
+    # replica (weak scaling): every rank owns a whole model with its own seeds;
+    # lpt (strong scaling, C4): one model, whole tensors assigned to ranks by
+    # LPT on element count (shard.py) -- each rank compresses and decodes only
+    # its tensors, no collective on the data path.
+    from paper_2410_20650_b200.shard import lpt_assign
+
+    groups = llama_layout(MODELS[args.model])
+    flat = [numel(shape) for _, ts in groups for _, shape, _ in ts]
+    owner = lpt_assign(flat, world) if args.shard == "lpt" else [rank] * len(flat)
     blobs, plans_meta = [], []
     t0 = time.time()
     gen = torch.Generator(device=dev)
-    tensor_idx = 0
+    tensor_idx = -1
     for gname, tensors in groups:
         gb = []
         for tname, shape, kind in tensors:
+            tensor_idx += 1
+            if owner[tensor_idx] != rank:
+                continue
             n = numel(shape)
             if kind == "norm":
                 w = torch.ones(n, dtype=torch.bfloat16, device=dev)
             else:
-                gen.manual_seed(args.seed * 1000003 + rank * 10007 + tensor_idx)
+                salt = rank * 10007 if args.shard == "replica" else 0
+                gen.manual_seed(args.seed * 1000003 + salt + tensor_idx)
                 w = (torch.randn(n, device=dev, generator=gen) * 0.02).to(torch.bfloat16)
             blob = nz.DeviceBlob.compress(w, precision=args.precision, block_size=args.block,
                                           interval=args.interval, meta=nz.TensorMeta(shape))
@@ -179,8 +202,8 @@ def run_gpu(args):
                     assert torch.equal(back.view(torch.int16), w.view(torch.int16)), f"round trip {tname}"
             del w
             gb.append((tname, shape, blob))
-            tensor_idx += 1
-        blobs.append((gname, gb))
+        if gb:
+            blobs.append((gname, gb))
     torch.cuda.synchronize()
     t_compress = time.time() - t0
 
@@ -239,7 +262,12 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
 
-    value = world * bytes_algo * args.steps / t_max / 1e9
+    bytes_all = bytes_algo  # algorithmic bytes of every rank's tensors (sum over ranks)
+    if dist:
+        bt = torch.tensor([float(bytes_algo)], dtype=torch.float64, device=dev)
+        dist.all_reduce(bt, op=dist.ReduceOp.SUM)
+        bytes_all = int(bt.item())
+    value = bytes_all * args.steps / t_max / 1e9
     peak, peak_kind = load_peaks()
     achieved = bytes_algo * args.steps / kernel_time / 1e9  # per-launch bytes / launch time, aggregated
     traffic = None
@@ -266,23 +294,24 @@ def run_gpu(args):
         "warmup": args.warmup,
         "ms_per_step": round(t_max / args.steps * 1e3, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.shard == "replica" else "strong",
         "vs_baseline": None,
         "dtype": "u8" if args.precision == 7 else "u8+bf16",
         "data": "synthetic: random-init N(0,0.02^2) bf16 weights (torch.randn on GPU), RMSNorm=1.0",
         "config": {
-            "workload": "Llama-3-8B-shaped per-layer decode" + ("" if args.precision == 7 else f" lossy k={args.precision} B={args.block}"),
-            "model": "llama-3-8b (random init)",
-            "params_per_gpu": total_n,
+            "workload": workload_name(args, world),
+            "elements_rank0": total_n,
             "precision": args.precision,
+            "block_size": args.block if args.precision != 7 else None,
             "chunk_symbols": 65536,
             "checkpoint_interval": int(blobs[0][1][0][2].info.interval),
-            "launches_per_step": launches_per_step,
-            "bytes_algo_per_step_per_gpu": bytes_algo,
-            "index_bytes_per_gpu": index_bytes,
+            "launches_per_step_rank0": launches_per_step,
+            "bytes_algo_per_step": bytes_all,
+            "index_bytes_rank0": index_bytes,
             "ratio": round(2 * total_n / total_fp, 6),
-            "l2": "no flush: one step moves ~26 GB >> 126 MB L2",
-            "parallelism": f"weak dp{world}: one model replica per GPU, no collective",
+            "l2": "no flush: one step moves >= 3.4 GB per GPU >> 126 MB L2",
+            "parallelism": (f"weak dp{world}: one model replica per GPU, no collective" if args.shard == "replica"
+                            else f"strong: whole tensors LPT-sharded over {world} GPU(s), no collective"),
             "compress_s": round(t_compress, 2),
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
@@ -363,7 +392,8 @@ def cpu_sample(args):
     from oracle.oracle import Oracle
 
     gen = Oracle("port")
-    h, f, kv = 4096, 14336, 1024
+    cfg = MODELS[args.model]
+    h, f, kv = cfg["hidden"], cfg["ffn"], cfg["kv"]
     shapes = [(h, h), (kv, h), (kv, h), (h, h), (f, h), (f, h), (h, f)][: args.cpu_tensors]
     vals = [gen.gaussian_bf16(gen.derive(42, i), numel(s), 0.02) for i, s in enumerate(shapes)]
     return shapes, vals
@@ -450,14 +480,15 @@ def run_reference(args):
     algo = sum(step() for _ in range(args.steps))
     dt = time.perf_counter() - t0
     value = algo / dt / 1e9
-    sample = f"decompress of Llama-3-8B layer-0 tensors {shapes} per step, NEUZIP_THREADS={cores}"
+    sample = f"decompress of Llama-3-{args.model.upper()} layer-0 tensors {shapes} per step, NEUZIP_THREADS={cores}"
     print(json.dumps({
         "impl": "reference",
         "metric": "decode GB/s of reconstructed bf16 weights (% HBM roofline); ratio",
         "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak" if args.shard == "replica" else "strong",
         "vs_baseline": None, "dtype": "u8" if args.precision == 7 else "u8+f64", "data": "synthetic (reference rng.hpp)",
-        "config": {"workload": "Llama-3-8B-shaped per-layer decode (CPU sample: layer 0)", "precision": args.precision},
+        "config": {"workload": workload_name(args, world) + " (CPU sample: layer 0)", "precision": args.precision},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -470,6 +501,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--precision", type=int, default=7, choices=[7, 3, 1, 0])
+    ap.add_argument("--model", choices=sorted(MODELS), default="8b",
+                    help="8b: BASELINE configs[1] (default); 70b: configs[3]")
+    ap.add_argument("--shard", choices=["replica", "lpt"], default=None,
+                    help="replica: a model per GPU (weak, 8b default); lpt: one model sharded (strong, 70b default)")
     ap.add_argument("--block", type=int, default=512)
     ap.add_argument("--interval", type=int, default=0, help="checkpoint stride K (0 = auto)")
     ap.add_argument("--seed", type=int, default=42)
@@ -478,6 +513,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verify", type=int, default=1)
     args = ap.parse_args()
+    if args.shard is None:
+        args.shard = "lpt" if args.model == "70b" else "replica"
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
         run_reference(args)
