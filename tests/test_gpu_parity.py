@@ -63,6 +63,27 @@ def test_gpu_checkpoint_intervals(nz, port, interval):
     assert (nz.decompress_lossless(blob) == v).all()
 
 
+@pytest.mark.parametrize("dist", ["gaussian", "uniform", "laplace"])
+def test_gpu_chunk_sweep_streams_match_oracle(nz, port, dist):
+    """C5: chunk sizes 64 Ki .. 4 Mi symbols on the three weight
+    distributions of the sweep -- the GPU stream must be the oracle's byte for
+    byte (so the ratio is the reference's), and decode back exactly."""
+    import math
+
+    n = 1 << 22
+    if dist == "gaussian":
+        v = port.gaussian_bf16(5, n, 0.02)
+    elif dist == "uniform":
+        v = inputs.bf16_uniform(n, 7, math.sqrt(3.0) * 0.02)
+    else:
+        v = inputs.bf16_laplace(n, 11, 0.02 / math.sqrt(2.0))
+    for S in (1 << 16, 1 << 18, 1 << 20, 1 << 22):
+        blob = nz.compress_lossless(v, chunk_symbols=S)
+        f, s, sm = port.compress_lossless(v, S)
+        assert blob.stream == s and (blob.freqs == f).all(), S
+        assert (nz.decompress_lossless(blob) == v).all(), S
+
+
 def test_gpu_c1_headline_tensor(nz, port, golden):
     rec = golden["c1_4096sq_seed42"]
     v = port.gaussian_bf16(42, 4096 * 4096)

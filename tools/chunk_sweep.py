@@ -1,0 +1,72 @@
+"""C5 (BASELINE configs[4]): chunk-size sweep, ratio vs decode throughput.
+
+S in {64 Ki .. 16 Mi} exponent symbols per rANS chunk (kChunkSymbols,
+ans.hpp:33, overridden) x {Gaussian sigma=0.02, uniform +-sqrt(3)*0.02,
+Laplace b=0.02/sqrt(2)} on n = 2^24 elements.  For each
+point: compression ratio 2n / footprint (tensorstore.hpp:249-252; streams are
+byte-identical to the reference's, checked by
+tests/test_gpu_parity.py::test_gpu_chunk_sweep_streams_match_oracle) and the
+decode time of the GPU codec (CUDA events, L2 flushed between iterations:
+the 55 MB working set fits in the 126 MB L2).  Prints one JSON line per point.
+
+usage: chunk_sweep.py [n] [iters]"""
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+
+import paper_2410_20650_b200 as nz
+from tests import inputs
+
+PEAK = 6536.4
+
+
+def tensors(n):
+    g = torch.Generator(device="cuda").manual_seed(42)
+    gauss = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    uni = torch.from_numpy(inputs.bf16_uniform(n, 7, math.sqrt(3.0) * 0.02).view(np.int16)).cuda()
+    lap = torch.from_numpy(inputs.bf16_laplace(n, 11, 0.02 / math.sqrt(2.0)).view(np.int16)).cuda()
+    return {"gaussian": gauss, "uniform": uni.view(torch.bfloat16), "laplace": lap.view(torch.bfloat16)}
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
+    iters = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for dist, w in tensors(n).items():
+        for s_log in range(16, 25):
+            S = 1 << s_log
+            blob = nz.DeviceBlob.compress(w, chunk_symbols=S)
+            info = blob.info
+            out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            plan = nz.DecodePlan([blob], [out])
+            for _ in range(3):
+                plan.launch()
+            plan.status()
+            assert torch.equal(out.view(torch.int16), w.view(torch.int16)), (dist, S)
+            ts = []
+            for _ in range(iters):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                plan.launch()
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b) * 1e-3)
+            t = float(np.median(ts))
+            algo = int(info.payload_bytes) + 2 * n
+            footprint = int(info.payload_bytes) + nz.codec.nzt_header_bytes(1)
+            print(json.dumps({"dist": dist, "chunk_symbols": S, "n": n, "ratio": round(2 * n / footprint, 6),
+                              "stream_bytes": int(info.stream_len), "decode_us": round(t * 1e6, 2),
+                              "decode_gbs": round(algo / t / 1e9, 1), "frac": round(algo / t / 1e9 / PEAK, 4),
+                              "kernel": plan.kernel}), flush=True)
+            plan.free()
+            blob.free()
+
+
+main()
