@@ -36,13 +36,17 @@ namespace {
 constexpr int kPWarps = NZ_PWARPS;
 constexpr int kPUnroll = NZ_PUNROLL;
 constexpr int kPThreads = kPWarps * 32;
-constexpr uint32_t kPHeader = 128 + 2 * 8 * kPWarps;  // LUT barrier + 2 mbarriers per warp
+constexpr uint32_t kPHeader = 128;  // LUT mbarrier
 
 __host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(log2k); }
 
-// Per-warp region: exponent tile (32 padded rows) + 2 payload windows.
+// Per-warp region: its 2 mbarriers (16 B), the exponent tile (32 padded
+// rows) and 2 payload windows -- every per-warp address is the region base
+// plus a constant, so register pressure never has to rematerialise more than
+// one value.
+constexpr uint32_t kPWarpBars = 16;
 __host__ __device__ constexpr uint32_t warp_region(int log2k, uint32_t win_cap) {
-    return (unit_words(log2k) * 4 + 2 * (win_cap + 2 * (1u << log2k) + 64) + 127) & ~127u;
+    return (kPWarpBars + unit_words(log2k) * 4 + 2 * (win_cap + 2 * (1u << log2k) + 64) + 127) & ~127u;
 }
 
 __host__ __device__ constexpr uint32_t persist_smem(int log2k, uint32_t win_cap) {
@@ -316,11 +320,12 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t sbase = smem_u32(smem);
     const uint32_t lut_bar = sbase;
-    const uint32_t my_bar0 = sbase + 128 + 16 * warp;  // two mbarriers per warp
     const uint32_t lut = sbase + kPHeader;
-    const uint32_t region = sbase + kPHeader + kLutBytes + warp * warp_region(LOG2K, win_cap);
-    uint32_t* exps = reinterpret_cast<uint32_t*>(smem + (region - sbase));
-    const uint32_t winbuf0 = region + unit_words(LOG2K) * 4;
+    const uint32_t wregion = warp_region(LOG2K, win_cap);
+    const uint32_t region = sbase + kPHeader + kLutBytes + warp * wregion;
+    const uint32_t my_bar0 = region;  // two mbarriers per warp
+    uint32_t* exps = reinterpret_cast<uint32_t*>(smem + (region - sbase) + kPWarpBars);
+    const uint32_t winbuf0 = region + kPWarpBars + unit_words(LOG2K) * 4;  // 16-B aligned
     const uint32_t winstride = win_cap + 2 * K + 64;
 
     // ---- which tensor / unit range this CTA owns
@@ -345,8 +350,9 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lut_bar));
         for (int w = 0; w < kPWarps; ++w) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + 128 + 16 * w));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbase + 128 + 16 * w + 8));
+            const uint32_t r = sbase + kPHeader + kLutBytes + w * wregion;
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r + 8));
         }
         fence_mbar_init();
         if (!single) {
@@ -482,8 +488,9 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
         const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
         // one fully unrolled loop per merge flavour, chosen once per unit
-        auto merge_groups = [&](auto flavour) {
+        auto merge_groups = [&](auto flavour, auto full_unit) {
             constexpr int M = decltype(flavour)::value;  // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path
+            constexpr bool FULL = decltype(full_unit)::value;
             uint32_t blk0 = 0, rem0 = 0;
             if constexpr (M == 1) {
                 blk0 = (uint32_t)(sym0 >> d.log2_block);
@@ -492,7 +499,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
 #pragma unroll
             for (int gi = 0; gi < G; ++gi) {
                 const uint32_t g = lane + gi * 32;
-                if (!full && g >= groups) break;
+                if (!FULL && g >= groups) break;
                 const HB s = pre[gi];
                 const uint32_t e = g << 3;
                 const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
@@ -537,14 +544,18 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                 }
             }
         };
+        auto merge_unit = [&](auto flavour) {
+            if (full) merge_groups(flavour, std::true_type{});
+            else merge_groups(flavour, std::false_type{});
+        };
         if constexpr (P == 7) {
-            merge_groups(std::integral_constant<int, 0>{});
+            merge_unit(std::integral_constant<int, 0>{});
         } else if (!fast_lossy) {
-            merge_groups(std::integral_constant<int, 3>{});
+            merge_unit(std::integral_constant<int, 3>{});
         } else if (d.log2_block != 0xFFFFFFFFu) {
-            merge_groups(std::integral_constant<int, 1>{});
+            merge_unit(std::integral_constant<int, 1>{});
         } else {
-            merge_groups(std::integral_constant<int, 2>{});
+            merge_unit(std::integral_constant<int, 2>{});
         }
         for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
             const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
