@@ -244,7 +244,7 @@ struct MulConsts {
 // state/position, symbol count) and the unit's payload window.
 struct LaneJob {
     uint32_t x0, xe, cnt, err;
-    int64_t p0, pe;  // absolute stream offsets
+    uint32_t p0, pe;  // stream offsets relative to the unit's first chunk (< 2^32 apart)
 };
 
 // Raw index records of a lane's sub-range, loaded one unit ahead so the
@@ -268,9 +268,9 @@ __device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint
 
 template <int LOG2K>
 __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uint32_t nsub, bool single,
-                                            const RawRec& raw) {
+                                            const RawRec& raw, uint32_t lo0) {
     constexpr int K = 1 << LOG2K;
-    LaneJob L{kStateLow, kStateLow, 0u, 0u, 0, 0};
+    LaneJob L{kStateLow, kStateLow, 0u, 0u, 0u, 0u};
     if (j >= nsub) return L;
     uint32_t ch, jin;
     sub_to_chunk(d, LOG2K, j, ch, jin);
@@ -290,7 +290,7 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
     }
     if (single) {
         if (jin == 0 && len >= 4 && (L.x0 != kStateLow || len != 4)) L.err |= L.x0 < kStateLow ? kErrTruncated : kErrDesync;
-        L.p0 = L.pe = (int64_t)(off + limit);
+        L.p0 = L.pe = ci.x - lo0 + limit;
         return L;
     }
     const uint2 rec = raw.rec;
@@ -300,8 +300,9 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
     if (jin != 0) L.x0 = rec.x;
     L.xe = end.x;
     if (e_start > limit || end.y > limit) L.err |= kErrDesync;
-    L.p0 = (int64_t)(off + limit - min(e_start, limit));
-    L.pe = (int64_t)(off + limit - min(end.y, limit));
+    const uint32_t rel = ci.x - lo0 + limit;  // chunk offsets of one unit differ by < 2^32
+    L.p0 = rel - min(e_start, limit);
+    L.pe = rel - min(end.y, limit);
     if (L.pe < L.p0) L.err |= kErrDesync;
     return L;
 }
@@ -369,28 +370,32 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     // ---- per-warp pipeline over units u = ubeg + warp + i * kPWarps
     uint32_t err = 0;
     // stage unit u into buffer b: returns this lane's job, issues the window TMA
-    auto stage = [&](uint32_t u, int b, uint64_t& wa_out, const RawRec& raw) -> LaneJob {
-        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw);
-        const int64_t a = __shfl_sync(0xFFFFFFFFu, L.p0, 0);
+    // Positions are 32-bit offsets from the unit's first chunk (lane 0's,
+    // whose 64-bit offset only lane 0 needs, for the TMA source).
+    auto stage = [&](uint32_t u, int b, uint32_t& wa_out, const RawRec& raw) -> LaneJob {
+        const uint32_t lo0 = __shfl_sync(0xFFFFFFFFu, raw.ci.x, 0);
+        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw, lo0);
+        const uint32_t a = __shfl_sync(0xFFFFFFFFu, L.p0, 0);
         const uint32_t last_lane = min(31u, nsub - u * 32 - 1);
-        const int64_t e = __shfl_sync(0xFFFFFFFFu, L.pe, last_lane);
-        const uint64_t wa = (uint64_t)a & ~15ull;
-        uint64_t bytes = single ? 0 : (((uint64_t)e + 15) & ~15ull) - wa;
-        if (!single && ((uint64_t)e < (uint64_t)a || bytes > win_cap)) {
+        const uint32_t e = __shfl_sync(0xFFFFFFFFu, L.pe, last_lane);
+        const uint32_t wa = a - ((lo0 + a) & 15u);             // 16-B aligned absolute start
+        const uint32_t eb = e + ((0u - (lo0 + e)) & 15u);      // 16-B aligned absolute end
+        uint32_t bytes = single ? 0u : eb - wa;
+        if (!single && (e < a || bytes > win_cap)) {
             L.err |= kErrDesync;
             bytes = 0;
         }
         if (!single && lane == 0) {
             const uint32_t bar = my_bar0 + 8 * b;
-            p_expect_tx(bar, (uint32_t)bytes);
-            if (bytes) p_bulk(winbuf0 + b * winstride, d.stream + wa, (uint32_t)bytes, bar);
+            p_expect_tx(bar, bytes);
+            if (bytes) p_bulk(winbuf0 + b * winstride, d.stream + (int64_t)chunk_offset(raw.ci) + (int32_t)wa, bytes, bar);
         }
         wa_out = wa;
         return L;
     };
 
     uint32_t u = ubeg + warp;
-    uint64_t wa_cur = 0, wa_nxt = 0;
+    uint32_t wa_cur = 0, wa_nxt = 0;
     LaneJob cur{}, nxt{};
     RawRec raw_n{};  // index records of unit u + kPWarps (loaded one iteration early)
     if (u < uend) {
@@ -438,7 +443,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
             if (!cur.err && cur.cnt) {
                 const uint32_t wbase = winbuf0 + b * winstride + t2;
                 uint32_t x = cur.x0;
-                const uint32_t p = wbase + (uint32_t)(cur.p0 - (int64_t)wa_cur);
+                const uint32_t p = wbase + (cur.p0 - wa_cur);
 #if NZ_PBYTES
                 uint32_t q = p, o8 = 0, w0 = 0, w1 = 0;
 #elif NZ_FLO
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                         }
                     }
                 }
-                const uint32_t pend = wbase + (uint32_t)(cur.pe - (int64_t)wa_cur);
+                const uint32_t pend = wbase + (cur.pe - wa_cur);
 #if NZ_PBYTES
                 const uint32_t pos = q;
 #elif NZ_FLO
