@@ -44,7 +44,8 @@ typedef enum nzgpu_status {
     NZGPU_FORMAT_TABLE = 6,     /* FormatError "does not sum to 4096" (ans.hpp:100) */
     NZGPU_CUDA_ERROR = 7,       /* CUDA runtime failure                          */
     NZGPU_OUT_OF_MEMORY = 8,
-    NZGPU_NO_DEVICE = 9         /* no CUDA device: the library never falls back to the CPU */
+    NZGPU_NO_DEVICE = 9,        /* no CUDA device: the library never falls back to the CPU */
+    NZGPU_CHECKSUM = 10         /* ChecksumError "nzt: checksum failure" (tensorstore.hpp:462) */
 } nzgpu_status;
 
 #define NZGPU_LOSSLESS 7            /* kLosslessPrecision, tensorstore.hpp:36 */
@@ -186,6 +187,28 @@ int nzgpu_lossy_roundtrip_host(const uint16_t* values, const uint8_t* scales, ui
  * {0,1,3,7}; packed holds ceil(n(k+1)/8) MSB-first bytes. */
 int nzgpu_pack_host(const uint8_t* items, uint64_t n, int k, uint8_t* packed);
 int nzgpu_unpack_host(const uint8_t* packed, uint64_t nbytes, int k, uint64_t n, uint8_t* items);
+
+/* ---- CRC-32 and the NZT container (tensorstore.hpp:289-477, crc32.hpp) -- */
+/* CRC-32 (IEEE, reflected 0xEDB88320, init/xorout 0xFFFFFFFF: crc32.hpp:26-43)
+ * of a device byte range, computed on the GPU (block CRCs joined by GF(2)
+ * multiplication).  Synchronises `cuda_stream`. */
+int nzgpu_crc32(const void* d_data, uint64_t len, void* cuda_stream, uint32_t* crc);
+/* Same over host buffers (staged through the GPU); `count` sections are
+ * checksummed as one concatenated byte string. */
+int nzgpu_crc32_host(const void* data, uint64_t len, uint32_t* crc);
+int nzgpu_crc32_host_sections(const void* const* ptrs, const uint64_t* lens, int count, uint32_t* crc);
+/* Size in bytes of the NZT file of a blob with `ndim` dimensions. */
+int nzgpu_blob_nzt_size(nzgpu_blob blob, int ndim, uint64_t* size);
+/* write_nzt (tensorstore.hpp:352-376) of a device blob into a host buffer:
+ * sections copied D2H, CRC computed on the GPU.  shape must multiply to n. */
+int nzgpu_blob_write_nzt(nzgpu_blob blob, const uint64_t* shape, int ndim, uint8_t* out, uint64_t cap,
+                         uint64_t* written);
+/* read_nzt (tensorstore.hpp:403-477) from a host buffer into a new device
+ * blob: framing and lengths validated first, CRC checked on the GPU
+ * (NZGPU_CHECKSUM), then table/stream validated and the checkpoint index
+ * built as nzgpu_blob_import does.  shape: 8 u64 (may be NULL). */
+int nzgpu_blob_read_nzt(const uint8_t* data, uint64_t len, uint32_t interval, void* cuda_stream, nzgpu_blob* out,
+                        uint64_t* shape, int* ndim);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,8 @@ class Oracle:
             self._free_prepared = fn("free_prepared", None, [_vp])
             self._entropy = fn("entropy_report", None, [_vp, _u64, _vp])
             self._nzt = fn("write_nzt_lossless", _i64, [_vp, _vp, _int, _vp, _u64])
+            self._nzt_lossy = fn("write_nzt_lossy", _i64, [_vp, _vp, _int, _int, _u32, _vp, _u64])
+            self._read_nzt = fn("read_nzt", _int, [_vp, _u64, _vp, _u64, _vp])
 
     # -- tables / coder -------------------------------------------------
     def build_table(self, counts) -> np.ndarray:
@@ -286,6 +288,25 @@ class Oracle:
         out = np.zeros(5, np.float64)
         self._entropy(_p(v), v.size, _p(out))
         return out
+
+    def write_nzt_lossy(self, values, shape, k: int, block: int = 512) -> bytes:
+        v = np.ascontiguousarray(values, dtype=np.uint16)
+        dims = np.asarray(shape, dtype=np.uint64)
+        out = np.zeros(v.size * 4 + 4096, np.uint8)
+        n = self._nzt_lossy(_p(v), _p(dims), dims.size, k, block, _p(out), out.size)
+        if n < 0:
+            raise OracleError(n, "write_nzt")
+        return out[:n].tobytes()
+
+    def read_nzt(self, data: bytes, max_n: int):
+        """The reference's read_nzt + decompress: (status, values); status 0 or
+        the exception class code (-2 truncated, -3 desync, -4 length/format,
+        -6 table, -7 checksum)."""
+        buf = np.frombuffer(data, np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+        out = np.zeros(max(max_n, 1), np.uint16)
+        n = np.zeros(1, np.uint64)
+        rc = self._read_nzt(_p(buf), len(data), _p(out), out.size, _p(n))
+        return rc, out[: int(n[0])]
 
     def write_nzt_lossless(self, values, shape) -> bytes:
         v = np.ascontiguousarray(values, dtype=np.uint16)

@@ -30,10 +30,11 @@ using namespace neuzip;
 namespace {
 
 constexpr int kOk = 0, kInvalid = -1, kTruncated = -2, kDesync = -3, kLength = -4,
-              kNonFinite = -5, kBadTable = -6;
+              kNonFinite = -5, kBadTable = -6, kChecksum = -7;
 
 int classify(const std::exception& e) {
     if (dynamic_cast<const NonFiniteError*>(&e)) return kNonFinite;
+    if (dynamic_cast<const ChecksumError*>(&e)) return kChecksum;
     if (dynamic_cast<const FormatError*>(&e)) {
         const std::string what = e.what();
         if (what.find("truncated") != std::string::npos) return kTruncated;
@@ -262,6 +263,42 @@ std::int64_t ref_write_nzt_lossless(const std::uint16_t* values, const std::uint
     if (s.size() > cap) return kInvalid;
     std::memcpy(out, s.data(), s.size());
     return static_cast<std::int64_t>(s.size());
+    GUARD_END
+}
+
+// write_nzt of a lossy blob (tensorstore.hpp:382-390); returns bytes written.
+std::int64_t ref_write_nzt_lossy(const std::uint16_t* values, const std::uint64_t* shape, int ndim, int k,
+                                 std::uint32_t block, std::uint8_t* out, std::uint64_t cap) {
+    GUARD_BEGIN
+    std::uint64_t n = 1;
+    std::vector<std::uint64_t> dims(shape, shape + ndim);
+    for (auto d : dims) n *= d;
+    std::ostringstream os(std::ios::binary);
+    write_nzt(Blob(compress_lossy(as_bf16(values, n), k, block, TensorMeta{dims})), os);
+    const std::string s = os.str();
+    if (s.size() > cap) return kInvalid;
+    std::memcpy(out, s.data(), s.size());
+    return static_cast<std::int64_t>(s.size());
+    GUARD_END
+}
+
+// read_nzt + decompress (tensorstore.hpp:403-477, :112-125, :215-238):
+// 0 and the values on success, else the reference's exception class.
+int ref_read_nzt(const std::uint8_t* data, std::uint64_t len, std::uint16_t* values, std::uint64_t cap_n,
+                 std::uint64_t* n_out) {
+    GUARD_BEGIN
+    std::istringstream is(std::string(reinterpret_cast<const char*>(data), len), std::ios::binary);
+    const Blob blob = read_nzt(is);
+    const std::vector<Bf16> out = std::visit(
+        [](const auto& b) {
+            if constexpr (std::is_same_v<std::decay_t<decltype(b)>, LosslessBlob>) return decompress_lossless(b);
+            else return decompress_lossy(b);
+        },
+        blob);
+    if (out.size() > cap_n) return kInvalid;
+    std::memcpy(values, out.data(), out.size() * 2);
+    *n_out = out.size();
+    return kOk;
     GUARD_END
 }
 

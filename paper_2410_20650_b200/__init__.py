@@ -26,6 +26,7 @@ from .codec import (  # noqa: F401
     build_table,
     compress_lossless,
     compress_lossy,
+    crc32,
     decompress_batch,
     decompress_lossless,
     decompress_lossy,
@@ -36,7 +37,9 @@ from .codec import (  # noqa: F401
     lossy_roundtrip,
     pack_signed_mantissas,
     ratio,
+    read_nzt,
     unpack_signed_mantissas,
+    write_nzt,
 )
 
 LIB_PATH = nzgpu.LIB_PATH

@@ -235,6 +235,74 @@ class DeviceBlob:
                          mant[: i.mantissa_len], idx)
 
 
+    # -- NZT container (tensorstore.hpp:289-477)
+    def to_nzt(self, shape=None) -> bytes:
+        """write_nzt of this blob: sections D2H, CRC-32 on the GPU."""
+        shape = tuple(shape if shape is not None else (self.meta.shape if self.meta else (self.n,)))
+        size = C.c_uint64()
+        N.check(N.lib.nzgpu_blob_nzt_size(self._h, len(shape), C.byref(size)), "nzt size")
+        out = np.zeros(size.value, np.uint8)
+        dims = (C.c_uint64 * len(shape))(*shape)
+        written = C.c_uint64()
+        N.check(N.lib.nzgpu_blob_write_nzt(self._h, dims, len(shape), _ptr(out), size.value, C.byref(written)),
+                "write_nzt")
+        return out[: written.value].tobytes()
+
+    @classmethod
+    def from_nzt(cls, data: bytes, interval: int = 0) -> "DeviceBlob":
+        """read_nzt into a device blob (CRC checked on the GPU)."""
+        buf = np.frombuffer(data, np.uint8)
+        h = C.c_void_p()
+        dims = (C.c_uint64 * 8)()
+        nd = C.c_int()
+        N.check(N.lib.nzgpu_blob_read_nzt(_ptr(buf) if buf.size else None, buf.size, interval, None, C.byref(h),
+                                          dims, C.byref(nd)), "read_nzt")
+        return cls(h, TensorMeta(tuple(int(dims[i]) for i in range(nd.value))))
+
+
+def crc32(*sections) -> int:
+    """crc32.hpp:38-42 over the concatenation of host byte sections,
+    computed on the GPU."""
+    arrs = [np.ascontiguousarray(np.frombuffer(bytes(s), np.uint8) if isinstance(s, (bytes, bytearray, memoryview))
+                                 else np.asarray(s).view(np.uint8).reshape(-1)) for s in sections]
+    ptrs = (C.c_void_p * max(len(arrs), 1))(*[_ptr(a) if a.size else None for a in arrs])
+    lens = (C.c_uint64 * max(len(arrs), 1))(*[a.size for a in arrs])
+    out = C.c_uint32()
+    N.check(N.lib.nzgpu_crc32_host_sections(ptrs, lens, len(arrs), C.byref(out)), "crc32")
+    return int(out.value)
+
+
+def write_nzt(blob: Blob) -> bytes:
+    """write_nzt (tensorstore.hpp:352-376) of a host blob; the CRC is computed
+    on the GPU.  Byte-identical to the reference's file."""
+    import struct
+
+    blob.meta.validate()
+    lossless = isinstance(blob, LosslessBlob)
+    prec = kLosslessPrecision if lossless else int(blob.precision)
+    block = 0 if lossless else int(blob.block_size)
+    table = np.ascontiguousarray(blob.freqs, dtype="<u2").tobytes()
+    scales = b"" if lossless else np.ascontiguousarray(blob.scales, np.uint8).tobytes()
+    stream = bytes(blob.stream)
+    sm = np.ascontiguousarray(blob.signmant, np.uint8).tobytes()
+    crc = crc32(table, scales, stream, sm)
+    head = b"NZT1" + struct.pack("<BBIB", 1, prec, block, len(blob.meta.shape))
+    head += b"".join(struct.pack("<Q", d) for d in blob.meta.shape)
+    return b"".join([head, table, struct.pack("<I", len(scales)), scales, struct.pack("<Q", len(stream)), stream,
+                     struct.pack("<Q", len(sm)), sm, struct.pack("<I", crc)])
+
+
+def read_nzt(data: bytes) -> Blob:
+    """read_nzt (tensorstore.hpp:403-477): framing, CRC (on the GPU;
+    ChecksumError), table and stream validation; returns the host blob with
+    the GPU checkpoint index attached."""
+    db = DeviceBlob.from_nzt(data)
+    try:
+        return db.to_host()
+    finally:
+        db.free()
+
+
 def _stream_ptr(stream):
     if stream is None:
         try:

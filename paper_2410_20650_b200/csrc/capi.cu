@@ -51,6 +51,10 @@ cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* de
 uint32_t persist_resident_ctas(int log2k, uint32_t win_cap);
 bool persist_fits(int log2k, uint32_t win_cap);
 cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
+// crc32.cu
+cudaError_t crc_raw_device(const uint8_t* d, uint64_t len, cudaStream_t s, uint32_t* raw);
+uint32_t crc_combine_raw(uint32_t raw_a, uint32_t raw_b, uint64_t len_b);
+uint32_t crc_finalize(uint32_t raw, uint64_t len);
 }  // namespace nzgpu
 
 namespace {
@@ -601,6 +605,7 @@ const char* nzgpu_status_string(int status) {
         case NZGPU_CUDA_ERROR: return "CUDA error";
         case NZGPU_OUT_OF_MEMORY: return "out of device memory";
         case NZGPU_NO_DEVICE: return "no CUDA device (the codec has no CPU fallback)";
+        case NZGPU_CHECKSUM: return "nzt: checksum failure";
         default: return "unknown status";
     }
 }
@@ -1230,6 +1235,214 @@ int nzgpu_lossy_roundtrip_host(const uint16_t* values, const uint8_t* scales, ui
     CK(cudaMemcpyAsync(out, dout, n * 2, cudaMemcpyDeviceToHost, sg.s));
     CK(cudaFreeAsync(tmp, sg.s));
     CK(cudaStreamSynchronize(sg.s));
+    return NZGPU_OK;
+}
+
+
+// --------------------------------------------------------- CRC-32 / NZT --
+int nzgpu_crc32(const void* d_data, uint64_t len, void* cuda_stream, uint32_t* crc) {
+    if (!crc || (len && !d_data)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg(cuda_stream);
+    uint32_t raw = 0;
+    CK(crc_raw_device(static_cast<const uint8_t*>(d_data), len, sg.s, &raw));
+    *crc = crc_finalize(raw, len);
+    return NZGPU_OK;
+}
+
+int nzgpu_crc32_host_sections(const void* const* ptrs, const uint64_t* lens, int count, uint32_t* crc) {
+    if (!crc || count < 0 || (count && (!ptrs || !lens))) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg{StreamGuard::Own{}};
+    constexpr uint64_t kPiece = 256ull << 20;  // staging bound
+    uint64_t cap = 0, total = 0;
+    for (int i = 0; i < count; ++i) cap = std::max(cap, std::min(lens[i], kPiece));
+    uint8_t* d = nullptr;
+    if (cap) CK(cudaMallocAsync(&d, cap, sg.s));
+    uint32_t raw_all = 0;
+    int rc = NZGPU_OK;
+    for (int i = 0; i < count && rc == NZGPU_OK; ++i) {
+        if (lens[i] && !ptrs[i]) {
+            rc = NZGPU_INVALID_ARGUMENT;
+            break;
+        }
+        for (uint64_t off = 0; off < lens[i]; off += kPiece) {
+            const uint64_t m = std::min(kPiece, lens[i] - off);
+            cudaError_t e = cudaMemcpyAsync(d, static_cast<const uint8_t*>(ptrs[i]) + off, m,
+                                            cudaMemcpyHostToDevice, sg.s);
+            uint32_t raw = 0;
+            if (e == cudaSuccess) e = crc_raw_device(d, m, sg.s, &raw);
+            if (e != cudaSuccess) {
+                rc = fail_cuda(e, "crc32 host sections");
+                break;
+            }
+            raw_all = crc_combine_raw(raw_all, raw, m);
+            total += m;
+        }
+    }
+    if (d) cudaFreeAsync(d, sg.s);
+    cudaStreamSynchronize(sg.s);
+    if (rc) return rc;
+    *crc = crc_finalize(raw_all, total);
+    return NZGPU_OK;
+}
+
+int nzgpu_crc32_host(const void* data, uint64_t len, uint32_t* crc) {
+    return nzgpu_crc32_host_sections(&data, &len, 1, crc);
+}
+
+namespace {
+// NZT framing (tensorstore.hpp:289-300): "NZT1" u8 version u8 precision
+// u32 block u8 ndim u64*ndim shape | 512 table | u32 scales_len scales |
+// u64 exp_len stream | u64 signmant_len mantissas | u32 crc.
+uint64_t nzt_size(uint64_t ndim, uint64_t scales, uint64_t stream, uint64_t mant) {
+    return 4 + 1 + 1 + 4 + 1 + 8 * ndim + 512 + 4 + scales + 8 + stream + 8 + mant + 4;
+}
+uint8_t* put_le(uint8_t* p, uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) *p++ = (uint8_t)(v >> (8 * i));
+    return p;
+}
+uint64_t get_le(const uint8_t* p, int bytes) {
+    uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+}  // namespace
+
+int nzgpu_blob_nzt_size(nzgpu_blob b, int ndim, uint64_t* size) {
+    if (!b || !size || ndim < 1 || ndim > 8) return NZGPU_INVALID_ARGUMENT;
+    *size = nzt_size((uint64_t)ndim, b->scales_len, b->stream_len, b->mant_len);
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_write_nzt(nzgpu_blob b, const uint64_t* shape, int ndim, uint8_t* out, uint64_t cap,
+                         uint64_t* written) {
+    if (!b || !shape || !out || ndim < 1 || ndim > 8) return NZGPU_INVALID_ARGUMENT;
+    uint64_t n = 1;
+    for (int i = 0; i < ndim; ++i) {
+        if (shape[i] == 0) return NZGPU_INVALID_ARGUMENT;  // TensorMeta::validate
+        n *= shape[i];
+    }
+    if (n != b->n) return NZGPU_INVALID_ARGUMENT;
+    const uint64_t size = nzt_size((uint64_t)ndim, b->scales_len, b->stream_len, b->mant_len);
+    if (cap < size) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg{StreamGuard::Own{}};
+    CK(cudaDeviceSynchronize());
+    // CRC over table | scales | stream | mantissas, each section on the GPU
+    const uint8_t* sec[4] = {reinterpret_cast<const uint8_t*>(b->freqs), b->scales, b->stream, b->mant};
+    const uint64_t len[4] = {512, b->scales_len, b->stream_len, b->mant_len};
+    uint32_t raw_all = 0;
+    uint64_t total = 0;
+    for (int i = 0; i < 4; ++i) {
+        uint32_t raw = 0;
+        CK(crc_raw_device(sec[i], len[i], sg.s, &raw));
+        raw_all = crc_combine_raw(raw_all, raw, len[i]);
+        total += len[i];
+    }
+    const uint32_t crc = crc_finalize(raw_all, total);
+    uint8_t* p = out;
+    std::memcpy(p, "NZT1", 4);
+    p += 4;
+    p = put_le(p, 1, 1);
+    p = put_le(p, (uint64_t)b->precision, 1);
+    p = put_le(p, b->precision == 7 ? 0 : b->block, 4);
+    p = put_le(p, (uint64_t)ndim, 1);
+    for (int i = 0; i < ndim; ++i) p = put_le(p, shape[i], 8);
+    CK(cudaMemcpy(p, b->freqs, 512, cudaMemcpyDeviceToHost));  // LE u16 table
+    p += 512;
+    p = put_le(p, b->scales_len, 4);
+    if (b->scales_len) CK(cudaMemcpy(p, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
+    p += b->scales_len;
+    p = put_le(p, b->stream_len, 8);
+    if (b->stream_len) CK(cudaMemcpy(p, b->stream, b->stream_len, cudaMemcpyDeviceToHost));
+    p += b->stream_len;
+    p = put_le(p, b->mant_len, 8);
+    if (b->mant_len) CK(cudaMemcpy(p, b->mant, b->mant_len, cudaMemcpyDeviceToHost));
+    p += b->mant_len;
+    p = put_le(p, crc, 4);
+    if (written) *written = (uint64_t)(p - out);
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_read_nzt(const uint8_t* data, uint64_t len, uint32_t interval, void* cuda_stream, nzgpu_blob* out,
+                        uint64_t* shape, int* ndim_out) {
+    if (!out || (len && !data)) return NZGPU_INVALID_ARGUMENT;
+    *out = nullptr;
+    // read_nzt (tensorstore.hpp:403-477): every length is validated against
+    // the element count before anything is copied.
+    uint64_t pos = 0;
+    auto need = [&](uint64_t k) { return len - pos >= k; };
+    if (!need(4) || std::memcmp(data, "NZT1", 4) != 0) {
+        std::snprintf(g_msg, sizeof(g_msg), "nzt: bad magic");
+        return NZGPU_FORMAT_LENGTH;
+    }
+    pos = 4;
+    if (!need(7)) return NZGPU_FORMAT_TRUNCATED;  // "unexpected end of file"
+    const uint64_t version = data[pos], precision = data[pos + 1];
+    const uint64_t block = get_le(data + pos + 2, 4), ndim = data[pos + 6];
+    pos += 7;
+    if (version != 1 || !valid_precision((int)precision) || ndim == 0 || ndim > 8) return NZGPU_FORMAT_LENGTH;
+    if (!need(8 * ndim)) return NZGPU_FORMAT_TRUNCATED;
+    uint64_t n = 1, dims[8];
+    for (uint64_t i = 0; i < ndim; ++i) {
+        dims[i] = get_le(data + pos + 8 * i, 8);
+        if (dims[i] == 0 || dims[i] > (1ull << 40) / n) return NZGPU_FORMAT_LENGTH;
+        n *= dims[i];
+    }
+    pos += 8 * ndim;
+    if (precision == 7 ? block != 0 : block == 0) return NZGPU_FORMAT_LENGTH;
+    const uint64_t exp_scales = precision == 7 ? 0 : (n + block - 1) / block;
+    const uint64_t exp_mant = mant_bytes(n, (int)precision);
+    const uint64_t cap = 2 * n + 16 * ((n + kDefaultChunk - 1) / kDefaultChunk) + 64;
+    if (!need(512 + 4)) return NZGPU_FORMAT_TRUNCATED;
+    const uint8_t* table = data + pos;
+    pos += 512;
+    const uint64_t scales_len = get_le(data + pos, 4);
+    pos += 4;
+    if (scales_len != exp_scales) return NZGPU_FORMAT_LENGTH;
+    if (!need(scales_len + 8)) return NZGPU_FORMAT_TRUNCATED;
+    const uint8_t* scales = data + pos;
+    pos += scales_len;
+    const uint64_t exp_len = get_le(data + pos, 8);
+    pos += 8;
+    if (exp_len > cap) return NZGPU_FORMAT_LENGTH;
+    if (!need(exp_len + 8)) return NZGPU_FORMAT_TRUNCATED;
+    const uint8_t* stream = data + pos;
+    pos += exp_len;
+    const uint64_t mlen = get_le(data + pos, 8);
+    pos += 8;
+    if (mlen != exp_mant) return NZGPU_FORMAT_LENGTH;
+    if (!need(mlen + 4)) return NZGPU_FORMAT_TRUNCATED;
+    const uint8_t* mant = data + pos;
+    pos += mlen;
+    const uint32_t stored = (uint32_t)get_le(data + pos, 4);
+    // CRC over the four payload sections on the GPU (tensorstore.hpp:449-457)
+    uint32_t crc = 0;
+    {
+        const void* ptrs[4] = {table, scales, stream, mant};
+        const uint64_t lens[4] = {512, scales_len, exp_len, mlen};
+        if (int rc = nzgpu_crc32_host_sections(ptrs, lens, 4, &crc)) return rc;
+    }
+    if (crc != stored) return NZGPU_CHECKSUM;
+    // deserialize_table / deserialize_stream / count check: the import path
+    uint16_t freqs[256];
+    std::memcpy(freqs, table, 512);  // little-endian host
+    nzgpu_host_tensor t{};
+    t.n = n;
+    t.precision = (int32_t)precision;
+    t.block_size = (uint32_t)block;
+    t.freqs = freqs;
+    t.stream = stream;
+    t.stream_len = exp_len;
+    t.mantissas = mant;
+    t.mantissa_len = mlen;
+    t.scales = precision == 7 ? nullptr : scales;
+    t.scales_len = scales_len;
+    if (int rc = nzgpu_blob_import(&t, interval, cuda_stream, out)) return rc;
+    if (shape)
+        for (uint64_t i = 0; i < ndim; ++i) shape[i] = dims[i];
+    if (ndim_out) *ndim_out = (int)ndim;
     return NZGPU_OK;
 }
 

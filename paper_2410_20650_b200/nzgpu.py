@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, os.path.basename(os.environ.get("NZGPU_LIB", "libn
 
 OK, INVALID_ARGUMENT, FORMAT_TRUNCATED, FORMAT_DESYNC, FORMAT_LENGTH = 0, 1, 2, 3, 4
 NONFINITE, FORMAT_TABLE, CUDA_ERROR, OUT_OF_MEMORY, NO_DEVICE = 5, 6, 7, 8, 9
+CHECKSUM = 10
 LOSSLESS = 7
 DEFAULT_BLOCK = 512
 DEFAULT_CHUNK = 65536
@@ -58,6 +59,10 @@ def _raise(rc: int, what: str) -> None:
         raise ValueError(msg)  # std::invalid_argument
     if rc in (FORMAT_TRUNCATED, FORMAT_DESYNC, FORMAT_LENGTH, FORMAT_TABLE):
         err = FormatError(msg)
+        err.status = rc
+        raise err
+    if rc == CHECKSUM:
+        err = ChecksumError(msg)
         err.status = rc
         raise err
     if rc == NONFINITE:
@@ -138,6 +143,12 @@ SIGNATURES = {
     "nzgpu_lossy_roundtrip_host": (_i, [_vp, _vp, _u64, _i, _vp]),
     "nzgpu_pack_host": (_i, [_vp, _u64, _i, _vp]),
     "nzgpu_unpack_host": (_i, [_vp, _u64, _i, _u64, _vp]),
+    "nzgpu_crc32": (_i, [_vp, _u64, _vp, _p(_u32)]),
+    "nzgpu_crc32_host": (_i, [_vp, _u64, _p(_u32)]),
+    "nzgpu_crc32_host_sections": (_i, [_p(_vp), _p(_u64), _i, _p(_u32)]),
+    "nzgpu_blob_nzt_size": (_i, [_vp, _i, _p(_u64)]),
+    "nzgpu_blob_write_nzt": (_i, [_vp, _p(_u64), _i, _vp, _u64, _p(_u64)]),
+    "nzgpu_blob_read_nzt": (_i, [_vp, _u64, _u32, _vp, _p(_vp), _p(_u64), _p(_i)]),
 }
 
 

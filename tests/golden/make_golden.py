@@ -93,6 +93,13 @@ def main() -> None:
             "stream_len": len(st), "stream_sha": sha(st), "packed_sha": sha(pk), "scales_sha": sha(sc),
             "ratio": 2 * v.size / footprint_total(len(st), pk.size, sc.size, 2)}
 
+    # NZT containers written by the reference (tensorstore.hpp:352-390).
+    out["nzt"] = {}
+    for name, gen, shape, k, block in G.nzt_cases():
+        v = gen(R)
+        data = (R.write_nzt_lossless(v, shape) if k == 7 else R.write_nzt_lossy(v, shape, k, block))
+        out["nzt"][name] = {"len": len(data), "sha": sha(data), "crc": int.from_bytes(data[-4:], "little")}
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1, sort_keys=True)
 

@@ -113,3 +113,17 @@ def table_cases():
                 c[s] = 1
         out.append((f"rand_repair_{t}", c))
     return out
+
+
+# NZT containers (tensorstore.hpp:289-477): (name, generator, shape, precision, block)
+def nzt_cases():
+    g = lambda seed, n, sigma=0.02: (lambda o: o.gaussian_bf16(seed, n, sigma))
+    return [
+        ("const16_k7", lambda o: np.full(16, 0x3F80, np.uint16), (16,), 7, 0),
+        ("gauss_4x4096_k7", g(42, 4 * 4096), (4, 4096), 7, 0),
+        ("gauss_300k_k7", g(8, 300000), (300, 1000), 7, 0),
+        ("gauss_2x3x7x1000_k7", g(9, 42000), (2, 3, 7, 1000), 7, 0),
+        ("gauss_70000_k3_B512", g(10, 70000), (70000,), 3, 512),
+        ("gauss_70000_k1_B100", g(11, 70000), (700, 100), 1, 100),
+        ("gauss_70000_k0_B37", g(12, 70000), (70000,), 0, 37),
+    ]
