@@ -16,6 +16,8 @@
 // count (front-padded with zero blocks) using x^(8*16384*2^k).  The host
 // joins sections (table, scales, stream, mantissas) and applies the
 // init/xorout term -- a few GF(2) multiplies.
+#include <mutex>
+
 #include "nzgpu_internal.cuh"
 
 namespace nzgpu {
@@ -96,6 +98,75 @@ __global__ void __launch_bounds__(256) crc_raw_blocks_kernel(const uint8_t* __re
     if (lane == 0) out[wblock] = c;
 }
 
+// Same result for large inputs, conflict-free: the four 256-entry tables
+// are replicated per bank (word (t*256 + e)*32 + lane, 128 KiB), so every
+// warp-wide lookup is one shared-memory wavefront instead of ~3.5; a
+// persistent grid (one 512-thread CTA per SM) amortises the table fill.
+constexpr int kCrcWideThreads = 512;
+constexpr uint32_t kCrcWideSmem = 4 * 256 * 32 * 4;
+
+__global__ void __launch_bounds__(kCrcWideThreads) crc_raw_blocks_wide_kernel(
+    const uint8_t* __restrict__ data, uint64_t len, uint64_t pad, uint64_t nblocks,
+    const uint32_t* __restrict__ tables_g, CrcConsts cc, uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint32_t Tw[];
+    for (int w = threadIdx.x; w < 4 * 256 * 32; w += blockDim.x) Tw[w] = __ldg(tables_g + (w >> 5));
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(Tw) + lane * 4;  // bank = lane
+    auto lk = [&](int t, uint32_t e) {
+        uint32_t v;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(tb + ((uint32_t)t << 15) + (e << 7)));
+        return v;
+    };
+    const uint64_t warps = (uint64_t)gridDim.x * (kCrcWideThreads / 32);
+    for (uint64_t wblock = blockIdx.x * (uint64_t)(kCrcWideThreads / 32) + (threadIdx.x >> 5); wblock < nblocks;
+         wblock += warps) {
+        const uint64_t ps = wblock * kCrcBlock + (uint64_t)lane * kCrcLane;
+        const uint64_t pe = ps + kCrcLane;
+        const uint64_t s = ps > pad ? ps - pad : 0, e = pe > pad ? pe - pad : 0;
+        uint32_t c = 0;
+        if (e > s) {
+            uint64_t i = s;
+            const uint64_t base = reinterpret_cast<uintptr_t>(data);
+            const uint64_t al = ((base + s + 15) & ~15ull) - base;
+            const uint64_t head_end = e < al ? e : al;
+            for (; i < head_end; ++i) c = lk(0, (c ^ __ldg(data + i)) & 0xFFu) ^ (c >> 8);
+            auto word = [&](uint32_t w) {
+                const uint32_t x = c ^ w;
+                c = lk(3, x & 0xFFu) ^ lk(2, __byte_perm(x, 0, 0x4441)) ^ lk(1, __byte_perm(x, 0, 0x4442)) ^
+                    lk(0, x >> 24);
+            };
+            // 8 loads (128 B) in flight per lane before the serial CRC chain
+            for (; i + 128 <= e; i += 128) {
+                uint4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(data + i) + q);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    word(v[q].x);
+                    word(v[q].y);
+                    word(v[q].z);
+                    word(v[q].w);
+                }
+            }
+            for (; i + 16 <= e; i += 16) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(data + i));
+                word(v.x);
+                word(v.y);
+                word(v.z);
+                word(v.w);
+            }
+            for (; i < e; ++i) c = lk(0, (c ^ __ldg(data + i)) & 0xFFu) ^ (c >> 8);
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const uint32_t r = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+            if ((lane & ((2 << k) - 1)) == 0) c = gf2_mulmod(cc.lane[k], c) ^ r;
+        }
+        if (lane == 0) out[wblock] = c;
+    }
+}
+
 // Tree over v[0 .. 2^levels): the data's blocks occupy the tail, the front
 // entries are zero blocks (raw CRC 0).  One CTA; v[0] holds the result.
 __global__ void __launch_bounds__(1024) crc_join_kernel(uint32_t* __restrict__ v, int levels, CrcConsts cc) {
@@ -169,17 +240,42 @@ cudaError_t crc_raw_device(const uint8_t* d, uint64_t len, cudaStream_t s, uint3
     int levels = 0;
     while ((1ull << levels) < nblocks) ++levels;
     const uint64_t nb2 = 1ull << levels, lead = nb2 - nblocks;
-    uint32_t* v = nullptr;
-    if ((e = cudaMallocAsync(&v, nb2 * sizeof(uint32_t), s)) != cudaSuccess) return e;
+    // grow-only scratch per device (a stream-ordered allocation per call costs
+    // milliseconds when the pool trims at every synchronisation)
+    static std::mutex mu;
+    static uint32_t* scratch[64] = {};
+    static uint64_t scratch_n[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (scratch_n[dev] < nb2) {
+        if (scratch[dev]) cudaFree(scratch[dev]);
+        scratch[dev] = nullptr;
+        scratch_n[dev] = 0;
+        if ((e = cudaMalloc(&scratch[dev], nb2 * sizeof(uint32_t))) != cudaSuccess) return e;
+        scratch_n[dev] = nb2;
+    }
+    uint32_t* v = scratch[dev];
     if (lead) cudaMemsetAsync(v, 0, lead * sizeof(uint32_t), s);
-    const uint64_t threads = nblocks * 32;
-    crc_raw_blocks_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d, len, pad, nblocks, g_crc_tables.d[dev],
-                                                                           cc, v + lead);
+    if (len >= (64ull << 20)) {
+        static bool attr[64] = {};
+        if (!attr[dev]) {
+            if ((e = cudaFuncSetAttribute(crc_raw_blocks_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kCrcWideSmem)) != cudaSuccess)
+                return e;
+            attr[dev] = true;
+        }
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        crc_raw_blocks_wide_kernel<<<(unsigned)sms, kCrcWideThreads, kCrcWideSmem, s>>>(
+            d, len, pad, nblocks, g_crc_tables.d[dev], cc, v + lead);
+    } else {
+        const uint64_t threads = nblocks * 32;
+        crc_raw_blocks_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d, len, pad, nblocks,
+                                                                               g_crc_tables.d[dev], cc, v + lead);
+    }
     if (levels) crc_join_kernel<<<1, 1024, 0, s>>>(v, levels, cc);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(raw, v, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-    cudaFreeAsync(v, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // before the scratch can be reused
     return e;
 }
 
