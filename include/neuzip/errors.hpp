@@ -41,6 +41,7 @@ namespace detail {
         case NZGPU_FORMAT_DESYNC:
         case NZGPU_FORMAT_LENGTH:
         case NZGPU_FORMAT_TABLE: throw FormatError(msg);
+        case NZGPU_CHECKSUM: throw ChecksumError(msg);
         case NZGPU_NONFINITE: throw NonFiniteError(msg);
         default: throw Error(msg + " (" + nzgpu_last_error_message() + ")");
     }

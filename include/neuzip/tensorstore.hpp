@@ -13,12 +13,16 @@
 // validation first.
 
 #include <cstdint>
+#include <istream>
+#include <ostream>
 #include <span>
+#include <string>
 #include <variant>
 #include <vector>
 
 #include "neuzip/ans.hpp"
 #include "neuzip/bitfloat.hpp"
+#include "neuzip/crc32.hpp"
 #include "neuzip/errors.hpp"
 
 namespace neuzip {
@@ -217,6 +221,177 @@ inline Footprint footprint(const LossyBlob& b) {
 }
 inline Footprint footprint(const Blob& b) {
     return std::visit([](const auto& x) { return footprint(x); }, b);
+}
+
+// --- NZT container (tensorstore.hpp:289-477) --------------------------------
+// Same byte layout; the CRC is computed on the GPU and read_nzt validates on
+// the GPU (framing, CRC -> ChecksumError, table, stream, counts) through
+// nzgpu_blob_read_nzt, so the error classes are the reference's.
+
+namespace detail {
+template <typename T>
+void nzt_put(std::string& out, T v) {
+    for (std::size_t i = 0; i < sizeof(T); ++i) out.push_back(static_cast<char>(static_cast<std::uint64_t>(v) >> (8 * i)));
+}
+
+inline void write_nzt_sections(std::ostream& out, const TensorMeta& meta, int precision, std::uint32_t block,
+                               const FrequencyTable& table, const std::vector<std::uint8_t>& scales,
+                               const std::vector<std::uint8_t>& exp_bytes, const std::vector<std::uint8_t>& signmant) {
+    const auto tb = table.serialize();
+    const void* ptrs[4] = {tb.data(), scales.data(), exp_bytes.data(), signmant.data()};
+    const std::uint64_t lens[4] = {tb.size(), scales.size(), exp_bytes.size(), signmant.size()};
+    std::uint32_t crc = 0;
+    check(nzgpu_crc32_host_sections(ptrs, lens, 4, &crc), "write_nzt");
+    std::string head("NZT1");
+    nzt_put<std::uint8_t>(head, 1);
+    nzt_put<std::uint8_t>(head, static_cast<std::uint8_t>(precision));
+    nzt_put<std::uint32_t>(head, block);
+    nzt_put<std::uint8_t>(head, static_cast<std::uint8_t>(meta.shape.size()));
+    for (std::uint64_t d : meta.shape) nzt_put<std::uint64_t>(head, d);
+    out.write(head.data(), static_cast<std::streamsize>(head.size()));
+    out.write(reinterpret_cast<const char*>(tb.data()), static_cast<std::streamsize>(tb.size()));
+    std::string len4;
+    nzt_put<std::uint32_t>(len4, static_cast<std::uint32_t>(scales.size()));
+    out.write(len4.data(), 4);
+    out.write(reinterpret_cast<const char*>(scales.data()), static_cast<std::streamsize>(scales.size()));
+    std::string len8;
+    nzt_put<std::uint64_t>(len8, exp_bytes.size());
+    out.write(len8.data(), 8);
+    out.write(reinterpret_cast<const char*>(exp_bytes.data()), static_cast<std::streamsize>(exp_bytes.size()));
+    len8.clear();
+    nzt_put<std::uint64_t>(len8, signmant.size());
+    out.write(len8.data(), 8);
+    out.write(reinterpret_cast<const char*>(signmant.data()), static_cast<std::streamsize>(signmant.size()));
+    std::string c4;
+    nzt_put<std::uint32_t>(c4, crc);
+    out.write(c4.data(), 4);
+    if (!out) throw Error("nzt: write failed");
+}
+
+// Pull `k` more bytes of the file into `buf` (FormatError at end of file).
+inline void nzt_pull(std::istream& in, std::string& buf, std::uint64_t k) {
+    const std::size_t at = buf.size();
+    buf.resize(at + k);
+    in.read(buf.data() + at, static_cast<std::streamsize>(k));
+    if (static_cast<std::uint64_t>(in.gcount()) != k) throw FormatError("unexpected end of file");
+}
+inline std::uint64_t nzt_le(const std::string& buf, std::size_t at, int bytes) {
+    std::uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= static_cast<std::uint64_t>(static_cast<std::uint8_t>(buf[at + i])) << (8 * i);
+    return v;
+}
+}  // namespace detail
+
+inline void write_nzt(const LosslessBlob& blob, std::ostream& out) {  // tensorstore.hpp:372-380
+    detail::write_nzt_sections(out, blob.meta, kLosslessPrecision, 0, blob.table(), {}, serialize_stream(blob.exp_stream),
+                               blob.signmant);
+}
+
+inline void write_nzt(const LossyBlob& blob, std::ostream& out) {  // tensorstore.hpp:382-390
+    detail::write_nzt_sections(out, blob.meta, blob.precision, blob.block_size, blob.table(), blob.scales,
+                               serialize_stream(blob.exp_stream), blob.signmant);
+}
+
+inline void write_nzt(const Blob& blob, std::ostream& out) {
+    std::visit([&](const auto& b) { write_nzt(b, out); }, blob);
+}
+
+// tensorstore.hpp:403-477: the header fields are read one by one so that a
+// stream positioned after this file is left there; the payload lengths come
+// from the header, and the assembled file is validated by the GPU reader.
+inline Blob read_nzt(std::istream& in) {
+    std::string f;
+    char magic[4];
+    in.read(magic, 4);
+    if (in.gcount() != 4 || std::string(magic, 4) != "NZT1") throw FormatError("nzt: bad magic");
+    f.assign(magic, 4);
+    detail::nzt_pull(in, f, 2);
+    if (static_cast<std::uint8_t>(f[4]) != 1) throw FormatError("nzt: unsupported version");
+    const int precision = static_cast<std::uint8_t>(f[5]);
+    if (precision != 0 && precision != 1 && precision != 3 && precision != kLosslessPrecision)
+        throw FormatError("nzt: invalid precision");
+    detail::nzt_pull(in, f, 5);
+    const std::uint64_t block = detail::nzt_le(f, 6, 4);
+    const std::uint64_t ndim = static_cast<std::uint8_t>(f[10]);
+    if (ndim == 0 || ndim > 8) throw FormatError("nzt: invalid rank");
+    detail::nzt_pull(in, f, 8 * ndim);
+    std::uint64_t n = 1;
+    for (std::uint64_t i = 0; i < ndim; ++i) {
+        const std::uint64_t d = detail::nzt_le(f, 11 + 8 * i, 8);
+        if (d == 0) throw FormatError("nzt: zero dimension");
+        if (d > (std::uint64_t{1} << 40) / n) throw FormatError("nzt: element count overflow");
+        n *= d;
+    }
+    // section lengths are checked against the element count before reading
+    if (precision == kLosslessPrecision ? block != 0 : block == 0) throw FormatError("nzt: block size");
+    const std::uint64_t want_scales = precision == kLosslessPrecision ? 0 : (n + block - 1) / block;
+    const std::uint64_t want_sm = (n * (static_cast<std::uint64_t>(precision) + 1) + 7) / 8;
+    const std::uint64_t cap = 2 * n + 16 * ((n + ans::kChunkSymbols - 1) / ans::kChunkSymbols) + 64;
+    detail::nzt_pull(in, f, 512 + 4);
+    if (detail::nzt_le(f, f.size() - 4, 4) != want_scales) throw FormatError("nzt: scale count mismatch");
+    detail::nzt_pull(in, f, want_scales + 8);
+    const std::uint64_t exp_len = detail::nzt_le(f, f.size() - 8, 8);
+    if (exp_len > cap) throw FormatError("nzt: exponent stream oversized");
+    detail::nzt_pull(in, f, exp_len + 8);
+    if (detail::nzt_le(f, f.size() - 8, 8) != want_sm) throw FormatError("nzt: sign-mantissa length mismatch");
+    detail::nzt_pull(in, f, want_sm + 4);
+    detail::DeviceBlob b;
+    std::uint64_t dims[8] = {};
+    int nd = 0;
+    detail::check(nzgpu_blob_read_nzt(reinterpret_cast<const std::uint8_t*>(f.data()), f.size(), 0, nullptr, &b.h,
+                                      dims, &nd),
+                  "read_nzt");
+    TensorMeta meta{std::vector<std::uint64_t>(dims, dims + nd)};
+    detail::Sections s = detail::export_blob(b.h);
+    const FrequencyTable table = detail::table_from(s.freqs);
+    if (precision == kLosslessPrecision)
+        return LosslessBlob{std::move(meta), deserialize_stream(s.stream, table), std::move(s.mantissas),
+                            std::move(s.index)};
+    return LossyBlob{std::move(meta),         precision,           static_cast<std::uint32_t>(block),
+                     std::move(s.scales),     deserialize_stream(s.stream, table), std::move(s.mantissas),
+                     std::move(s.index)};
+}
+
+// --- BFT raw tensor format (tensorstore.hpp:479-517) -------------------------
+inline void write_bft(const Tensor& tensor, std::ostream& out) {
+    tensor.meta.validate();
+    if (tensor.meta.element_count() != tensor.values.size())
+        throw std::invalid_argument("bft: shape does not match value count");
+    std::string head("BFT1");
+    detail::nzt_put<std::uint8_t>(head, static_cast<std::uint8_t>(tensor.meta.shape.size()));
+    for (std::uint64_t d : tensor.meta.shape) detail::nzt_put<std::uint64_t>(head, d);
+    out.write(head.data(), static_cast<std::streamsize>(head.size()));
+    std::string body;
+    body.reserve(2 * tensor.values.size());
+    for (Bf16 v : tensor.values) detail::nzt_put<std::uint16_t>(body, v.bits);
+    out.write(body.data(), static_cast<std::streamsize>(body.size()));
+    if (!out) throw Error("bft: write failed");
+}
+
+inline Tensor read_bft(std::istream& in) {
+    char magic[4];
+    in.read(magic, 4);
+    if (in.gcount() != 4 || std::string(magic, 4) != "BFT1") throw FormatError("bft: bad magic");
+    std::string f;
+    detail::nzt_pull(in, f, 1);
+    const std::uint64_t ndim = static_cast<std::uint8_t>(f[0]);
+    if (ndim == 0 || ndim > 8) throw FormatError("bft: invalid rank");
+    detail::nzt_pull(in, f, 8 * ndim);
+    Tensor t;
+    t.meta.shape.resize(ndim);
+    std::uint64_t n = 1;
+    for (std::uint64_t i = 0; i < ndim; ++i) {
+        const std::uint64_t d = detail::nzt_le(f, 1 + 8 * i, 8);
+        if (d == 0) throw FormatError("bft: zero dimension");
+        if (d > (std::uint64_t{1} << 40) / n) throw FormatError("bft: element count overflow");
+        t.meta.shape[i] = d;
+        n *= d;
+    }
+    std::string body;
+    detail::nzt_pull(in, body, 2 * n);
+    t.values.resize(n);
+    for (std::uint64_t i = 0; i < n; ++i) t.values[i].bits = static_cast<std::uint16_t>(detail::nzt_le(body, 2 * i, 2));
+    return t;
 }
 
 }  // namespace neuzip

@@ -5,6 +5,7 @@
 // Exits 0 when every check passes.  Built and run by tests/test_cpp_dropin.py.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <cstring>
 #include <functional>
 #include <random>
@@ -209,6 +210,60 @@ int main() {
         CHECK(throws<std::invalid_argument>([] { (void)compress_lossy(std::vector<Bf16>{Bf16{0x3F80}}, 2, 512); }));
         CHECK(throws<std::invalid_argument>([] { (void)compress_lossy(std::vector<Bf16>{Bf16{0x3F80}}, 3, 0); }));
         CHECK(throws<std::invalid_argument>([] { (void)compress_lossless(std::vector<Bf16>{}); }));
+    }
+    {  // crc32.hpp + NZT/BFT containers (tensorstore.hpp:289-517)
+        const std::string chk = "123456789";
+        CHECK(crc32(std::span(reinterpret_cast<const std::uint8_t*>(chk.data()), chk.size())) == 0xCBF43926u);
+        Crc32 inc;  // incremental updates join to the one-shot value
+        inc.update(std::span(reinterpret_cast<const std::uint8_t*>(chk.data()), 4));
+        inc.update(std::span(reinterpret_cast<const std::uint8_t*>(chk.data()) + 4, 5));
+        CHECK(inc.value() == 0xCBF43926u);
+        CHECK(Crc32{}.value() == 0u);
+        // const16_k7.nzt (gen_golden.cpp:34-41): 587 bytes, CRC ec9e894f
+        const LosslessBlob c16 = compress_lossless(std::vector<Bf16>(16, Bf16{0x3F80}));
+        std::ostringstream os(std::ios::binary);
+        write_nzt(Blob(c16), os);
+        const std::string file = os.str();
+        CHECK(file.size() == 587);
+        CHECK(static_cast<std::uint8_t>(file[583]) == 0xEC && static_cast<std::uint8_t>(file[586]) == 0x4F);
+        std::istringstream is(file, std::ios::binary);
+        const Blob back = read_nzt(is);
+        CHECK(decompress_lossless(std::get<LosslessBlob>(back)) == std::vector<Bf16>(16, Bf16{0x3F80}));
+        const auto g = gaussian(11, 70000, 0.02);
+        for (int k : {7, 3, 0}) {
+            std::ostringstream o2(std::ios::binary);
+            const TensorMeta meta{{700, 100}};
+            if (k == 7) write_nzt(compress_lossless(g, meta), o2);
+            else write_nzt(compress_lossy(g, k, 64, meta), o2);
+            std::string f2 = o2.str();
+            std::istringstream i2(f2 + "tail", std::ios::binary);  // a reader stops at the file's end
+            const Blob b2 = read_nzt(i2);
+            std::string rest;
+            i2 >> rest;
+            CHECK(rest == "tail");
+            if (k == 7) CHECK(decompress_lossless(std::get<LosslessBlob>(b2)) == g);
+            else CHECK(std::get<LossyBlob>(b2).meta == meta && std::get<LossyBlob>(b2).block_size == 64);
+            f2[f2.size() / 2] ^= 0x20;  // payload byte -> ChecksumError
+            CHECK(throws<ChecksumError>([&] {
+                std::istringstream i3(f2, std::ios::binary);
+                (void)read_nzt(i3);
+            }));
+            CHECK(throws<FormatError>([&] {
+                std::istringstream i4(f2.substr(0, 100), std::ios::binary);
+                (void)read_nzt(i4);
+            }));
+        }
+        CHECK(throws<FormatError>([] {
+            std::istringstream i5(std::string("NZT2xxxxxxxxxx"), std::ios::binary);
+            (void)read_nzt(i5);
+        }));
+        Tensor t{TensorMeta{{2, 3}}, {Bf16{1}, Bf16{2}, Bf16{3}, Bf16{0x8000}, Bf16{0x7F80}, Bf16{0xFFFF}}};
+        std::ostringstream ob(std::ios::binary);
+        write_bft(t, ob);
+        CHECK(ob.str().size() == 4 + 1 + 16 + 12);
+        std::istringstream ib(ob.str(), std::ios::binary);
+        const Tensor tb = read_bft(ib);
+        CHECK(tb.meta == t.meta && tb.values == t.values);
     }
     std::printf("dropin_test: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
