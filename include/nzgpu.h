@@ -149,6 +149,10 @@ int nzgpu_plan_launch_count(nzgpu_plan plan);
 /* Decode kernel nzgpu_plan_launch uses now: 0 persistent, 1 tiles, -1 none
  * (empty plan). */
 int nzgpu_plan_kernel(nzgpu_plan plan);
+/* Cap the persistent decode at `max_ctas` CTAs (one per SM; 0 = all
+ * resident), leaving the other SMs to concurrent work on another stream --
+ * the layer-wise consumer decodes layer l+1 beside layer l's GEMM. */
+int nzgpu_plan_set_max_ctas(nzgpu_plan plan, uint32_t max_ctas);
 
 /* ---- host tier: the reference-facing calls (host buffers, synchronous) --- */
 /* Compress host values; returns a device blob (export its sections with

@@ -511,6 +511,11 @@ class DecodePlan:
     def launches(self) -> int:
         return int(N.lib.nzgpu_plan_launch_count(self._h))
 
+    def set_max_ctas(self, max_ctas: int) -> None:
+        """Decode on at most `max_ctas` SMs (0 = all), leaving the rest to
+        concurrent kernels on other streams."""
+        N.check(N.lib.nzgpu_plan_set_max_ctas(self._h, int(max_ctas)), "plan_set_max_ctas")
+
     @property
     def kernel(self) -> str:
         """Decode kernel the next launch uses."""

@@ -582,6 +582,8 @@ struct nzgpu_plan_s {
     // persistent schedule
     uint32_t ctas = 0, upc = 1, win_cap_unit = 0;
     uint32_t* d_cta_prefix = nullptr;
+    std::vector<uint64_t> tunits;  // work units per tensor
+    uint32_t max_ctas = 0;         // 0 = every resident CTA (nzgpu_plan_set_max_ctas)
     ~nzgpu_plan_s() {
         if (d_descs) cudaFree(d_descs);
         if (d_prefix) cudaFree(d_prefix);
@@ -589,6 +591,42 @@ struct nzgpu_plan_s {
         if (d_cta_prefix) cudaFree(d_cta_prefix);
     }
 };
+
+// Persistent schedule of a plan: every CTA owns `upc` units of one tensor.
+// The per-tensor round-up must not push the CTA count past one resident wave
+// (a second wave of a few CTAs doubles the launch time), so upc is the
+// smallest value with sum_i ceil(units_i / upc) <= resident CTAs.  Returns
+// the per-tensor first-CTA prefix.
+std::vector<uint32_t> persist_geometry(nzgpu_plan_s* p) {
+    std::vector<uint32_t> cta_prefix;
+    uint64_t units = 0;
+    for (uint64_t u : p->tunits) units += u;
+    p->ctas = 0;
+    if (!units) return cta_prefix;
+    uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
+    if (p->max_ctas) resident = std::min<uint64_t>(resident, p->max_ctas);
+    auto ctas_for = [&](uint64_t upc) {
+        uint64_t c = 0;
+        for (uint64_t u : p->tunits) c += ceil_div(u, upc);
+        return c;
+    };
+    const uint64_t umax = *std::max_element(p->tunits.begin(), p->tunits.end());
+    uint64_t lo = std::max<uint64_t>(1, ceil_div(units, resident)), hi = lo;
+    while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
+    hi = std::max(lo, std::min(hi, umax));
+    while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
+        const uint64_t mid = (lo + hi) / 2;
+        if (ctas_for(mid) > resident) lo = mid + 1; else hi = mid;
+    }
+    p->upc = (uint32_t)lo;
+    uint32_t ctas = 0;
+    for (uint64_t u : p->tunits) {
+        cta_prefix.push_back(ctas);
+        ctas += (uint32_t)ceil_div(u, p->upc);
+    }
+    p->ctas = ctas;
+    return cta_prefix;
+}
 
 // =================================================================== C ABI
 extern "C" {
@@ -745,40 +783,8 @@ int nzgpu_plan_create(const nzgpu_blob* blobs, uint16_t* const* d_outs, int coun
     }
     p->tiles = tiles;
     p->count = (int)descs.size();
-    // Persistent schedule: every CTA owns `upc` units of one tensor.  The
-    // per-tensor round-up must not push the CTA count past one resident wave
-    // (a second wave of a few CTAs doubles the launch time), so upc is the
-    // smallest value with sum_i ceil(units_i / upc) <= resident CTAs.
-    std::vector<uint32_t> cta_prefix;
-    std::vector<uint64_t> tunits;
-    uint64_t units = 0;
-    for (const DecodeDesc& d : descs) {
-        tunits.push_back(ceil_div(ceil_div(d.n, 1ull << p->log2k), 32));
-        units += tunits.back();
-    }
-    if (units) {
-        const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
-        auto ctas_for = [&](uint64_t upc) {
-            uint64_t c = 0;
-            for (uint64_t u : tunits) c += ceil_div(u, upc);
-            return c;
-        };
-        const uint64_t umax = *std::max_element(tunits.begin(), tunits.end());
-        uint64_t lo = std::max<uint64_t>(1, ceil_div(units, resident)), hi = lo;
-        while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
-        hi = std::max(lo, std::min(hi, umax));
-        while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
-            const uint64_t mid = (lo + hi) / 2;
-            if (ctas_for(mid) > resident) lo = mid + 1; else hi = mid;
-        }
-        p->upc = (uint32_t)lo;
-        uint32_t ctas = 0;
-        for (const DecodeDesc& d : descs) {
-            cta_prefix.push_back(ctas);
-            ctas += (uint32_t)ceil_div(ceil_div(ceil_div(d.n, 1ull << p->log2k), 32), p->upc);
-        }
-        p->ctas = ctas;
-    }
+    for (const DecodeDesc& d : descs) p->tunits.push_back(ceil_div(ceil_div(d.n, 1ull << p->log2k), 32));
+    const std::vector<uint32_t> cta_prefix = persist_geometry(p.get());
     if (!descs.empty()) {
         CK(cudaMalloc(&p->d_descs, descs.size() * sizeof(DecodeDesc)));
         CK(cudaMalloc(&p->d_prefix, prefix.size() * sizeof(uint64_t)));
@@ -817,6 +823,16 @@ int nzgpu_plan_free(nzgpu_plan p) {
 }
 
 int nzgpu_plan_launch_count(nzgpu_plan p) { return p && p->tiles ? 1 : 0; }
+
+int nzgpu_plan_set_max_ctas(nzgpu_plan p, uint32_t max_ctas) {
+    if (!p) return NZGPU_INVALID_ARGUMENT;
+    p->max_ctas = max_ctas;
+    const std::vector<uint32_t> cta_prefix = persist_geometry(p);
+    if (!cta_prefix.empty())
+        CK(cudaMemcpy(p->d_cta_prefix, cta_prefix.data(), cta_prefix.size() * sizeof(uint32_t),
+                      cudaMemcpyHostToDevice));
+    return NZGPU_OK;
+}
 
 int nzgpu_plan_kernel(nzgpu_plan p) {
     if (!p || !p->tiles) return -1;

@@ -132,6 +132,7 @@ SIGNATURES = {
     "nzgpu_plan_free": (_i, [_vp]),
     "nzgpu_plan_launch_count": (_i, [_vp]),
     "nzgpu_plan_kernel": (_i, [_vp]),
+    "nzgpu_plan_set_max_ctas": (_i, [_vp, _u32]),
     "nzgpu_compress_host": (_i, [_vp, _u64, _i, _u32, _u32, _u32, _p(_vp)]),
     "nzgpu_decompress_host": (_i, [_p(HostTensor), _vp]),
     "nzgpu_decompress_host_batch": (_i, [_p(HostTensor), _i, _p(_vp)]),
