@@ -102,6 +102,35 @@ def _sgd(w, g, lr):
     return (w.float() - lr * g.float()).to(torch.bfloat16)
 
 
+class _SmTarget:
+    """While the decode is capped to `ctas` SMs, ask cuBLAS to size its GEMMs
+    for the remaining SMs (cublasSetSmCountTarget on torch's handle), so the
+    two kernels actually run side by side instead of taking turns."""
+    _lib = None
+
+    def __init__(self, ctas: int):
+        self.ctas = ctas
+
+    def __enter__(self):
+        if not self.ctas:
+            return self
+        import ctypes as C
+
+        import torch
+
+        if _SmTarget._lib is None:
+            _SmTarget._lib = C.CDLL("libcublas.so.12")
+            _SmTarget._lib.cublasSetSmCountTarget.argtypes = [C.c_void_p, C.c_int]
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        self.h = C.c_void_p(torch.cuda.current_blas_handle())
+        _SmTarget._lib.cublasSetSmCountTarget(self.h, max(1, sms - self.ctas))
+        return self
+
+    def __exit__(self, *a):
+        if self.ctas:
+            _SmTarget._lib.cublasSetSmCountTarget(self.h, 0)
+
+
 class CompressedMlp:
     """nn.hpp MlpModel with a double-buffered, overlapped layer decode."""
 
@@ -115,7 +144,9 @@ class CompressedMlp:
         self.decode_ctas = decode_ctas
         maxn = max(l.out_dim * l.in_dim for l in layers)
         self.bufs = [torch.empty(maxn + 64, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
-        self.side = torch.cuda.Stream()
+        # high priority: as GEMM CTAs retire, the block scheduler hands the
+        # freed SMs to the pending decode CTAs first
+        self.side = torch.cuda.Stream(priority=-1)
         self.plans = [None] * len(layers)
         for i in range(len(layers)):
             self._plan(i)
@@ -151,11 +182,13 @@ class CompressedMlp:
         if self.meter:
             self.meter.on_weight_free(2 * self.layers[i].out_dim * self.layers[i].in_dim)
 
-    def forward(self, x0, tape: Optional[ActivationTape] = None):
-        """nn.hpp:256-268 with layer l+1 decoded beside layer l's GEMM."""
+    def forward(self, x0, tape: Optional[ActivationTape] = None, check: bool = True):
+        """nn.hpp:256-268 with layer l+1 decoded beside layer l's GEMM.
+        check: read every plan's decode status at the end (one sync each)."""
         import torch
 
         main = torch.cuda.current_stream()
+        sm_target = _SmTarget(self.decode_ctas)
         L = len(self.layers)
         ready = [torch.cuda.Event() for _ in range(L)]
         free = [torch.cuda.Event(), torch.cuda.Event()]
@@ -178,13 +211,15 @@ class CompressedMlp:
             if tape is not None:
                 tape.inputs.append(x)
             main.wait_event(ready[i])
-            x = _linear(x, self._weight(i), self.layers[i].bias)
+            with sm_target:
+                x = _linear(x, self._weight(i), self.layers[i].bias)
             free[i % 2].record(main)
             self._meter_free(i)
             if i + 1 != L and self.activation == Activation.Relu:
                 _relu_(x)
-        for p in self.plans:
-            p.status(main)
+        if check:
+            for p in self.plans:
+                p.status(main)
         return x
 
     def backward_and_update(self, tape: ActivationTape, grad_out, lr: float, alg1_literal: bool = False):
