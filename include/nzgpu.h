@@ -214,6 +214,18 @@ int nzgpu_blob_write_nzt(nzgpu_blob blob, const uint64_t* shape, int ndim, uint8
 int nzgpu_blob_read_nzt(const uint8_t* data, uint64_t len, uint32_t interval, void* cuda_stream, nzgpu_blob* out,
                         uint64_t* shape, int* ndim);
 
+/* ---- entropy report (entropy.hpp:17-94) ---------------------------------- */
+/* ComponentHistogram of a device bf16 tensor (16-byte aligned): counts[386] =
+ * sign[2] | exponent[256] | mantissa[128] (entropy.hpp:17-39). */
+int nzgpu_component_histogram(const uint16_t* d_values, uint64_t n, void* cuda_stream, uint64_t* counts);
+int nzgpu_component_histogram_host(const uint16_t* values, uint64_t n, uint64_t* counts);
+/* report_from_histogram (entropy.hpp:69-81): out5 = h_sign, h_exp, h_mant,
+ * ideal_ratio, exponent_only_ratio. */
+int nzgpu_entropy_from_histogram(const uint64_t* counts, double* out5);
+/* analyze_tensor (entropy.hpp:89-94) of a device / host tensor. */
+int nzgpu_entropy_report(const uint16_t* d_values, uint64_t n, void* cuda_stream, double* out5);
+int nzgpu_entropy_report_host(const uint16_t* values, uint64_t n, double* out5);
+
 #ifdef __cplusplus
 }
 #endif

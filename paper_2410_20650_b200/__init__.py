@@ -13,6 +13,7 @@ from .codec import (  # noqa: F401
     Blob,
     ChecksumError,
     DecodePlan,
+    EntropyReport,
     DeviceBlob,
     Error,
     FormatError,
@@ -21,9 +22,11 @@ from .codec import (  # noqa: F401
     LossyBlob,
     NonFiniteError,
     TensorMeta,
+    analyze_tensor,
     ans_decode,
     ans_encode,
     build_table,
+    component_histogram,
     compress_lossless,
     compress_lossy,
     crc32,

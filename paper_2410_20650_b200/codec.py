@@ -272,6 +272,50 @@ def crc32(*sections) -> int:
     return int(out.value)
 
 
+@dataclass
+class EntropyReport:
+    """entropy.hpp:57-66"""
+    h_sign: float
+    h_exp: float
+    h_mant: float
+    ideal_ratio: float
+    exponent_only_ratio: float
+
+
+def component_histogram(values):
+    """ComponentHistogram (entropy.hpp:17-39) on the GPU: (sign[2], exp[256],
+    mant[128]) counts.  values: CUDA bf16/int16 tensor."""
+    import torch
+
+    if values.dtype == torch.bfloat16:
+        values = values.view(torch.int16)
+    values = values.contiguous().view(-1)
+    counts = np.zeros(386, np.uint64)
+    N.check(N.lib.nzgpu_component_histogram(C.c_void_p(values.data_ptr()), values.numel(), _stream_ptr(None),
+                                            _ptr(counts)), "component_histogram")
+    return counts[:2], counts[2:258], counts[258:]
+
+
+def analyze_tensor(values) -> EntropyReport:
+    """analyze_tensor (entropy.hpp:89-94): host bf16 bit patterns or a CUDA
+    tensor; the histogram runs on the GPU."""
+    out = np.zeros(5, np.float64)
+    if hasattr(values, "is_cuda") and values.is_cuda:
+        import torch
+
+        v = values.view(torch.int16).contiguous().view(-1) if values.dtype == torch.bfloat16 else values.contiguous().view(-1)
+        if v.numel() == 0:
+            raise ValueError("analyze_tensor: empty input")
+        N.check(N.lib.nzgpu_entropy_report(C.c_void_p(v.data_ptr()), v.numel(), _stream_ptr(None), _ptr(out)),
+                "analyze_tensor")
+    else:
+        v = _as_u16(values)
+        if v.size == 0:
+            raise ValueError("analyze_tensor: empty input")
+        N.check(N.lib.nzgpu_entropy_report_host(_ptr(v), v.size, _ptr(out)), "analyze_tensor")
+    return EntropyReport(*[float(x) for x in out])
+
+
 def write_nzt(blob: Blob) -> bytes:
     """write_nzt (tensorstore.hpp:352-376) of a host blob; the CRC is computed
     on the GPU.  Byte-identical to the reference's file."""

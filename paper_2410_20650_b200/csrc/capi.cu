@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -51,6 +52,8 @@ cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* de
 uint32_t persist_resident_ctas(int log2k, uint32_t win_cap);
 bool persist_fits(int log2k, uint32_t win_cap);
 cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
+// entropy.cu
+__global__ void component_hist_kernel(const uint16_t*, uint64_t, unsigned long long*);
 // crc32.cu
 cudaError_t crc_raw_device(const uint8_t* d, uint64_t len, cudaStream_t s, uint32_t* raw);
 uint32_t crc_combine_raw(uint32_t raw_a, uint32_t raw_b, uint64_t len_b);
@@ -1460,6 +1463,87 @@ int nzgpu_blob_read_nzt(const uint8_t* data, uint64_t len, uint32_t interval, vo
         for (uint64_t i = 0; i < ndim; ++i) shape[i] = dims[i];
     if (ndim_out) *ndim_out = (int)ndim;
     return NZGPU_OK;
+}
+
+
+// ------------------------------------------------------ entropy report ---
+int nzgpu_component_histogram(const uint16_t* d_values, uint64_t n, void* cuda_stream, uint64_t* counts) {
+    if (!counts || (n && !d_values) || (reinterpret_cast<uintptr_t>(d_values) & 15)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg(cuda_stream);
+    unsigned long long* d = nullptr;
+    CK(cudaMallocAsync(&d, 386 * sizeof(unsigned long long), sg.s));
+    CK(cudaMemsetAsync(d, 0, 386 * sizeof(unsigned long long), sg.s));
+    if (n) component_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, sg.s>>>(d_values, n, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(counts, d, 386 * sizeof(uint64_t), cudaMemcpyDeviceToHost, sg.s));
+    CK(cudaFreeAsync(d, sg.s));
+    CK(cudaStreamSynchronize(sg.s));
+    counts[0] = n - counts[1];  // sign 0
+    return NZGPU_OK;
+}
+
+namespace {
+// shannon_entropy (entropy.hpp:41-55): same bins, order and arithmetic.
+double shannon(const uint64_t* c, int bins) {
+    uint64_t total = 0;
+    for (int i = 0; i < bins; ++i) total += c[i];
+    double h = 0.0;
+    const double n = static_cast<double>(total);
+    for (int i = 0; i < bins; ++i) {
+        if (c[i] == 0) continue;
+        const double p = static_cast<double>(c[i]) / n;
+        h -= p * std::log2(p);
+    }
+    return h < 0.0 ? 0.0 : h;
+}
+}  // namespace
+
+int nzgpu_entropy_from_histogram(const uint64_t* counts, double* out5) {
+    if (!counts || !out5) return NZGPU_INVALID_ARGUMENT;
+    if (counts[0] + counts[1] == 0) return NZGPU_INVALID_ARGUMENT;  // "entropy report: empty histogram"
+    // report_from_histogram (entropy.hpp:69-81)
+    const double hs = shannon(counts, 2), he = shannon(counts + 2, 256), hm = shannon(counts + 258, 128);
+    const double cap = 999.0, h = hs + he + hm;
+    out5[0] = hs;
+    out5[1] = he;
+    out5[2] = hm;
+    out5[3] = (h <= 16.0 / cap) ? cap : 16.0 / h;
+    out5[4] = 16.0 / (1.0 + he + 7.0);
+    return NZGPU_OK;
+}
+
+int nzgpu_entropy_report(const uint16_t* d_values, uint64_t n, void* cuda_stream, double* out5) {
+    if (n == 0) return NZGPU_INVALID_ARGUMENT;  // analyze_tensor: empty input
+    uint64_t counts[386];
+    if (int rc = nzgpu_component_histogram(d_values, n, cuda_stream, counts)) return rc;
+    return nzgpu_entropy_from_histogram(counts, out5);
+}
+
+int nzgpu_component_histogram_host(const uint16_t* values, uint64_t n, uint64_t* counts) {
+    if (!counts || (n && !values)) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint16_t* d = nullptr;
+    CK(cudaMallocAsync(&d, n * 2 + 16, sg.s));
+    if (n) CK(cudaMemcpyAsync(d, values, n * 2, cudaMemcpyHostToDevice, sg.s));
+    const int rc = nzgpu_component_histogram(d, n, sg.s, counts);
+    cudaFreeAsync(d, sg.s);
+    cudaStreamSynchronize(sg.s);
+    return rc;
+}
+
+int nzgpu_entropy_report_host(const uint16_t* values, uint64_t n, double* out5) {
+    if (n == 0 || !values) return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint16_t* d = nullptr;
+    CK(cudaMallocAsync(&d, n * 2 + 16, sg.s));
+    CK(cudaMemcpyAsync(d, values, n * 2, cudaMemcpyHostToDevice, sg.s));
+    const int rc = nzgpu_entropy_report(d, n, sg.s, out5);
+    cudaFreeAsync(d, sg.s);
+    cudaStreamSynchronize(sg.s);
+    return rc;
 }
 
 }  // extern "C"

@@ -150,6 +150,11 @@ SIGNATURES = {
     "nzgpu_blob_nzt_size": (_i, [_vp, _i, _p(_u64)]),
     "nzgpu_blob_write_nzt": (_i, [_vp, _p(_u64), _i, _vp, _u64, _p(_u64)]),
     "nzgpu_blob_read_nzt": (_i, [_vp, _u64, _u32, _vp, _p(_vp), _p(_u64), _p(_i)]),
+    "nzgpu_component_histogram": (_i, [_vp, _u64, _vp, _vp]),
+    "nzgpu_component_histogram_host": (_i, [_vp, _u64, _vp]),
+    "nzgpu_entropy_from_histogram": (_i, [_vp, _vp]),
+    "nzgpu_entropy_report": (_i, [_vp, _u64, _vp, _vp]),
+    "nzgpu_entropy_report_host": (_i, [_vp, _u64, _vp]),
 }
 
 

@@ -265,6 +265,18 @@ int main() {
         const Tensor tb = read_bft(ib);
         CHECK(tb.meta == t.meta && tb.values == t.values);
     }
+    {  // entropy.hpp: GPU histogram, host entropy arithmetic (gen_golden.cpp:22-33 values)
+        const auto g = gaussian(42, 1 << 20, 0.02);
+        const ComponentHistogram h = build_histogram(g);
+        ComponentHistogram cpu;
+        for (Bf16 v : g) cpu.add(v);
+        CHECK(h.sign_counts == cpu.sign_counts && h.exp_counts == cpu.exp_counts && h.mant_counts == cpu.mant_counts &&
+              h.total == cpu.total);
+        const EntropyReport r = analyze_tensor(g);
+        const EntropyReport rc = report_from_histogram(cpu);
+        CHECK(r.h_sign == rc.h_sign && r.h_exp == rc.h_exp && r.h_mant == rc.h_mant && r.ideal_ratio == rc.ideal_ratio);
+        CHECK(throws<std::invalid_argument>([] { (void)analyze_tensor(std::vector<Bf16>{}); }));
+    }
     std::printf("dropin_test: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
