@@ -67,7 +67,29 @@ def build(verbose: bool = False, defines=(), lib: str = LIB) -> str:
         out = subprocess.run(cmd, capture_output=True, text=True)
         if out.returncode != 0:
             raise RuntimeError(f"link failed:\n{out.stdout}\n{out.stderr}")
+    if lib == LIB:
+        build_cli()
     return lib
+
+
+CLI_SRC = os.path.join(HERE, "..", "tools", "neuzip_cli.cpp")
+CLI = os.path.join(HERE, "neuzip")
+
+
+def build_cli() -> str:
+    """The `neuzip` command-line tool (analyze / compress / decompress /
+    bench, proj/tools/neuzip.cpp) on the drop-in headers, linked against the
+    in-tree libnzgpu.so (rpath $ORIGIN)."""
+    deps = [CLI_SRC, LIB] + [os.path.join(HERE, "..", "include", "neuzip", f)
+                             for f in os.listdir(os.path.join(HERE, "..", "include", "neuzip"))]
+    if os.path.exists(CLI) and all(os.path.getmtime(CLI) >= os.path.getmtime(d) for d in deps):
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-Wall", "-Wextra", "-I", os.path.join(HERE, "..", "include"),
+           CLI_SRC, "-o", CLI, "-L", HERE, "-lnzgpu", "-Wl,-rpath,$ORIGIN"]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"neuzip CLI build failed:\n{out.stdout}\n{out.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":
