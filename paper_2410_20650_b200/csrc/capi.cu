@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -891,9 +892,47 @@ struct HostSlot {
     cudaStream_t s = nullptr;
     DevBuf main, stream, out;
     uint32_t* err = nullptr;
+    // Pinned staging for the host-built chunk table: a cudaMemcpyAsync from
+    // pageable memory may wait for the stream, which would serialise this
+    // slot's H2D behind the previous tensor's D2H.  A ring of buffers, so the
+    // host only ever waits for a copy issued four tensors ago.
+    static constexpr int kRing = 4;
+    uint4* info_h[kRing] = {};
+    uint64_t info_cap[kRing] = {};
+    cudaEvent_t info_done[kRing] = {};
+    bool info_pending[kRing] = {};
+    int ring = 0;
     ~HostSlot() {
         if (err) cudaFree(err);
+        for (int i = 0; i < kRing; ++i) {
+            if (info_h[i]) cudaFreeHost(info_h[i]);
+            if (info_done[i]) cudaEventDestroy(info_done[i]);
+        }
         if (s) cudaStreamDestroy(s);
+    }
+    // Copy `info` into the next ring buffer; returns it (the caller issues the
+    // H2D and then info_issued()).
+    int stage_info(const std::vector<uint4>& info, uint4** buf) {
+        const int r = ring;
+        if (info_pending[r]) CK(cudaEventSynchronize(info_done[r]));
+        info_pending[r] = false;
+        if (info.size() > info_cap[r]) {  // grow generously: pinned allocations synchronise
+            if (info_h[r]) CK(cudaFreeHost(info_h[r]));
+            info_h[r] = nullptr;
+            const uint64_t want = std::max<uint64_t>({info.size(), 2 * info_cap[r], 8192});
+            info_cap[r] = 0;
+            CK(cudaMallocHost(&info_h[r], want * sizeof(uint4)));
+            info_cap[r] = want;
+        }
+        std::memcpy(info_h[r], info.data(), info.size() * sizeof(uint4));
+        *buf = info_h[r];
+        return NZGPU_OK;
+    }
+    int info_issued() {
+        CK(cudaEventRecord(info_done[ring], s));
+        info_pending[ring] = true;
+        ring = (ring + 1) % kRing;
+        return NZGPU_OK;
     }
 };
 
@@ -903,6 +942,8 @@ struct HostCtx {
         for (HostSlot& sl : slot) {
             if (!sl.s) CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
             if (!sl.err) CK(cudaMalloc(&sl.err, 64));
+            for (auto& ev : sl.info_done)
+                if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         }
         return NZGPU_OK;
     }
@@ -951,7 +992,9 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     IndexHeader h;
     if (t->index_len < sizeof(h)) return 1;
     std::memcpy(&h, t->index, sizeof(h));
-    const uint32_t S = info[0].w;
+    // a tensor shorter than one chunk has a single, short chunk: its chunk
+    // size is the encoder's (from the index), not the first chunk's length
+    const uint32_t S = info.size() == 1 && info[0].w <= h.chunk_syms ? h.chunk_syms : info[0].w;
     const int log2k = log2_of(h.interval);
     if (h.magic != kIndexMagic || h.version != kIndexVersion || log2k < 0 || h.chunk_syms != S || h.n != t->n ||
         h.nchunks != info.size() || h.stream_len != t->stream_len || S % h.interval ||
@@ -1001,7 +1044,10 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     CK(cudaMemcpyAsync(b.stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
     if (b.mant_len) CK(cudaMemcpyAsync(b.mant, t->mantissas, b.mant_len, cudaMemcpyHostToDevice, s));
     if (b.scales_len) CK(cudaMemcpyAsync(b.scales, t->scales, b.scales_len, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.chunk_info, info.data(), info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    uint4* info_pinned = nullptr;
+    if (int rc = sl.stage_info(info, &info_pinned)) return rc;
+    CK(cudaMemcpyAsync(b.chunk_info, info_pinned, info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    if (int rc = sl.info_issued()) return rc;
     CK(cudaMemcpyAsync(b.ckpt, ck, b.nsub * sizeof(uint2), cudaMemcpyHostToDevice, s));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
@@ -1023,11 +1069,18 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
     HostCtx& h = *g_host;
     if (int rc = h.init()) return rc;
     for (HostSlot& sl : h.slot) CK(cudaMemsetAsync(sl.err, 0, 64, sl.s));
+    static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
+    double host_us = 0;
+    int general = 0;
+    const auto tcall = std::chrono::steady_clock::now();
     for (int i = 0; i < count; ++i) {
         HostSlot& sl = h.slot[i & 1];
         const nzgpu_host_tensor* t = ts + i;
+        const auto t0 = std::chrono::steady_clock::now();
         int rc = stage_and_decode(sl, t, outs[i]);
+        if (trace) host_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
         if (rc == 1) {
+            ++general;
             // General path (no/foreign index, irregular framing, or a format
             // error to report exactly): import with full validation.
             nzgpu_blob_s b;
@@ -1049,10 +1102,16 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
         }
     }
     int rc = NZGPU_OK;
+    const auto t1 = std::chrono::steady_clock::now();
     for (HostSlot& sl : h.slot) {
         const int r = sync_status(sl.s, sl.err, true);
         if (!rc) rc = r;
     }
+    if (trace)
+        std::fprintf(stderr, "nzgpu batch: %d tensors (%d general), host enqueue %.0f us, final wait %.0f us, call %.0f us\n",
+                     count, general, host_us,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t1).count(),
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tcall).count());
     return rc;
 }
 
