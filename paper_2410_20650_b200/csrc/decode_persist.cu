@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const bool fast_lossy = d.block_size >= 8 && !(d.flags & kFlagSlowLossy);
 
     if (threadIdx.x == 0) {
+        *reinterpret_cast<uint32_t*>(smem + 16) = ubeg + 2 * kPWarps;  // dynamic unit counter
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lut_bar));
         for (int w = 0; w < kPWarps; ++w) {
             const uint32_t r = sbase + kPHeader + kLutBytes + w * wregion;
@@ -394,13 +395,24 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         return L;
     };
 
-    uint32_t u = ubeg + warp;
+    // Units are handed out dynamically: each warp starts with units
+    // ubeg + warp and ubeg + kPWarps + warp, then takes the next free unit
+    // of the CTA's range from a shared counter, so warps that drew cheaper
+    // units take more and the CTA ends within about one unit of its average
+    // (a static round-robin left ~7 % of SM time idle in the tail).
+    uint32_t* s_next = reinterpret_cast<uint32_t*>(smem + 16);
+    auto grab = [&]() -> uint32_t {
+        uint32_t v = 0;
+        if (lane == 0) v = atomicAdd(s_next, 1u);
+        return __shfl_sync(0xFFFFFFFFu, v, 0);
+    };
+    uint32_t u = ubeg + warp, un = ubeg + kPWarps + warp, unn = 0;
     uint32_t wa_cur = 0, wa_nxt = 0;
     LaneJob cur{}, nxt{};
-    RawRec raw_n{};  // index records of unit u + kPWarps (loaded one iteration early)
+    RawRec raw_n{};  // index records of unit `un` (loaded one iteration early)
     if (u < uend) {
         const RawRec r0 = load_raw<LOG2K>(d, u * 32 + lane, nsub);
-        if (u + kPWarps < uend) raw_n = load_raw<LOG2K>(d, (u + kPWarps) * 32 + lane, nsub);
+        if (un < uend) raw_n = load_raw<LOG2K>(d, un * 32 + lane, nsub);
         cur = stage(u, 0, wa_cur, r0);
     }
     uint32_t tok = 0;
@@ -409,12 +421,14 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const uint32_t lutm = lutt - (1u << 26);
     (void)lutm;
 
-    for (uint32_t i = 0; u < uend; ++i, u += kPWarps) {
+    for (uint32_t i = 0; u < uend; ++i) {
         const int b = i & 1;
-        const uint32_t un = u + kPWarps;
         if (un < uend) {
             nxt = stage(un, b ^ 1, wa_nxt, raw_n);
-            if (un + kPWarps < uend) raw_n = load_raw<LOG2K>(d, (un + kPWarps) * 32 + lane, nsub);
+            unn = grab();
+            if (unn < uend) raw_n = load_raw<LOG2K>(d, unn * 32 + lane, nsub);
+        } else {
+            unn = uend;
         }
         const uint64_t sym0 = (uint64_t)u * 32 * K;
         const uint32_t unit_syms = (uint32_t)min((uint64_t)32 * K, d.n - sym0);
@@ -576,6 +590,8 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         __syncwarp();
         cur = nxt;
         wa_cur = wa_nxt;
+        u = un;
+        un = unn;
     }
     err = __reduce_or_sync(0xFFFFFFFFu, err);
     if (lane == 0 && err) atomicOr(d.err, err);
