@@ -118,6 +118,21 @@ int nzgpu_set_decode_kernel(int which);
  * exact stream allocation).  d_values must be 16-byte aligned. */
 int nzgpu_compress(const uint16_t* d_values, uint64_t n, int precision, uint32_t block_size,
                    uint32_t chunk_symbols, uint32_t interval, void* cuda_stream, nzgpu_blob* out);
+/* Compress `count` device tensors with one shared parameter set: out[i] is
+ * byte-identical to nzgpu_compress(d_values[i], n[i], ...).  One encode
+ * launch covers the chunks of every tensor (the per-chunk rANS chains are
+ * serial, so a whole layer or model must share a launch to fill the GPU), the
+ * stream is synchronised once for the batch (plus once for the decode window
+ * sizes) instead of twice per tensor, and the blobs of the batch share two
+ * device allocations (released with the last blob).  d_workspace (256-byte
+ * aligned, >= nzgpu_compress_batch_workspace_size bytes, about 3 bytes per
+ * element) holds the temporaries; NULL = stream-ordered allocation.  On
+ * error every out[i] is NULL. */
+int nzgpu_compress_batch_workspace_size(const uint64_t* n, int count, int precision, uint32_t chunk_symbols,
+                                        uint64_t* bytes);
+int nzgpu_compress_batch(const uint16_t* const* d_values, const uint64_t* n, int count, int precision,
+                         uint32_t block_size, uint32_t chunk_symbols, uint32_t interval, void* d_workspace,
+                         uint64_t workspace_bytes, void* cuda_stream, nzgpu_blob* out);
 /* Decompress into d_out (16-byte aligned, n bf16), asynchronously on
  * `stream`; errors are sticky in the blob until nzgpu_blob_status. */
 int nzgpu_decompress(nzgpu_blob blob, uint16_t* d_out, void* cuda_stream);

@@ -194,6 +194,48 @@ class DeviceBlob:
         return cls(h, meta)
 
     @classmethod
+    def compress_batch(cls, values: Sequence, precision: int = kLosslessPrecision,
+                       block_size: int = kDefaultBlockSize, chunk_symbols: int = kChunkSymbols,
+                       interval: int = 0, stream=None, metas: Optional[Sequence[TensorMeta]] = None,
+                       max_batch_elements: int = 1 << 32) -> list:
+        """Compress many CUDA tensors with one encode launch per batch
+        (nzgpu_compress_batch); result i is byte-identical to
+        ``compress(values[i], ...)``.  Batches are cut at
+        ``max_batch_elements`` (temporaries are ~3 B per element)."""
+        import torch
+
+        flat = []
+        for v in values:
+            if v.dtype == torch.bfloat16:
+                v = v.view(torch.int16)
+            flat.append(v.contiguous().view(-1))
+        out: list = []
+        i = 0
+        while i < len(flat):
+            j, tot = i, 0
+            while j < len(flat) and (j == i or tot + flat[j].numel() <= max_batch_elements):
+                tot += flat[j].numel()
+                j += 1
+            part = flat[i:j]
+            ptrs = (C.c_void_p * len(part))(*[t.data_ptr() for t in part])
+            ns = (C.c_uint64 * len(part))(*[t.numel() for t in part])
+            hs = (C.c_void_p * len(part))()
+            # temporaries from torch's caching allocator: repeated batches
+            # reuse the mapping instead of paying for fresh device memory
+            wsb = C.c_uint64()
+            N.check(N.lib.nzgpu_compress_batch_workspace_size(ns, len(part), precision, chunk_symbols,
+                                                              C.byref(wsb)), "compress_batch")
+            ws = torch.empty(wsb.value + 256, dtype=torch.uint8, device=part[0].device)
+            wp = (ws.data_ptr() + 255) & ~255
+            rc = N.lib.nzgpu_compress_batch(ptrs, ns, len(part), precision, block_size, chunk_symbols, interval,
+                                            C.c_void_p(wp), wsb.value, _stream_ptr(stream), hs)
+            N.check(rc, "compress_batch")
+            for k in range(len(part)):
+                out.append(cls(C.c_void_p(hs[k]), metas[i + k] if metas else None))
+            i = j
+        return out
+
+    @classmethod
     def from_host(cls, blob: Blob, interval: int = 0) -> "DeviceBlob":
         t, keep = _host_tensor(blob)
         h = C.c_void_p()

@@ -27,10 +27,9 @@ __global__ void split_hist_kernel(const uint16_t*, uint64_t, uint8_t*, uint8_t*,
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
-__global__ void ans_encode_kernel(const uint8_t*, uint64_t, uint32_t, uint32_t, const EncSym*, uint8_t*, uint64_t,
-                                  uint32_t*, uint2*, uint32_t*);
-__global__ void stream_scan_kernel(const uint32_t*, uint64_t, uint64_t, uint32_t, uint4*, uint8_t*,
-                                   unsigned long long*);
+__global__ void ans_encode_kernel(const EncTask*, int, const __grid_constant__ EncTask);
+__global__ void stream_scan_kernel(const EncTask*, const __grid_constant__ EncTask);
+__global__ void gather_u32_kernel(const uint32_t* const*, uint32_t*, int);
 __global__ void stream_copy_kernel(const uint8_t*, uint64_t, const uint4*, uint8_t*);
 __global__ void lossy_normalize_kernel(const uint16_t*, uint64_t, int, uint32_t, uint8_t*, uint8_t*, uint8_t*,
                                        uint32_t*);
@@ -203,11 +202,14 @@ struct nzgpu_blob_s {
     uint64_t stream_len = 0;
 
     bool owns = true;  // false: a descriptor over buffers owned by a host-pipeline slot
+    // Batched compress: base / stream sections live in allocations shared by
+    // the blobs of one batch, freed with the last of them.
+    std::shared_ptr<void> base_arena, stream_arena;
 
     ~nzgpu_blob_s() {
         if (!owns) return;
-        if (base) cudaFree(base);
-        if (stream) cudaFree(stream);
+        if (base && !base_arena) cudaFree(base);
+        if (stream && !stream_arena) cudaFree(stream);
     }
 
     DecodeDesc desc(uint16_t* out) const {
@@ -236,8 +238,22 @@ struct nzgpu_blob_s {
 
 namespace {
 
-// Allocate the main section block of a blob (everything but the stream).
-int blob_alloc(nzgpu_blob_s* b, bool irregular) {
+// Main section block of a blob (everything but the stream): its size, and
+// its carving from `at` (a fresh cudaMalloc when null).
+uint64_t blob_base_bytes(const nzgpu_blob_s* b, bool irregular) {
+    Carve cv;
+    cv.take(512);
+    cv.take(16384);
+    cv.take(std::max<uint64_t>(b->mant_len, 1) + 16);
+    cv.take(std::max<uint64_t>(b->scales_len, 1));
+    cv.take(std::max<uint64_t>(b->nchunks, 1) * sizeof(uint4));
+    cv.take(irregular ? std::max<uint64_t>(b->nchunks, 1) * 8 : 8);
+    cv.take(std::max<uint64_t>(b->nsub, 1) * sizeof(uint2) + 16);
+    cv.take(64);
+    return cv.size;
+}
+
+int blob_alloc(nzgpu_blob_s* b, bool irregular, uint8_t* at = nullptr) {
     Carve cv;
     const uint64_t o_freqs = cv.take(512);
     const uint64_t o_lut = cv.take(16384);
@@ -247,7 +263,11 @@ int blob_alloc(nzgpu_blob_s* b, bool irregular) {
     const uint64_t o_sym0 = cv.take(irregular ? std::max<uint64_t>(b->nchunks, 1) * 8 : 8);
     const uint64_t o_ckpt = cv.take(std::max<uint64_t>(b->nsub, 1) * sizeof(uint2) + 16);
     const uint64_t o_err = cv.take(64);
-    CK(cudaMalloc(&b->base, cv.size));
+    if (at) {
+        b->base = at;
+    } else {
+        CK(cudaMalloc(&b->base, cv.size));
+    }
     uint8_t* p = static_cast<uint8_t*>(b->base);
     b->freqs = reinterpret_cast<uint16_t*>(p + o_freqs);
     b->lut = reinterpret_cast<uint32_t*>(p + o_lut);
@@ -258,6 +278,14 @@ int blob_alloc(nzgpu_blob_s* b, bool irregular) {
     b->ckpt = reinterpret_cast<uint2*>(p + o_ckpt);
     b->err = reinterpret_cast<uint32_t*>(p + o_err);
     b->scratch_u32 = b->err + 4;
+    return NZGPU_OK;
+}
+
+// One device allocation shared by the blobs of a batch (freed with the last).
+int arena_alloc(uint64_t bytes, std::shared_ptr<void>& out) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<uint64_t>(bytes, 256)));
+    out = std::shared_ptr<void>(p, [](void* q) { cudaFree(q); });
     return NZGPU_OK;
 }
 
@@ -317,19 +345,48 @@ int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
     return NZGPU_OK;
 }
 
-int compute_window(nzgpu_blob_s* b, cudaStream_t s) {
-    b->max_window = b->max_window_unit = 0;
-    if ((b->flags & kFlagIrregular) || b->nsub == 0 || (b->flags & kFlagSingleSymbol)) return NZGPU_OK;
-    CK(cudaMemsetAsync(b->scratch_u32 + 2, 0, 8, s));
-    CK(launch_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 3, s));
-    CK(launch_unit_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 2, s));
-    uint32_t w[2];
-    CK(cudaMemcpyAsync(w, b->scratch_u32 + 2, 8, cudaMemcpyDeviceToHost, s));
+// Largest payload window per decode tile / warp unit of each blob (sizes the
+// decoders' shared-memory windows): the window kernels of every blob, then one
+// readback.
+int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s) {
+    std::vector<const uint32_t*> ptrs;
+    std::vector<int> who;
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = bs[i];
+        b->max_window = b->max_window_unit = 0;
+        if ((b->flags & kFlagIrregular) || b->nsub == 0 || (b->flags & kFlagSingleSymbol)) continue;
+        CK(cudaMemsetAsync(b->scratch_u32 + 2, 0, 8, s));
+        CK(launch_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 3, s));
+        CK(launch_unit_window_max(b->log2k, b->desc(nullptr), b->scratch_u32 + 2, s));
+        ptrs.push_back(b->scratch_u32 + 2);
+        ptrs.push_back(b->scratch_u32 + 3);
+        who.push_back(i);
+    }
+    if (who.empty()) return NZGPU_OK;
+    std::vector<uint32_t> w(ptrs.size());
+    if (who.size() == 1) {
+        CK(cudaMemcpyAsync(w.data(), ptrs[0], 8, cudaMemcpyDeviceToHost, s));
+    } else {
+        uint8_t* tmp = nullptr;
+        const uint64_t pb = align_up(ptrs.size() * sizeof(void*), 256);
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), pb + ptrs.size() * 4, s));
+        CK(cudaMemcpyAsync(tmp, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+        gather_u32_kernel<<<grid_for(ptrs.size(), 256), 256, 0, s>>>(reinterpret_cast<const uint32_t* const*>(tmp),
+                                                                      reinterpret_cast<uint32_t*>(tmp + pb),
+                                                                      (int)ptrs.size());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(w.data(), tmp + pb, w.size() * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(tmp, s));
+    }
     CK(cudaStreamSynchronize(s));
-    b->max_window_unit = w[0];
-    b->max_window = w[1];
+    for (size_t j = 0; j < who.size(); ++j) {
+        bs[who[j]]->max_window_unit = w[2 * j];
+        bs[who[j]]->max_window = w[2 * j + 1];
+    }
     return NZGPU_OK;
 }
+
+int compute_window(nzgpu_blob_s* b, cudaStream_t s) { return compute_windows(&b, 1, s); }
 
 // Persistent-kernel geometry: 32-sub-range units, `upc` units per CTA so
 // that the grid is about one resident wave.
@@ -468,11 +525,50 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
     return compute_window(b, s);
 }
 
-int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision, uint32_t block,
-                  uint32_t chunk_syms, uint32_t interval, cudaStream_t s) {
-    if (!valid_precision(precision) || n == 0 || !v) return NZGPU_INVALID_ARGUMENT;  // tensorstore.hpp:47-53
-    if (precision != 7 && block == 0) return NZGPU_INVALID_ARGUMENT;              // tensorstore.hpp:146-148
-    if (reinterpret_cast<uintptr_t>(v) & 15) return NZGPU_INVALID_ARGUMENT;
+// Workspace layout of a batched compress: per-tensor exponent plane, lossy
+// items, worst-case payload slots, histogram, payload lengths, stream length,
+// encoder constants and stream header, then the task / readback arrays.
+struct BatchLayout {
+    struct Tmp {
+        uint64_t exps, items, scratch, counts, plen, total, enc, hdr;
+    };
+    std::vector<Tmp> to;
+    uint64_t tasks = 0, ptrs = 0, res = 0, size = 0, slot = 0;
+    BatchLayout(const uint64_t* ns, int count, int precision, uint32_t chunk_syms) : to(count) {
+        slot = align_up(2ull * chunk_syms + 8, 16);
+        Carve cv;
+        for (int i = 0; i < count; ++i) {
+            const uint64_t n = ns[i], nchunks = ceil_div(n, chunk_syms);
+            to[i].exps = cv.take(n + 16);
+            to[i].items = cv.take(precision == 7 ? 16 : n + 16);
+            to[i].scratch = cv.take(nchunks * slot + 16);
+            to[i].counts = cv.take(256 * 8);
+            to[i].plen = cv.take(nchunks * 4);
+            to[i].total = cv.take(16);
+            to[i].enc = cv.take(256 * sizeof(EncSym));
+            to[i].hdr = cv.take(16);
+        }
+        tasks = cv.take(count * sizeof(EncTask));
+        ptrs = cv.take(count * 6 * sizeof(void*));
+        res = cv.take(count * 6 * 4);
+        size = cv.size;
+    }
+};
+
+// Compress `count` tensors in one pipeline: per-tensor split / histogram /
+// table kernels, ONE K3 launch over the chunks of every tensor (the chunk
+// chains are serial and latency-bound, so tensors must share a launch to fill
+// the GPU), one K4 scan launch, then a single host synchronisation to learn
+// the stream lengths before the streams are allocated and compacted.  The
+// blobs of a batch share two allocations (sections, streams): per-blob
+// cudaMalloc calls cost more than the kernels.  `ws` (ws_bytes >=
+// BatchLayout::size) holds the temporaries; null = stream-ordered allocation.
+// On error every blob is left empty (the caller frees them).
+int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint64_t* ns, int count, int precision,
+                  uint32_t block, uint32_t chunk_syms, uint32_t interval, cudaStream_t s, void* ws = nullptr,
+                  uint64_t ws_bytes = 0) {
+    if (count <= 0 || !valid_precision(precision)) return NZGPU_INVALID_ARGUMENT;
+    if (precision != 7 && block == 0) return NZGPU_INVALID_ARGUMENT;  // tensorstore.hpp:146-148
     if (chunk_syms == 0) chunk_syms = kDefaultChunk;
     // interval 0 = auto: the default stride if it divides S, else 64; chunk
     // sizes divisible by neither keep the reference format but decode with
@@ -484,76 +580,169 @@ int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision,
     }
     const int log2k = log2_of(interval);
     if (log2k < 0 || (!irregular && chunk_syms % interval)) return NZGPU_INVALID_ARGUMENT;
-    if (ceil_div(n, interval) >= 0xFFFFFFFFull) return NZGPU_INVALID_ARGUMENT;  // 32-bit sub-range ids
-    b->n = n;
-    b->precision = precision;
-    b->block = precision == 7 ? 0 : block;
-    b->chunk_syms = chunk_syms;
-    b->interval = interval;
-    b->log2k = log2k;
-    b->nchunks = ceil_div(n, chunk_syms);
-    b->nsub = ceil_div(n, interval);
-    b->mant_len = mant_bytes(n, precision);
-    b->scales_len = precision == 7 ? 0 : ceil_div(n, block);
-    b->flags = 0;
-    int rc = blob_alloc(b, false);
-    if (rc) return rc;
-    // Temporaries (stream-ordered allocator).
-    const uint64_t slot = align_up(2ull * chunk_syms + 8, 16);
-    Carve cv;
-    const uint64_t o_exps = cv.take(n + 16);
-    const uint64_t o_items = cv.take(precision == 7 ? 16 : n + 16);
-    const uint64_t o_scratch = cv.take(b->nchunks * slot + 16);
-    const uint64_t o_counts = cv.take(256 * 8);
-    const uint64_t o_plen = cv.take(b->nchunks * 4);
-    const uint64_t o_total = cv.take(16);
-    const uint64_t o_enc = cv.take(256 * sizeof(EncSym));
-    const uint64_t o_hdr = cv.take(16);
-    uint8_t* tmp = nullptr;
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), cv.size, s));
-    uint8_t* exps = tmp + o_exps;
-    uint8_t* items = tmp + o_items;
-    uint8_t* scratch = tmp + o_scratch;
-    auto* counts = reinterpret_cast<unsigned long long*>(tmp + o_counts);
-    auto* plen = reinterpret_cast<uint32_t*>(tmp + o_plen);
-    auto* total = reinterpret_cast<unsigned long long*>(tmp + o_total);
-    auto* enc = reinterpret_cast<EncSym*>(tmp + o_enc);
-    uint8_t* hdr = tmp + o_hdr;
-    CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
-    CK(cudaMemsetAsync(b->err, 0, 64, s));
-    if (precision == 7) {
-        split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>(v, n, exps, b->mant, counts);
-    } else {
-        lossy_normalize_kernel<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, s>>>(v, n, precision, block,
-                                                                                       b->scales, exps, items, b->err);
-        byte_hist_kernel<<<grid_for(n / 16 + 1, 256), 256, 0, s>>>(exps, n, counts);
-        pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
+    for (int i = 0; i < count; ++i) {
+        if (!bs[i] || ns[i] == 0 || !vs[i]) return NZGPU_INVALID_ARGUMENT;  // tensorstore.hpp:47-53
+        if (reinterpret_cast<uintptr_t>(vs[i]) & 15) return NZGPU_INVALID_ARGUMENT;
+        if (ceil_div(ns[i], interval) >= 0xFFFFFFFFull) return NZGPU_INVALID_ARGUMENT;  // 32-bit sub-range ids
     }
-    build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
-    ans_encode_kernel<<<grid_for(b->nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(
-        exps, n, chunk_syms, (uint32_t)log2k, enc, scratch, slot, plen, irregular ? nullptr : b->ckpt, b->err);
-    stream_scan_kernel<<<1, 1024, 0, s>>>(plen, b->nchunks, n, chunk_syms, b->chunk_info, hdr, total);
+    static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
+    auto tlast = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[nzgpu] compress_many(%d) %-10s %9.1f us\n", count, what,
+                     std::chrono::duration<double, std::micro>(now - tlast).count());
+        tlast = now;
+    };
+    const BatchLayout L(ns, count, precision, chunk_syms);
+    const uint64_t slot = L.slot;
+    if (ws && (ws_bytes < L.size || (reinterpret_cast<uintptr_t>(ws) & 255))) return NZGPU_INVALID_ARGUMENT;
+    uint8_t* tmp = static_cast<uint8_t*>(ws);
+    if (!tmp) CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), L.size, s));
+    struct TmpGuard {
+        uint8_t* p;
+        cudaStream_t s;
+        ~TmpGuard() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } guard{ws ? nullptr : tmp, s};
+    mark("tmp alloc");
+    // Section block of every blob: one shared allocation for a batch.
+    std::vector<uint64_t> boff(count);
+    uint64_t btotal = 0;
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = bs[i];
+        const uint64_t n = ns[i];
+        b->n = n;
+        b->precision = precision;
+        b->block = precision == 7 ? 0 : block;
+        b->chunk_syms = chunk_syms;
+        b->interval = interval;
+        b->log2k = log2k;
+        b->nchunks = ceil_div(n, chunk_syms);
+        b->nsub = ceil_div(n, interval);
+        b->mant_len = mant_bytes(n, precision);
+        b->scales_len = precision == 7 ? 0 : ceil_div(n, block);
+        b->flags = 0;
+        boff[i] = btotal;
+        btotal += align_up(blob_base_bytes(b, false), 256);
+    }
+    std::shared_ptr<void> base_arena;
+    if (count > 1) {
+        if (int rc = arena_alloc(btotal, base_arena)) return rc;
+    }
+    mark("blob alloc");
+    std::vector<EncTask> tasks(count);
+    uint32_t ctas = 0;
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = bs[i];
+        const uint64_t n = ns[i];
+        if (base_arena) {
+            b->base_arena = base_arena;
+            blob_alloc(b, false, static_cast<uint8_t*>(base_arena.get()) + boff[i]);
+        } else if (int rc = blob_alloc(b, false)) {
+            return rc;
+        }
+        uint8_t* exps = tmp + L.to[i].exps;
+        auto* counts = reinterpret_cast<unsigned long long*>(tmp + L.to[i].counts);
+        auto* enc = reinterpret_cast<EncSym*>(tmp + L.to[i].enc);
+        CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
+        CK(cudaMemsetAsync(b->err, 0, 64, s));
+        if (precision == 7) {
+            split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>(vs[i], n, exps, b->mant, counts);
+        } else {
+            uint8_t* items = tmp + L.to[i].items;
+            lossy_normalize_kernel<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, s>>>(
+                vs[i], n, precision, block, b->scales, exps, items, b->err);
+            byte_hist_kernel<<<grid_for(n / 16 + 1, 256), 256, 0, s>>>(exps, n, counts);
+            pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
+        }
+        build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
+        EncTask& t = tasks[i];
+        t = EncTask{};
+        t.exps = exps;
+        t.enc = enc;
+        t.scratch = tmp + L.to[i].scratch;
+        t.plen = reinterpret_cast<uint32_t*>(tmp + L.to[i].plen);
+        t.ckpt = irregular ? nullptr : b->ckpt;
+        t.err = b->err;
+        t.chunk_info = b->chunk_info;
+        t.hdr = tmp + L.to[i].hdr;
+        t.total = reinterpret_cast<unsigned long long*>(tmp + L.to[i].total);
+        t.n = n;
+        t.slot_bytes = slot;
+        t.chunk_syms = chunk_syms;
+        t.log2k = (uint32_t)log2k;
+        t.cta0 = ctas;
+        const uint64_t c = ceil_div(b->nchunks, NZ_ENC_THREADS);
+        if (ctas + c >= (1ull << 31)) return NZGPU_INVALID_ARGUMENT;
+        ctas += (uint32_t)c;
+    }
+    mark("setup");
+    auto* d_tasks = reinterpret_cast<EncTask*>(tmp + L.tasks);
+    if (count > 1) CK(cudaMemcpyAsync(d_tasks, tasks.data(), count * sizeof(EncTask), cudaMemcpyHostToDevice, s));
+    ans_encode_kernel<<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
+    stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);
     CK(cudaGetLastError());
-    uint32_t info[3] = {0, 0, 0};
-    uint32_t err_bits = 0;
-    unsigned long long stream_len = 0;
-    CK(cudaMemcpyAsync(info, b->scratch_u32, 12, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&err_bits, b->err, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&stream_len, total, 8, cudaMemcpyDeviceToHost, s));
+    // One readback for every tensor: table info[3], error bits, stream length.
+    std::vector<const uint32_t*> ptrs(count * 6);
+    for (int i = 0; i < count; ++i) {
+        const uint32_t* tot = reinterpret_cast<const uint32_t*>(tasks[i].total);
+        const uint32_t* src[6] = {bs[i]->scratch_u32, bs[i]->scratch_u32 + 1, bs[i]->scratch_u32 + 2,
+                                  bs[i]->err, tot, tot + 1};
+        for (int k = 0; k < 6; ++k) ptrs[i * 6 + k] = src[k];
+    }
+    auto* d_ptrs = reinterpret_cast<const uint32_t**>(tmp + L.ptrs);
+    auto* d_res = reinterpret_cast<uint32_t*>(tmp + L.res);
+    CK(cudaMemcpyAsync(d_ptrs, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+    gather_u32_kernel<<<grid_for(count * 6, 256), 256, 0, s>>>(d_ptrs, d_res, count * 6);
+    CK(cudaGetLastError());
+    std::vector<uint32_t> res(count * 6);
+    CK(cudaMemcpyAsync(res.data(), d_res, res.size() * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (err_bits | info[2]) {
-        cudaFreeAsync(tmp, s);
-        return status_from_bits(err_bits | info[2]);
+    mark("encode");
+    for (int i = 0; i < count; ++i) {
+        const uint32_t* r = &res[i * 6];
+        if (r[3] | r[2]) return status_from_bits(r[3] | r[2]);
     }
-    b->flags = (info[0] & (kFlagSingleSymbol | kFlagHas255)) | (irregular ? kFlagIrregular : 0u);
-    b->single_symbol = info[1];
-    b->stream_len = stream_len;
-    CK(cudaMalloc(reinterpret_cast<void**>(&b->stream), align_up(stream_len, 16) + 32));
-    CK(cudaMemcpyAsync(b->stream, hdr, 4, cudaMemcpyDeviceToDevice, s));
-    stream_copy_kernel<<<(unsigned)b->nchunks, 256, 0, s>>>(scratch, slot, b->chunk_info, b->stream);
-    CK(cudaGetLastError());
-    CK(cudaFreeAsync(tmp, s));
-    return compute_window(b, s);
+    std::vector<uint64_t> soff(count);
+    uint64_t stotal = 0;
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = bs[i];
+        const uint32_t* r = &res[i * 6];
+        b->flags = (r[0] & (kFlagSingleSymbol | kFlagHas255)) | (irregular ? kFlagIrregular : 0u);
+        b->single_symbol = r[1];
+        b->stream_len = (uint64_t)r[4] | ((uint64_t)r[5] << 32);
+        soff[i] = stotal;
+        stotal += align_up(align_up(b->stream_len, 16) + 32, 256);
+    }
+    std::shared_ptr<void> stream_arena;
+    if (count > 1) {
+        if (int rc = arena_alloc(stotal, stream_arena)) return rc;
+    }
+    for (int i = 0; i < count; ++i) {
+        nzgpu_blob_s* b = bs[i];
+        if (stream_arena) {
+            b->stream_arena = stream_arena;
+            b->stream = static_cast<uint8_t*>(stream_arena.get()) + soff[i];
+        } else {
+            CK(cudaMalloc(reinterpret_cast<void**>(&b->stream), align_up(b->stream_len, 16) + 32));
+        }
+        CK(cudaMemcpyAsync(b->stream, tasks[i].hdr, 4, cudaMemcpyDeviceToDevice, s));
+        stream_copy_kernel<<<(unsigned)b->nchunks, 256, 0, s>>>(tasks[i].scratch, slot, b->chunk_info, b->stream);
+        CK(cudaGetLastError());
+    }
+    mark("streams");
+    const int rc = compute_windows(bs, count, s);
+    // a caller's workspace must be free to reuse when this returns
+    if (ws) CK(cudaStreamSynchronize(s));
+    mark("windows");
+    return rc;
+}
+
+int compress_into(nzgpu_blob_s* b, const uint16_t* v, uint64_t n, int precision, uint32_t block,
+                  uint32_t chunk_syms, uint32_t interval, cudaStream_t s) {
+    return compress_many(&b, &v, &n, 1, precision, block, chunk_syms, interval, s);
 }
 
 // Device-tier calls run on the caller's stream (NULL = the legacy default
@@ -685,6 +874,37 @@ int nzgpu_compress(const uint16_t* d_values, uint64_t n, int precision, uint32_t
     if (sg.own) cudaStreamSynchronize(sg.s);
     if (rc) return rc;
     *out = b.release();
+    return NZGPU_OK;
+}
+
+int nzgpu_compress_batch_workspace_size(const uint64_t* n, int count, int precision, uint32_t chunk_symbols,
+                                        uint64_t* bytes) {
+    if (!bytes || count <= 0 || !n || !valid_precision(precision)) return NZGPU_INVALID_ARGUMENT;
+    *bytes = BatchLayout(n, count, precision, chunk_symbols ? chunk_symbols : kDefaultChunk).size;
+    return NZGPU_OK;
+}
+
+int nzgpu_compress_batch(const uint16_t* const* d_values, const uint64_t* n, int count, int precision,
+                         uint32_t block_size, uint32_t chunk_symbols, uint32_t interval, void* d_workspace,
+                         uint64_t workspace_bytes, void* cuda_stream, nzgpu_blob* out) {
+    if (!out || count <= 0 || !d_values || !n) return NZGPU_INVALID_ARGUMENT;
+    for (int i = 0; i < count; ++i) out[i] = nullptr;
+    if (int rc = device_ready()) return rc;
+    std::vector<std::unique_ptr<nzgpu_blob_s>> bs(count);
+    std::vector<nzgpu_blob_s*> raw(count);
+    for (int i = 0; i < count; ++i) {
+        bs[i].reset(new (std::nothrow) nzgpu_blob_s);
+        if (!bs[i]) return NZGPU_OUT_OF_MEMORY;
+        raw[i] = bs[i].get();
+    }
+    StreamGuard sg(cuda_stream);
+    const int rc = compress_many(raw.data(), d_values, n, count, precision, block_size, chunk_symbols, interval, sg.s,
+                                 d_workspace, workspace_bytes);
+    if (rc) {
+        cudaStreamSynchronize(sg.s);  // in-flight kernels may still write the blobs' buffers
+        return rc;
+    }
+    for (int i = 0; i < count; ++i) out[i] = bs[i].release();
     return NZGPU_OK;
 }
 
@@ -1194,12 +1414,20 @@ int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* fr
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, reinterpret_cast<uint16_t*>(tmp + o_fr), nullptr,
                                          reinterpret_cast<EncSym*>(tmp + o_enc), nullptr, meta);
     // The raw coder needs no side index: checkpoints off.
-    ans_encode_kernel<<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(
-        tmp + o_sym, n, chunk_symbols, 0u, reinterpret_cast<EncSym*>(tmp + o_enc), tmp + o_scr, slot,
-        reinterpret_cast<uint32_t*>(tmp + o_plen), nullptr, meta + 4);
-    stream_scan_kernel<<<1, 1024, 0, s>>>(reinterpret_cast<uint32_t*>(tmp + o_plen), nchunks, n, chunk_symbols,
-                                          reinterpret_cast<uint4*>(tmp + o_info), tmp + o_hdr,
-                                          reinterpret_cast<unsigned long long*>(tmp + o_tot));
+    EncTask t{};
+    t.exps = tmp + o_sym;
+    t.enc = reinterpret_cast<EncSym*>(tmp + o_enc);
+    t.scratch = tmp + o_scr;
+    t.plen = reinterpret_cast<uint32_t*>(tmp + o_plen);
+    t.err = meta + 4;
+    t.chunk_info = reinterpret_cast<uint4*>(tmp + o_info);
+    t.hdr = tmp + o_hdr;
+    t.total = reinterpret_cast<unsigned long long*>(tmp + o_tot);
+    t.n = n;
+    t.slot_bytes = slot;
+    t.chunk_syms = chunk_symbols;
+    ans_encode_kernel<<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(nullptr, 1, t);
+    stream_scan_kernel<<<1, 1024, 0, s>>>(nullptr, t);
     CK(cudaGetLastError());
     uint32_t m[8];
     unsigned long long total = 0;

@@ -21,24 +21,34 @@
 
 namespace nzgpu {
 
-__global__ void __launch_bounds__(128) ans_encode_kernel(const uint8_t* __restrict__ exps, uint64_t n,
-                                                         uint32_t chunk_syms, uint32_t log2_interval,
-                                                         const EncSym* __restrict__ enc_g,
-                                                         uint8_t* __restrict__ scratch,
-                                                         uint64_t slot_bytes,
-                                                         uint32_t* __restrict__ payload_len,
-                                                         uint2* __restrict__ ckpt,
-                                                         uint32_t* __restrict__ err) {
+// Task of CTA `blk`: the last task whose first CTA is <= blk (tasks are in
+// launch order); `one` stands in for a device array when ntasks == 1.
+__device__ __forceinline__ const EncTask& task_of(const EncTask* tasks, int ntasks, const EncTask& one, uint32_t blk) {
+    if (!tasks) return one;
+    int lo = 0, hi = ntasks - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tasks[mid].cta0 <= blk) lo = mid; else hi = mid - 1;
+    }
+    return tasks[lo];
+}
+
+__global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restrict__ tasks, int ntasks,
+                                                         const __grid_constant__ EncTask one) {
     __shared__ EncSym enc[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) enc[i] = enc_g[i];
+    const EncTask& t = task_of(tasks, ntasks, one, blockIdx.x);
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) enc[i] = t.enc[i];
     __syncthreads();
+    const uint64_t n = t.n;
+    const uint32_t chunk_syms = t.chunk_syms, log2_interval = t.log2k;
+    uint2* const ckpt = t.ckpt;
     const uint64_t nchunks = ceil_div(n, chunk_syms);
-    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t c = (blockIdx.x - t.cta0) * (uint64_t)blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
     const uint64_t begin = c * chunk_syms;
     const uint32_t len = (uint32_t)min((uint64_t)chunk_syms, n - begin);
-    uint8_t* const slot_end = scratch + (c + 1) * slot_bytes;  // 16-byte aligned
-    const uint8_t* src = exps + begin;
+    uint8_t* const slot_end = t.scratch + (c + 1) * t.slot_bytes;  // 16-byte aligned
+    const uint8_t* src = t.exps + begin;
 
     uint32_t x = kStateLow;
     uint32_t emitted = 0;
@@ -97,23 +107,27 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const uint8_t* __restri
         }
     }
     if (bad) {
-        atomicOr(err, kErrZeroFreq);
+        atomicOr(t.err, kErrZeroFreq);
         return;
     }
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
-    payload_len[c] = emitted + 4;
+    t.plen[c] = emitted + 4;
 }
 
 // Exclusive scan of (8 + len) over chunks -> chunk_info {off_lo, off_hi,
 // len, nsym}; writes the stream's leading u32 chunk count and the total
-// stream length.  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) stream_scan_kernel(const uint32_t* __restrict__ payload_len,
-                                                           uint64_t nchunks, uint64_t n,
-                                                           uint32_t chunk_syms,
-                                                           uint4* __restrict__ chunk_info,
-                                                           uint8_t* __restrict__ stream,
-                                                           unsigned long long* __restrict__ total_out) {
+// stream length.  One CTA of 1024 threads per task (blockIdx.x).
+__global__ void __launch_bounds__(1024) stream_scan_kernel(const EncTask* __restrict__ tasks,
+                                                           const __grid_constant__ EncTask one) {
+    const EncTask& t = tasks ? tasks[blockIdx.x] : one;
+    const uint32_t* __restrict__ payload_len = t.plen;
+    const uint64_t n = t.n;
+    const uint32_t chunk_syms = t.chunk_syms;
+    const uint64_t nchunks = ceil_div(n, chunk_syms);
+    uint4* __restrict__ chunk_info = t.chunk_info;
+    uint8_t* __restrict__ stream = t.hdr;
+    unsigned long long* __restrict__ total_out = t.total;
     __shared__ unsigned long long warp_sums[32];
     __shared__ unsigned long long carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -191,6 +205,12 @@ __global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restr
         d[w] = mis ? __funnelshift_r(lo, hi, 8 * mis) : lo;
     }
     for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+}
+
+// dst[i] = *src[i]: one readback of scattered per-tensor result words.
+__global__ void gather_u32_kernel(const uint32_t* const* __restrict__ src, uint32_t* __restrict__ dst, int count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) dst[i] = *src[i];
 }
 
 }  // namespace nzgpu

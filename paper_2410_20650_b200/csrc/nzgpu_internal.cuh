@@ -58,6 +58,27 @@ struct EncSym {
     uint32_t pad;  // shift 31 + l: x / f = (x * m) >> shift for x < 2^31
 };
 
+// One tensor of a (batched) encode launch: K3 encodes its chunks into
+// per-chunk scratch slots, K4 scans and compacts them.  A launch covers many
+// tensors so that their chunk chains run concurrently (one chain per thread).
+struct EncTask {
+    const uint8_t* exps;     // exponent symbols, n bytes
+    const EncSym* enc;       // 256 encoder constants
+    uint8_t* scratch;        // nchunks slots of slot_bytes (16-B aligned)
+    uint32_t* plen;          // payload length per chunk
+    uint2* ckpt;             // checkpoint index, or nullptr
+    uint32_t* err;           // sticky error word
+    uint4* chunk_info;       // K4 out: {off lo, off hi, len, nsym}
+    uint8_t* hdr;            // K4 out: the stream's leading u32 chunk count
+    unsigned long long* total;  // K4 out: serialized stream length
+    uint64_t n;
+    uint64_t slot_bytes;
+    uint32_t chunk_syms;
+    uint32_t log2k;
+    uint32_t cta0;           // first K3 CTA of this tensor in the launch
+    uint32_t pad_;
+};
+
 // Device view of one compressed tensor, as the decode kernels consume it.
 struct DecodeDesc {
     const uint8_t* stream;        // serialized stream (reference layout), 16-B aligned + 16 B pad

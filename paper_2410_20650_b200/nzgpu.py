@@ -120,6 +120,8 @@ SIGNATURES = {
     "nzgpu_last_error_message": (C.c_char_p, []),
     "nzgpu_set_decode_kernel": (_i, [_i]),
     "nzgpu_compress": (_i, [_vp, _u64, _i, _u32, _u32, _u32, _vp, _p(_vp)]),
+    "nzgpu_compress_batch_workspace_size": (_i, [_p(_u64), _i, _i, _u32, _p(_u64)]),
+    "nzgpu_compress_batch": (_i, [_p(_vp), _p(_u64), _i, _i, _u32, _u32, _u32, _vp, _u64, _vp, _p(_vp)]),
     "nzgpu_decompress": (_i, [_vp, _vp, _vp]),
     "nzgpu_blob_status": (_i, [_vp, _vp]),
     "nzgpu_blob_info_get": (_i, [_vp, _p(BlobInfo)]),
