@@ -24,11 +24,14 @@
 namespace nzgpu {
 // kernels (split_table.cu, encode.cu, lossy.cu, decode.cu)
 __global__ void split_hist_kernel(const uint16_t*, uint64_t, uint8_t*, uint8_t*, unsigned long long*);
+cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, unsigned long long*, cudaStream_t);
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
+template <bool QUEUE>
 __global__ void ans_encode_kernel(const EncTask*, int, const __grid_constant__ EncTask);
 __global__ void stream_scan_kernel(const EncTask*, const __grid_constant__ EncTask);
+__global__ void build_tables_kernel(const TableTask*);
 __global__ void gather_u32_kernel(const uint32_t* const*, uint32_t*, int);
 __global__ void stream_copy_kernel(const uint8_t*, uint64_t, const uint4*, uint8_t*);
 __global__ void lossy_normalize_kernel(const uint16_t*, uint64_t, int, uint32_t, uint8_t*, uint8_t*, uint8_t*,
@@ -69,6 +72,10 @@ namespace {
 #ifndef NZ_ENC_THREADS
 #define NZ_ENC_THREADS 32
 #endif
+#ifndef NZ_ENC_QUEUE_MIN_CTAS
+#define NZ_ENC_QUEUE_MIN_CTAS 600
+#endif
+constexpr uint32_t kEncQueueMinCtas = NZ_ENC_QUEUE_MIN_CTAS;
 
 int g_kernel = -1;  // -1: from the environment
 bool use_persist() {
@@ -533,7 +540,7 @@ struct BatchLayout {
         uint64_t exps, items, scratch, counts, plen, total, enc, hdr;
     };
     std::vector<Tmp> to;
-    uint64_t tasks = 0, ptrs = 0, res = 0, size = 0, slot = 0;
+    uint64_t tasks = 0, tables = 0, ptrs = 0, res = 0, size = 0, slot = 0;
     BatchLayout(const uint64_t* ns, int count, int precision, uint32_t chunk_syms) : to(count) {
         slot = align_up(2ull * chunk_syms + 8, 16);
         Carve cv;
@@ -549,6 +556,7 @@ struct BatchLayout {
             to[i].hdr = cv.take(16);
         }
         tasks = cv.take(count * sizeof(EncTask));
+        tables = cv.take(count * sizeof(TableTask));
         ptrs = cv.take(count * 6 * sizeof(void*));
         res = cv.take(count * 6 * 4);
         size = cv.size;
@@ -633,6 +641,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     }
     mark("blob alloc");
     std::vector<EncTask> tasks(count);
+    std::vector<TableTask> tables(count);
     uint32_t ctas = 0;
     for (int i = 0; i < count; ++i) {
         nzgpu_blob_s* b = bs[i];
@@ -649,7 +658,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
         CK(cudaMemsetAsync(b->err, 0, 64, s));
         if (precision == 7) {
-            split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>(vs[i], n, exps, b->mant, counts);
+            CK(launch_split_hist(vs[i], n, exps, b->mant, counts, s));
         } else {
             uint8_t* items = tmp + L.to[i].items;
             lossy_normalize_kernel<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, s>>>(
@@ -657,7 +666,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
             byte_hist_kernel<<<grid_for(n / 16 + 1, 256), 256, 0, s>>>(exps, n, counts);
             pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
         }
-        build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
+        tables[i] = TableTask{counts, b->freqs, enc, b->lut, b->scratch_u32};
+        if (count == 1) build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);
         EncTask& t = tasks[i];
         t = EncTask{};
         t.exps = exps;
@@ -680,8 +690,18 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     }
     mark("setup");
     auto* d_tasks = reinterpret_cast<EncTask*>(tmp + L.tasks);
-    if (count > 1) CK(cudaMemcpyAsync(d_tasks, tasks.data(), count * sizeof(EncTask), cudaMemcpyHostToDevice, s));
-    ans_encode_kernel<<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
+    if (count > 1) {
+        auto* d_tables = reinterpret_cast<TableTask*>(tmp + L.tables);
+        CK(cudaMemcpyAsync(d_tables, tables.data(), count * sizeof(TableTask), cudaMemcpyHostToDevice, s));
+        build_tables_kernel<<<count, 256, 0, s>>>(d_tables);  // K2 of every tensor in one launch
+        CK(cudaMemcpyAsync(d_tasks, tasks.data(), count * sizeof(EncTask), cudaMemcpyHostToDevice, s));
+    }
+    // Byte queue once L1 store sectors rather than the chain latency bound
+    // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
+    if (ctas >= kEncQueueMinCtas)
+        ans_encode_kernel<true><<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
+    else
+        ans_encode_kernel<false><<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
     stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);
     CK(cudaGetLastError());
     // One readback for every tensor: table info[3], error bits, stream length.
@@ -1344,9 +1364,8 @@ int nzgpu_split(const uint16_t* d_values, uint64_t n, uint8_t* d_exponents, uint
         (reinterpret_cast<uintptr_t>(d_signmant) & 7))
         return NZGPU_INVALID_ARGUMENT;
     if (n == 0) return NZGPU_OK;
-    split_hist_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
-        d_values, n, d_exponents, d_signmant, reinterpret_cast<unsigned long long*>(d_counts));
-    CK(cudaGetLastError());
+    CK(launch_split_hist(d_values, n, d_exponents, d_signmant, reinterpret_cast<unsigned long long*>(d_counts),
+                         static_cast<cudaStream_t>(cuda_stream)));
     return NZGPU_OK;
 }
 
@@ -1426,7 +1445,7 @@ int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* fr
     t.n = n;
     t.slot_bytes = slot;
     t.chunk_syms = chunk_symbols;
-    ans_encode_kernel<<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(nullptr, 1, t);
+    ans_encode_kernel<false><<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(nullptr, 1, t);
     stream_scan_kernel<<<1, 1024, 0, s>>>(nullptr, t);
     CK(cudaGetLastError());
     uint32_t m[8];

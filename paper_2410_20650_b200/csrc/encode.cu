@@ -33,6 +33,10 @@ __device__ __forceinline__ const EncTask& task_of(const EncTask* tasks, int ntas
     return tasks[lo];
 }
 
+// QUEUE: word stores from the byte queue (throughput: many chains per SM,
+// where per-lane byte stores saturate L1); otherwise direct byte stores,
+// fewer instructions per step for latency-bound launches of few chains.
+template <bool QUEUE>
 __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restrict__ tasks, int ntasks,
                                                          const __grid_constant__ EncTask one) {
     __shared__ EncSym enc[256];
@@ -52,22 +56,38 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
 
     uint32_t x = kStateLow;
     uint32_t emitted = 0;
-    uint8_t* out = slot_end - 4;  // renormalisation bytes go backwards from here
+    // Renormalisation bytes go backwards from slot_end - 4.  Every lane writes
+    // a different chunk, so a byte store costs one L2 sector per lane: with
+    // QUEUE the bytes are queued in a 64-bit register pair (newest at the top,
+    // pulled in by funnel shifts) and leave as aligned 32-bit words.
+    uint32_t qlo = 0, qhi = 0, qc = 0;
+    uint32_t* wo = reinterpret_cast<uint32_t*>(slot_end - 4);
+    uint8_t* out = slot_end - 4;
     bool bad = false;
     const uint32_t kmask = (1u << log2_interval) - 1u;
     // Branch-free step (lanes of a warp encode different chunks, so any
     // data-dependent branch diverges).  The serial chain is
     // x -> compare -> select -> IMAD.WIDE -> shift -> IMAD -> x; the byte
-    // stores and the checkpoint record hang off it.
+    // queue and the checkpoint record hang off it.
     auto step = [&](const EncSym& e, uint32_t i, bool may_ckpt) {
         const uint32_t limit = e.freq << 19;
         bad |= e.freq == 0;  // ans.hpp:210-212
         // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
         const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
-        if (n1) out[-1] = (uint8_t)x;
-        if (n2) out[-2] = (uint8_t)(x >> 8);
         const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
-        out -= nb;
+        if constexpr (QUEUE) {
+            qlo = __funnelshift_r(qlo, qhi, 8 * nb);
+            qhi = __funnelshift_r(qhi, x, 8 * nb);  // x & 0xFF first, then (x >> 8) & 0xFF
+            qc += nb;
+            if (qc >= 4) {  // the 4 oldest queued bytes, oldest at the highest address
+                *--wo = __byte_perm(__funnelshift_rc(qlo, qhi, 64 - 8 * qc), 0, 0x0123);
+                qc -= 4;
+            }
+        } else {
+            if (n1) out[-1] = (uint8_t)x;
+            if (n2) out[-2] = (uint8_t)(x >> 8);
+            out -= nb;
+        }
         emitted += nb;
         x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
         // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
@@ -110,6 +130,9 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
         atomicOr(t.err, kErrZeroFreq);
         return;
     }
+    // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie below
+    // the payload start, inside the slot.
+    if (QUEUE && qc) *--wo = __byte_perm(qhi, 0, 0x0123) << (32 - 8 * qc);
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
     t.plen[c] = emitted + 4;
@@ -206,6 +229,9 @@ __global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restr
     }
     for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
 }
+
+template __global__ void ans_encode_kernel<true>(const EncTask*, int, const __grid_constant__ EncTask);
+template __global__ void ans_encode_kernel<false>(const EncTask*, int, const __grid_constant__ EncTask);
 
 // dst[i] = *src[i]: one readback of scattered per-tensor result words.
 __global__ void gather_u32_kernel(const uint32_t* const* __restrict__ src, uint32_t* __restrict__ dst, int count) {

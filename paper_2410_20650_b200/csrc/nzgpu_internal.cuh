@@ -49,8 +49,8 @@ __host__ __device__ inline uint32_t lut_entry(uint32_t sym, uint32_t bias, uint3
 enum : uint32_t { kFlagSingleSymbol = 1u, kFlagHas255 = 4u, kFlagWideScale = 8u };
 constexpr uint32_t kFlagSlowLossy = kFlagHas255 | kFlagWideScale;
 
-// Per-symbol encoder constants (ans.hpp:209-219):
-// rcp = floor(2^32 / f) (f == 1: 0xFFFFFFFF), used with one correction step.
+// Per-symbol encoder constants (ans.hpp:209-219): x / f as one exact
+// multiply-shift (Granlund-Montgomery), valid for the encoder's x < 2^31.
 struct EncSym {
     uint32_t freq;
     uint32_t cum;
@@ -77,6 +77,15 @@ struct EncTask {
     uint32_t log2k;
     uint32_t cta0;           // first K3 CTA of this tensor in the launch
     uint32_t pad_;
+};
+
+// One tensor of a batched table build (K2): histogram in, tables out.
+struct TableTask {
+    const unsigned long long* counts;
+    uint16_t* freqs;
+    EncSym* enc;
+    uint32_t* lut;
+    uint32_t* info;
 };
 
 // Device view of one compressed tensor, as the decode kernels consume it.

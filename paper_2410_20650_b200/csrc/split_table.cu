@@ -9,6 +9,8 @@
 // and also emits the derived tables the coder needs: cumulative starts and
 // reciprocals for the encoder (ans.hpp:209-219) and the packed 4096-slot
 // decode LUT (ans.hpp:137-147 slot_to_symbol, plus freq and slot-cum).
+#include <algorithm>
+
 #include "nzgpu_internal.cuh"
 
 namespace nzgpu {
@@ -84,6 +86,96 @@ __global__ void __launch_bounds__(256) split_hist_kernel(const uint16_t* __restr
     }
 }
 
+// K1 with per-lane private 16-bit counters in shared memory instead of
+// warp-aggregated atomics: counter (warp, bin, lane) at u16 index
+// (warp*256 + bin)*32 + lane, so a warp's 32 increments touch at most two
+// lanes per bank (<= 2-way conflicts) and need no match/atomic.  A lane
+// counts at most kLaneMax elements (the grid is sized for it), so 16 bits
+// cannot overflow.
+constexpr int kLaneHistWarps = 4;
+constexpr uint32_t kLaneHistSmem = kLaneHistWarps * 256 * 32 * 2;  // 64 KiB
+constexpr uint64_t kLaneMax = 65000;
+constexpr int kLaneUnroll = 8;
+
+__global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(const uint16_t* __restrict__ v,
+                                                                              uint64_t n,
+                                                                              uint8_t* __restrict__ exps,
+                                                                              uint8_t* __restrict__ signmant,
+                                                                              unsigned long long* __restrict__ counts) {
+    extern __shared__ uint32_t lh[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < (int)(kLaneHistSmem / 4); i += blockDim.x) lh[i] = 0;
+    __syncthreads();
+    uint16_t* h = reinterpret_cast<uint16_t*>(lh) + warp * 256 * 32 + lane;
+    const uint64_t groups = n / 8;
+    const uint4* v4 = reinterpret_cast<const uint4*>(v);
+    // Only 12 warps fit per SM (64 KiB of counters per CTA), so each thread
+    // keeps kLaneUnroll 16-byte loads in flight to cover HBM latency.
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + tid; g0 < groups; g0 += kLaneUnroll * stride) {
+        uint4 w[kLaneUnroll];
+#pragma unroll
+        for (int k = 0; k < kLaneUnroll; ++k)
+            if (g0 + k * stride < groups) w[k] = __ldcs(v4 + g0 + k * stride);
+#pragma unroll
+        for (int k = 0; k < kLaneUnroll; ++k) {
+            const uint64_t g = g0 + k * stride;
+            if (g >= groups) break;
+            uint2 e8, s8;
+            split8(w[k], e8, s8);
+            __stcs(reinterpret_cast<uint2*>(exps) + g, e8);
+            __stcs(reinterpret_cast<uint2*>(signmant) + g, s8);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) h[((e8.x >> (8 * b)) & 0xFFu) * 32] += 1;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) h[((e8.y >> (8 * b)) & 0xFFu) * 32] += 1;
+        }
+    }
+    if (blockIdx.x == 0 && tid < (n & 7)) {  // tail (n % 8 elements)
+        const uint64_t i = groups * 8 + tid;
+        const uint32_t b = v[i];
+        const uint32_t e = (b >> 7) & 0xFFu;
+        exps[i] = (uint8_t)e;
+        signmant[i] = (uint8_t)(((b >> 8) & 0x80u) | (b & 0x7Fu));
+        h[e * 32] += 1;
+    }
+    __syncthreads();
+    for (int bin = tid; bin < 256; bin += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int wp = 0; wp < kLaneHistWarps; ++wp) {
+            const uint32_t* row = lh + (wp * 256 + bin) * 16;  // 32 u16 counters = 16 words
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum += (row[(k + bin) & 15] & 0xFFFFu) + (row[(k + bin) & 15] >> 16);
+        }
+        if (sum) atomicAdd(counts + bin, (unsigned long long)sum);
+    }
+}
+
+#ifndef NZ_HIST_LANE
+#define NZ_HIST_LANE 1
+#endif
+
+// K1 launcher: exponent plane + sign/mantissa plane + exponent histogram.
+cudaError_t launch_split_hist(const uint16_t* v, uint64_t n, uint8_t* exps, uint8_t* signmant,
+                              unsigned long long* counts, cudaStream_t s) {
+    if (NZ_HIST_LANE && exps && signmant && counts) {
+        // per call: the attribute is per device, and the call is cheap
+        cudaError_t e = cudaFuncSetAttribute(split_hist_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kLaneHistSmem);
+        if (e != cudaSuccess) return e;
+        const uint64_t threads = kLaneHistWarps * 32;
+        const uint64_t want = ceil_div(n / 8 + 1, threads);
+        const uint64_t need = ceil_div(n, threads * kLaneMax);  // 16-bit counters
+        const uint64_t grid = std::max<uint64_t>(need, std::min<uint64_t>(want, 148 * 3));
+        split_hist_lane_kernel<<<(unsigned)grid, (unsigned)threads, kLaneHistSmem, s>>>(v, n, exps, signmant, counts);
+        return cudaGetLastError();
+    }
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n / 8 + 1, 256), 148 * 16));
+    split_hist_kernel<<<(unsigned)grid, 256, 0, s>>>(v, n, exps, signmant, counts);
+    return cudaGetLastError();
+}
+
 // Histogram of an exponent plane (lossy path: post-normalisation exponents,
 // tensorstore.hpp:201-203).
 __global__ void __launch_bounds__(256) byte_hist_kernel(const uint8_t* __restrict__ x, uint64_t n,
@@ -116,12 +208,12 @@ __global__ void __launch_bounds__(256) byte_hist_kernel(const uint8_t* __restric
 // One CTA of 256 threads; thread s owns symbol s.
 //   info[0] = flags (kFlagSingleSymbol), info[1] = that symbol,
 //   info[2] |= error bits.
-__global__ void __launch_bounds__(256) build_table_kernel(const unsigned long long* __restrict__ counts,
-                                                          const uint16_t* __restrict__ given_freqs,
-                                                          uint16_t* __restrict__ freqs_out,
-                                                          EncSym* __restrict__ enc,
-                                                          uint32_t* __restrict__ lut,
-                                                          uint32_t* __restrict__ info) {
+__device__ __forceinline__ void build_table_body(const unsigned long long* __restrict__ counts,
+                                                 const uint16_t* __restrict__ given_freqs,
+                                                 uint16_t* __restrict__ freqs_out,
+                                                 EncSym* __restrict__ enc,
+                                                 uint32_t* __restrict__ lut,
+                                                 uint32_t* __restrict__ info) {
     __shared__ unsigned long long rem[256];
     __shared__ uint32_t freq[256];
     __shared__ uint32_t cum[257];
@@ -260,6 +352,21 @@ __global__ void __launch_bounds__(256) build_table_kernel(const unsigned long lo
             lut[slot] = lut_entry((uint32_t)sym, slot - cum[sym], fs == kProbScale ? 0u : fs);
         }
     }
+}
+
+__global__ void __launch_bounds__(256) build_table_kernel(const unsigned long long* __restrict__ counts,
+                                                          const uint16_t* __restrict__ given_freqs,
+                                                          uint16_t* __restrict__ freqs_out,
+                                                          EncSym* __restrict__ enc,
+                                                          uint32_t* __restrict__ lut,
+                                                          uint32_t* __restrict__ info) {
+    build_table_body(counts, given_freqs, freqs_out, enc, lut, info);
+}
+
+// Batched compress: one CTA per tensor (blockIdx.x).
+__global__ void __launch_bounds__(256) build_tables_kernel(const TableTask* __restrict__ tasks) {
+    const TableTask t = tasks[blockIdx.x];
+    build_table_body(t.counts, nullptr, t.freqs, t.enc, t.lut, t.info);
 }
 
 }  // namespace nzgpu
