@@ -155,9 +155,9 @@ class CompressedMlp:
 
     @classmethod
     def from_raw(cls, raw: List[RawLayer], activation=Activation.Relu, meter=None, decode_ctas: int = 0):
-        layers = [LinearLayer(DeviceBlob.compress(r.weight.contiguous(), precision=kLosslessPrecision,
-                                                  meta=TensorMeta(tuple(r.weight.shape))), r.bias.clone())
-                  for r in raw]
+        blobs = DeviceBlob.compress_batch([r.weight.contiguous() for r in raw], precision=kLosslessPrecision,
+                                          metas=[TensorMeta(tuple(r.weight.shape)) for r in raw])
+        layers = [LinearLayer(b, r.bias.clone()) for b, r in zip(blobs, raw)]
         return cls(layers, activation, meter, decode_ctas)
 
     def _plan(self, i):
