@@ -181,6 +181,10 @@ int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out);
 /* Same for `count` tensors, pipelined across two CUDA streams (H2D of tensor
  * i+1 overlaps decode of i and D2H of i-1). */
 int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t* const* outs);
+/* The host tier keeps per-thread device staging (8 slots, each sized for the
+ * largest tensor it has staged) between calls; this frees the calling
+ * thread's staging after its queued work completes. */
+int nzgpu_host_release(void);
 
 /* ---- building blocks (device pointers, stream-ordered) ------------------ */
 /* K1: exponent plane, sign/mantissa plane and 256-bin u64 histogram

@@ -31,6 +31,7 @@ from .codec import (  # noqa: F401
     compress_lossy,
     crc32,
     decompress_batch,
+    release_host_buffers,
     decompress_lossless,
     decompress_lossy,
     footprint,

@@ -510,6 +510,11 @@ def decompress_batch(blobs: Sequence[Blob]) -> list:
     return [o[: b.meta.element_count()] for o, b in zip(outs, blobs)]
 
 
+def release_host_buffers() -> None:
+    """Free the calling thread's host-tier device staging (nzgpu_host_release)."""
+    N.check(N.lib.nzgpu_host_release(), "host_release")
+
+
 def build_table(counts) -> np.ndarray:
     """FrequencyTable::from_counts (ans.hpp:52-93), run by the K2 kernel."""
     c = np.ascontiguousarray(counts, dtype=np.uint64)

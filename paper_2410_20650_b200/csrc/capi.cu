@@ -92,7 +92,7 @@ using namespace nzgpu;
 namespace {
 
 constexpr uint32_t kIndexMagic = 0x58495A4Eu;  // "NZIX"
-constexpr uint32_t kIndexVersion = 1;
+constexpr uint32_t kIndexVersion = 2;  // 2: + max_window_unit
 constexpr uint32_t kFlagIrregular = 2u;
 
 struct IndexHeader {
@@ -104,8 +104,14 @@ struct IndexHeader {
     uint64_t nchunks;
     uint64_t nsub;
     uint64_t stream_len;
+    // Largest payload window of a 32-sub-range warp unit (the persistent
+    // decoder's shared-memory window), so host-tier decodes need not scan the
+    // index for it.  Only a sizing hint: a unit that does not fit is a decode
+    // error (decode_persist.cu, stage()), never an out-of-window read.
+    uint32_t max_window_unit;
+    uint32_t reserved;
 };
-static_assert(sizeof(IndexHeader) == 48, "index header layout");
+static_assert(sizeof(IndexHeader) == 56, "index header layout");
 
 thread_local char g_msg[512] = "";
 
@@ -975,7 +981,8 @@ int nzgpu_blob_export(nzgpu_blob b, uint16_t* freqs, uint8_t* stream, uint8_t* m
     if (mantissas && b->mant_len) CK(cudaMemcpy(mantissas, b->mant, b->mant_len, cudaMemcpyDeviceToHost));
     if (scales && b->scales_len) CK(cudaMemcpy(scales, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
     if (index && !(b->flags & kFlagIrregular)) {
-        IndexHeader h{kIndexMagic, kIndexVersion, b->chunk_syms, b->interval, b->n, b->nchunks, b->nsub, b->stream_len};
+        IndexHeader h{kIndexMagic, kIndexVersion, b->chunk_syms, b->interval, b->n, b->nchunks, b->nsub, b->stream_len,
+                      b->max_window_unit, 0};
         std::memcpy(index, &h, sizeof(h));
         if (b->nsub)
             CK(cudaMemcpy(static_cast<uint8_t*>(index) + sizeof(h), b->ckpt, b->nsub * sizeof(uint2),
@@ -1176,8 +1183,18 @@ struct HostSlot {
     }
 };
 
+// Slots in flight: slot i % kHostSlots stages tensor i.  A slot's H2D of the
+// next tensor queues behind its D2H of the previous one (one stream), so
+// with few slots a large tensor after a small one leaves the D2H engine
+// idle.  Measured on 4 Llama-3-8B layers (PCIe ceiling 86 GB/s): 2 slots
+// 62 GB/s, 4: 73, 6: 78, 8: 80.
+#ifndef NZ_HOST_SLOTS
+#define NZ_HOST_SLOTS 8
+#endif
+constexpr int kHostSlots = NZ_HOST_SLOTS;
+
 struct HostCtx {
-    HostSlot slot[2];
+    HostSlot slot[kHostSlots];
     int init() {
         for (HostSlot& sl : slot) {
             if (!sl.s) CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
@@ -1195,17 +1212,22 @@ thread_local std::unique_ptr<HostCtx> g_host;
 uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint64_t nsub, uint32_t S, int log2k,
                          uint64_t ts) {
     const uint64_t spc = S >> log2k;
+    // sub-range -> chunk by shift when S/K is a power of two (the default
+    // 65536/64): this loop runs once per warp unit of every staged tensor
+    const int sh = (spc & (spc - 1)) == 0 ? __builtin_ctzll(spc) : -1;
+    auto chunk_of = [&](uint64_t j) { return sh >= 0 ? j >> sh : j / spc; };
+    auto in_chunk = [&](uint64_t j) { return sh >= 0 ? j & (spc - 1) : j % spc; };
     uint64_t best = 0;
     for (uint64_t sub0 = 0; sub0 < nsub; sub0 += ts) {
         const uint64_t subs = std::min<uint64_t>(ts, nsub - sub0);
-        const uint4 c0 = info[sub0 / spc];
+        const uint4 c0 = info[chunk_of(sub0)];
         const uint64_t lim0 = c0.z >= 4 ? c0.z - 4 : 0;
-        const uint64_t e0 = sub0 % spc == 0 ? lim0 : std::min<uint64_t>(ckpt[sub0].y, lim0);
+        const uint64_t e0 = in_chunk(sub0) == 0 ? lim0 : std::min<uint64_t>(ckpt[sub0].y, lim0);
         const uint64_t a = ((uint64_t)c0.x | ((uint64_t)c0.y << 32)) + lim0 - e0;
         const uint64_t jl = sub0 + subs - 1;
-        const uint4 c1 = info[jl / spc];
+        const uint4 c1 = info[chunk_of(jl)];
         const uint64_t lim1 = c1.z >= 4 ? c1.z - 4 : 0;
-        const bool chunk_end = (((jl % spc) + 1) << log2k) >= c1.w;
+        const bool chunk_end = ((in_chunk(jl) + 1) << log2k) >= c1.w;
         const uint64_t e1 = (jl + 1 < nsub && !chunk_end) ? std::min<uint64_t>(ckpt[jl + 1].y, lim1) : 0;
         uint64_t b = ((uint64_t)c1.x | ((uint64_t)c1.y << 32)) + lim1 - e1;
         if (b < a) b = a;
@@ -1214,11 +1236,23 @@ uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint
     return (uint32_t)std::min<uint64_t>(best, 0xFFFFFFFFu);
 }
 
+// NZGPU_TRACE: host time per stage of stage_and_decode, summed over a batch.
+double g_stage_us[6] = {};
+struct StageClock {
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(int k) {
+        const auto now = std::chrono::steady_clock::now();
+        g_stage_us[k] += std::chrono::duration<double, std::micro>(now - t).count();
+        t = now;
+    }
+};
+
 // Stage + decode one host tensor on a slot without any host synchronisation
 // (uniform framing and a valid side index).  Returns 1 when the caller must
 // take the general (synchronising) path instead.
 int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_out) {
     if (!t || !valid_precision(t->precision) || !t->freqs || !t->index) return 1;
+    StageClock clk;
     std::vector<uint4> info;
     uint64_t total = 0;
     if (walk_stream(t->stream, t->stream_len, info, total) || info.empty() || total != t->n) return 1;
@@ -1267,6 +1301,7 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     const uint64_t o_info = cv.take(info.size() * sizeof(uint4));
     const uint64_t o_ckpt = cv.take(b.nsub * sizeof(uint2) + 16), o_scr = cv.take(64);
     cudaStream_t s = sl.s;
+    clk.lap(0);  // parse + validate
     if (int rc = sl.main.ensure(cv.size, s)) return rc;
     if (int rc = sl.stream.ensure(align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32, s)) return rc;
     if (int rc = sl.out.ensure(align_up(t->n * 2, 16) + 16, s)) return rc;
@@ -1280,10 +1315,12 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     b.scratch_u32 = reinterpret_cast<uint32_t*>(m + o_scr);
     b.stream = static_cast<uint8_t*>(sl.stream.p);
     b.err = sl.err;
+    clk.lap(1);  // buffers
     CK(cudaMemcpyAsync(b.freqs, t->freqs, 512, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(b.stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
     if (b.mant_len) CK(cudaMemcpyAsync(b.mant, t->mantissas, b.mant_len, cudaMemcpyHostToDevice, s));
     if (b.scales_len) CK(cudaMemcpyAsync(b.scales, t->scales, b.scales_len, cudaMemcpyHostToDevice, s));
+    clk.lap(2);  // section copies
     uint4* info_pinned = nullptr;
     if (int rc = sl.stage_info(info, &info_pinned)) return rc;
     CK(cudaMemcpyAsync(b.chunk_info, info_pinned, info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
@@ -1291,12 +1328,22 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     CK(cudaMemcpyAsync(b.ckpt, ck, b.nsub * sizeof(uint2), cudaMemcpyHostToDevice, s));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
+    clk.lap(3);  // chunk table + index + LUT
     if (!(b.flags & kFlagSingleSymbol)) {
-        b.max_window_unit = host_max_window(info, ck, b.nsub, S, log2k, 32);
-        b.max_window = host_max_window(info, ck, b.nsub, S, log2k, decode_tile_subs());
+        // the index's hint when plausible (at most 2 bytes per symbol plus the
+        // framing of the two chunks a unit can touch), else a scan
+        const uint64_t bound = 64ull * h.interval + 64;
+        b.max_window_unit = h.max_window_unit && h.max_window_unit <= bound
+                                ? h.max_window_unit
+                                : host_max_window(info, ck, b.nsub, S, log2k, 32);
+        // the tile window only matters when the persistent kernel cannot run
+        if (!(use_persist() && persist_fits(log2k, b.max_window_unit)))
+            b.max_window = host_max_window(info, ck, b.nsub, S, log2k, decode_tile_subs());
     }
+    clk.lap(4);  // windows
     if (int rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), s)) return rc;
     if (t->n) CK(cudaMemcpyAsync(host_out, sl.out.p, t->n * 2, cudaMemcpyDeviceToHost, s));
+    clk.lap(5);  // decode + D2H issue
     return NZGPU_OK;
 }
 
@@ -1314,7 +1361,7 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
     int general = 0;
     const auto tcall = std::chrono::steady_clock::now();
     for (int i = 0; i < count; ++i) {
-        HostSlot& sl = h.slot[i & 1];
+        HostSlot& sl = h.slot[i % kHostSlots];
         const nzgpu_host_tensor* t = ts + i;
         const auto t0 = std::chrono::steady_clock::now();
         int rc = stage_and_decode(sl, t, outs[i]);
@@ -1336,8 +1383,7 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
             if (!rc) CK(cudaStreamSynchronize(sl.s));  // b's buffers die here
         }
         if (rc) {
-            cudaStreamSynchronize(h.slot[0].s);
-            cudaStreamSynchronize(h.slot[1].s);
+            for (HostSlot& other : h.slot) cudaStreamSynchronize(other.s);
             return rc;
         }
     }
@@ -1346,6 +1392,12 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
     for (HostSlot& sl : h.slot) {
         const int r = sync_status(sl.s, sl.err, true);
         if (!rc) rc = r;
+    }
+    if (trace) {
+        std::fprintf(stderr, "nzgpu batch stages (us): parse %.0f buffers %.0f sections %.0f table %.0f windows %.0f "
+                     "decode+d2h %.0f\n", g_stage_us[0], g_stage_us[1], g_stage_us[2], g_stage_us[3], g_stage_us[4],
+                     g_stage_us[5]);
+        for (double& v : g_stage_us) v = 0;
     }
     if (trace)
         std::fprintf(stderr, "nzgpu batch: %d tensors (%d general), host enqueue %.0f us, final wait %.0f us, call %.0f us\n",
@@ -1356,6 +1408,15 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
 }
 
 int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out) { return nzgpu_decompress_host_batch(t, 1, &out); }
+
+int nzgpu_host_release(void) {
+    if (g_host) {
+        for (HostSlot& sl : g_host->slot)
+            if (sl.s) cudaStreamSynchronize(sl.s);
+        g_host.reset();
+    }
+    return NZGPU_OK;
+}
 
 // ------------------------------------------------------------ building blocks
 int nzgpu_split(const uint16_t* d_values, uint64_t n, uint8_t* d_exponents, uint8_t* d_signmant, uint64_t* d_counts,

@@ -138,6 +138,7 @@ SIGNATURES = {
     "nzgpu_compress_host": (_i, [_vp, _u64, _i, _u32, _u32, _u32, _p(_vp)]),
     "nzgpu_decompress_host": (_i, [_p(HostTensor), _vp]),
     "nzgpu_decompress_host_batch": (_i, [_p(HostTensor), _i, _p(_vp)]),
+    "nzgpu_host_release": (_i, []),
     "nzgpu_split": (_i, [_vp, _u64, _vp, _vp, _vp, _vp]),
     "nzgpu_build_table": (_i, [_vp, _vp, _vp]),
     "nzgpu_build_table_host": (_i, [_vp, _vp]),

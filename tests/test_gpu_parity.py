@@ -303,3 +303,31 @@ def test_gpu_batch_host_decode(nz, port):
     outs = nz.decompress_batch(blobs)
     for o, v in zip(outs, vs):
         assert (o == v).all()
+    # more tensors than staging slots, mixed sizes, then release and reuse
+    vs = [port.gaussian_bf16(100 + i, n, 0.02) for i, n in enumerate([70000, 3 * 65536 + 5, 1000, 1 << 20] * 5)]
+    blobs = [nz.compress_lossless(v) for v in vs]
+    for _ in range(2):
+        outs = nz.decompress_batch(blobs)
+        assert all((o == v).all() for o, v in zip(outs, vs))
+        nz.release_host_buffers()
+
+
+def test_gpu_index_window_hint_is_only_a_hint(nz, port):
+    """The exported index carries the unit window size (header offset 48).
+    A zeroed or implausible hint falls back to a scan and still decodes; an
+    understated hint is reported as a FormatError, never a bad decode."""
+    import struct
+
+    v = port.gaussian_bf16(5, 1 << 20, 0.02)
+    blob = nz.compress_lossless(v)
+    ix = bytearray(blob.index)
+    (hint,) = struct.unpack_from("<I", ix, 48)
+    assert 0 < hint <= 64 * 64 + 64
+    for bad in (0, 0xFFFFFFFF):
+        struct.pack_into("<I", ix, 48, bad)
+        b2 = nz.LosslessBlob(blob.meta, blob.freqs, blob.stream, blob.signmant, index=bytes(ix))
+        assert (nz.decompress_batch([b2])[0] == v).all()
+    struct.pack_into("<I", ix, 48, 16)
+    b3 = nz.LosslessBlob(blob.meta, blob.freqs, blob.stream, blob.signmant, index=bytes(ix))
+    with pytest.raises(nz.FormatError):
+        nz.decompress_batch([b3])
