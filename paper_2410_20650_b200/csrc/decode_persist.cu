@@ -400,10 +400,18 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     // of the CTA's range from a shared counter, so warps that drew cheaper
     // units take more and the CTA ends within about one unit of its average
     // (a static round-robin left ~7 % of SM time idle in the tail).
-    uint32_t* s_next = reinterpret_cast<uint32_t*>(smem + 16);
+    // One predicated ATOMS by lane 0.  With a warp-uniform address ptxas
+    // rewrites any shared atomic into a warp-aggregated one (vote, popc,
+    // shuffle, reconvergence: ~20 instructions per unit); the address gets
+    // a lane term that is zero at run time (mc.one == 1) but opaque to it.
+    const uint32_t s_next = sbase + 16 + lane * (mc.one - 1u);
     auto grab = [&]() -> uint32_t {
         uint32_t v = 0;
-        if (lane == 0) v = atomicAdd(s_next, 1u);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.eq.u32 p, %1, 0;\n@p atom.shared.add.u32 %0, [%2], 1;\n}\n"
+            : "+r"(v)
+            : "r"(lane), "r"(s_next)
+            : "memory");
         return __shfl_sync(0xFFFFFFFFu, v, 0);
     };
     uint32_t u = ubeg + warp, un = ubeg + kPWarps + warp, unn = 0;
