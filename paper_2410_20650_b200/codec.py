@@ -197,11 +197,13 @@ class DeviceBlob:
     def compress_batch(cls, values: Sequence, precision: int = kLosslessPrecision,
                        block_size: int = kDefaultBlockSize, chunk_symbols: int = kChunkSymbols,
                        interval: int = 0, stream=None, metas: Optional[Sequence[TensorMeta]] = None,
-                       max_batch_elements: int = 1 << 32) -> list:
+                       max_batch_elements: int = 1 << 32, workspace=None) -> list:
         """Compress many CUDA tensors with one encode launch per batch
         (nzgpu_compress_batch); result i is byte-identical to
         ``compress(values[i], ...)``.  Batches are cut at
-        ``max_batch_elements`` (temporaries are ~3 B per element)."""
+        ``max_batch_elements`` (temporaries are ~3 B per element).
+        ``workspace``: an optional uint8 CUDA tensor reused for the
+        temporaries when large enough (see ``compress_workspace_bytes``)."""
         import torch
 
         flat = []
@@ -225,7 +227,10 @@ class DeviceBlob:
             wsb = C.c_uint64()
             N.check(N.lib.nzgpu_compress_batch_workspace_size(ns, len(part), precision, chunk_symbols,
                                                               C.byref(wsb)), "compress_batch")
-            ws = torch.empty(wsb.value + 256, dtype=torch.uint8, device=part[0].device)
+            if workspace is not None and workspace.numel() >= wsb.value + 256:
+                ws = workspace
+            else:
+                ws = torch.empty(wsb.value + 256, dtype=torch.uint8, device=part[0].device)
             wp = (ws.data_ptr() + 255) & ~255
             rc = N.lib.nzgpu_compress_batch(ptrs, ns, len(part), precision, block_size, chunk_symbols, interval,
                                             C.c_void_p(wp), wsb.value, _stream_ptr(stream), hs)
@@ -234,6 +239,16 @@ class DeviceBlob:
                 out.append(cls(C.c_void_p(hs[k]), metas[i + k] if metas else None))
             i = j
         return out
+
+    @staticmethod
+    def compress_workspace_bytes(sizes: Sequence[int], precision: int = kLosslessPrecision,
+                                 chunk_symbols: int = kChunkSymbols) -> int:
+        """Workspace bytes of one compress_batch over tensors of these sizes."""
+        ns = (C.c_uint64 * len(sizes))(*sizes)
+        out = C.c_uint64()
+        N.check(N.lib.nzgpu_compress_batch_workspace_size(ns, len(sizes), precision, chunk_symbols, C.byref(out)),
+                "compress_workspace_bytes")
+        return int(out.value) + 256
 
     @classmethod
     def from_host(cls, blob: Blob, interval: int = 0) -> "DeviceBlob":

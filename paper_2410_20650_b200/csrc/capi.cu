@@ -361,7 +361,8 @@ int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
 // Largest payload window per decode tile / warp unit of each blob (sizes the
 // decoders' shared-memory windows): the window kernels of every blob, then one
 // readback.
-int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s) {
+int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s, uint8_t* scratch_ptrs = nullptr,
+                    uint32_t* scratch_res = nullptr) {
     std::vector<const uint32_t*> ptrs;
     std::vector<int> who;
     for (int i = 0; i < count; ++i) {
@@ -376,20 +377,42 @@ int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s) {
         who.push_back(i);
     }
     if (who.empty()) return NZGPU_OK;
+    static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[nzgpu]   compute_windows(%d) %-10s %9.1f us\n", count, what,
+                     std::chrono::duration<double, std::micro>(now - t0).count());
+        t0 = now;
+    };
+    mark("kernels");
     std::vector<uint32_t> w(ptrs.size());
     if (who.size() == 1) {
         CK(cudaMemcpyAsync(w.data(), ptrs[0], 8, cudaMemcpyDeviceToHost, s));
     } else {
+        // device scratch: the caller's (a compress batch's readback arrays,
+        // >= 2 pointers and 2 words per blob) or a stream-ordered allocation
         uint8_t* tmp = nullptr;
         const uint64_t pb = align_up(ptrs.size() * sizeof(void*), 256);
-        CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), pb + ptrs.size() * 4, s));
-        CK(cudaMemcpyAsync(tmp, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
-        gather_u32_kernel<<<grid_for(ptrs.size(), 256), 256, 0, s>>>(reinterpret_cast<const uint32_t* const*>(tmp),
-                                                                      reinterpret_cast<uint32_t*>(tmp + pb),
-                                                                      (int)ptrs.size());
+        const uint32_t* const* d_ptrs;
+        uint32_t* d_res;
+        if (scratch_ptrs && scratch_res) {
+            d_ptrs = reinterpret_cast<const uint32_t* const*>(scratch_ptrs);
+            d_res = scratch_res;
+        } else {
+            CK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), pb + ptrs.size() * 4, s));
+            d_ptrs = reinterpret_cast<const uint32_t* const*>(tmp);
+            d_res = reinterpret_cast<uint32_t*>(tmp + pb);
+        }
+        mark("scratch");
+        CK(cudaMemcpyAsync(const_cast<const uint32_t**>(d_ptrs), ptrs.data(), ptrs.size() * sizeof(void*),
+                           cudaMemcpyHostToDevice, s));
+        gather_u32_kernel<<<grid_for(ptrs.size(), 256), 256, 0, s>>>(d_ptrs, d_res, (int)ptrs.size());
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(w.data(), tmp + pb, w.size() * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaFreeAsync(tmp, s));
+        CK(cudaMemcpyAsync(w.data(), d_res, w.size() * 4, cudaMemcpyDeviceToHost, s));
+        if (tmp) CK(cudaFreeAsync(tmp, s));
     }
     CK(cudaStreamSynchronize(s));
     for (size_t j = 0; j < who.size(); ++j) {
@@ -603,6 +626,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     auto tlast = std::chrono::steady_clock::now();
     auto mark = [&](const char* what) {
         if (!trace) return;
+        cudaStreamSynchronize(s);  // attribute device time to the phase that queued it
         const auto now = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[nzgpu] compress_many(%d) %-10s %9.1f us\n", count, what,
                      std::chrono::duration<double, std::micro>(now - tlast).count());
@@ -746,6 +770,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     if (count > 1) {
         if (int rc = arena_alloc(stotal, stream_arena)) return rc;
     }
+    mark("str arena");
     for (int i = 0; i < count; ++i) {
         nzgpu_blob_s* b = bs[i];
         if (stream_arena) {
@@ -759,7 +784,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         CK(cudaGetLastError());
     }
     mark("streams");
-    const int rc = compute_windows(bs, count, s);
+    // the readback arrays (6 pointers and 6 words per blob) are free again
+    const int rc = compute_windows(bs, count, s, tmp + L.ptrs, reinterpret_cast<uint32_t*>(tmp + L.res));
     // a caller's workspace must be free to reuse when this returns
     if (ws) CK(cudaStreamSynchronize(s));
     mark("windows");
