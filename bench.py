@@ -493,20 +493,29 @@ def cpu_baseline(args):
         cores = min(os.cpu_count() or 1, 64) if kind == "reference" else 1
         os.environ["NEUZIP_THREADS"] = str(cores)
         decs = cpu_decoders(ref, kind, vals, args)
-        algo = 0
-        t0 = time.perf_counter()
-        reps = 0
-        while True:
-            for fn, a in decs:
-                fn()
-                algo += a
-            reps += 1
-            if time.perf_counter() - t0 > args.cpu_seconds or reps >= 50:
-                break
-        dt = time.perf_counter() - t0
-        return {"value": round(algo / dt / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+
+        def timed(seconds):
+            algo, reps, t0 = 0, 0, time.perf_counter()
+            while True:
+                for fn, a in decs:
+                    fn()
+                    algo += a
+                reps += 1
+                if time.perf_counter() - t0 > seconds or reps >= 50:
+                    break
+            return algo / (time.perf_counter() - t0) / 1e9, reps
+
+        value, reps = timed(args.cpu_seconds)
+        one = None
+        if kind == "reference" and cores > 1:  # also NEUZIP_THREADS=1 (read per call)
+            os.environ["NEUZIP_THREADS"] = "1"
+            one, _ = timed(args.cpu_seconds / 2)
+            os.environ["NEUZIP_THREADS"] = str(cores)
+        return {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                "value_1thread": round(one, 4) if one is not None else None,
                 "sample": f"decompress of layer-0 tensors {shapes}, {reps} reps, NEUZIP_THREADS={cores} "
-                          f"(reference caps workers at 64, parallel.hpp:24); host nproc={os.cpu_count()}"}
+                          f"(reference caps workers at 64, parallel.hpp:24); host nproc={os.cpu_count()}; "
+                          f"value_1thread: the same with NEUZIP_THREADS=1"}
     except Exception as e:  # the baseline is reported, never required
         return {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": repr(e)}
 
