@@ -330,7 +330,7 @@ def run_gpu(args):
             traffic = round(achieved * float(tj["dram_bytes_per_algo_byte"]), 2)
 
     # ---- e2e through the reference-facing host API (host buffers in/out)
-    e2e = run_e2e(args, nz, blobs, torch) if rank == 0 else None
+    e2e = run_e2e(args, nz, blobs, torch, dist)
     if dist:
         dist.barrier()
 
@@ -382,7 +382,7 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, nz, blobs, torch):
+def run_e2e(args, nz, blobs, torch, dist=None):
     """Same metric through nzgpu_decompress_host_batch: compressed sections
     H2D from pinned host memory, GPU decode, bf16 D2H to pinned memory, every
     step.  Bounded to the first `--e2e-layers` layers to cap host memory."""
@@ -430,13 +430,24 @@ def run_e2e(args, nz, blobs, torch):
     d2h = sum(2 * b.n for b in sel)
     N.check(N.lib.nzgpu_decompress_host_batch(arr, len(ts), ptrs), "e2e warmup")
     steps = max(1, min(args.steps, 5))
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         N.check(N.lib.nzgpu_decompress_host_batch(arr, len(ts), ptrs), "e2e")
     dt = time.perf_counter() - t0
+    # every rank decodes its own tensors through its own PCIe link: whole-job
+    # bytes over the slowest rank's time
+    if dist:
+        t = torch.tensor([dt, float(algo), float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        dt_max = t[:1].clone()
+        dist.all_reduce(dt_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dt, algo, h2d, d2h = float(dt_max.item()), int(t[1].item()), int(t[2].item()), int(t[3].item())
     return {"value": round(algo * steps / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "sample": f"first {args.e2e_layers} layers ({len(sel)} tensors), "
-            f"{steps} steps, nzgpu_decompress_host_batch (pinned host buffers)"}
+            "d2h_bytes_per_step": d2h, "sample": f"first {args.e2e_layers} layers of each rank "
+            f"({len(sel)} tensors on rank 0), {steps} steps, nzgpu_decompress_host_batch (pinned host "
+            f"buffers), all ranks concurrently: sum of bytes / max time"}
 
 
 # ------------------------------------------------------ CPU reference arm ---
