@@ -95,3 +95,40 @@ def test_gpu_compress_batch_errors(nz, port):
     # the library stays usable after a failed batch
     b = nz.DeviceBlob.compress_batch(_dev([good]))[0]
     assert (b.decompress().view(torch.int16).cpu().numpy().view(np.uint16) == good).all()
+
+
+@pytest.mark.parametrize("chunk,interval", [(65536, 128), (65536, 256), (131072, 0), (1 << 14, 64), (100000, 0)])
+def test_gpu_compress_batch_chunk_and_interval(nz, port, chunk, interval):
+    """Non-default chunk sizes S and checkpoint strides K, including an S no
+    stride divides (100000: reference framing, sequential decode, no index)."""
+    import torch
+
+    ts = [port.gaussian_bf16(port.derive(21, i), n, 0.02) for i, n in enumerate([5, 70001, 3 * 131072 + 9, 1 << 20])]
+    batch = nz.DeviceBlob.compress_batch(_dev(ts), chunk_symbols=chunk, interval=interval)
+    for b, d, t in zip(batch, _dev(ts), ts):
+        f, s, sm = port.compress_lossless(t, chunk)
+        h = b.to_host()
+        assert h.stream == s and (h.freqs == f).all() and (h.signmant == sm).all()
+        one = nz.DeviceBlob.compress(d, chunk_symbols=chunk, interval=interval).to_host()
+        assert one.stream == h.stream and one.index == h.index
+        assert (b.decompress().view(torch.int16).cpu().numpy().view(np.uint16) == t).all()
+
+
+def test_gpu_compress_batch_wide_launch_matches_oracle(nz, port):
+    """Enough chunks (>= 600 encoder CTAs) for the byte-queue encoder
+    variant; spot-check chunks of every tensor against the oracle's coder."""
+    import torch
+
+    # 24 tensors x 820 chunks = 19,680 chunks = 615 CTAs of 32 chains
+    g = torch.Generator(device="cuda")
+    ts = []
+    for i in range(24):
+        g.manual_seed(i)
+        ts.append((torch.randn(820 * 65536, device="cuda", generator=g) * (0.02 if i % 3 else 0.5)).to(torch.bfloat16))
+    batch = nz.DeviceBlob.compress_batch(ts)
+    for i in (0, 7, 23):
+        v = ts[i].view(torch.int16).cpu().numpy().view(np.uint16)
+        f, s, sm = port.compress_lossless(v)
+        h = batch[i].to_host()
+        assert h.stream == s and (h.freqs == f).all()
+        assert torch.equal(batch[i].decompress().view(torch.int16), ts[i].view(torch.int16))
