@@ -28,8 +28,8 @@ cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, uns
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
-template <bool QUEUE>
-__global__ void ans_encode_kernel(const EncTask*, int, const __grid_constant__ EncTask);
+cudaError_t launch_encode(bool queue, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
+                          const EncTask& one, cudaStream_t s);
 __global__ void stream_scan_kernel(const EncTask*, const __grid_constant__ EncTask);
 __global__ void build_tables_kernel(const TableTask*);
 __global__ void gather_u32_kernel(const uint32_t* const*, uint32_t*, int);
@@ -728,10 +728,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     }
     // Byte queue once L1 store sectors rather than the chain latency bound
     // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
-    if (ctas >= kEncQueueMinCtas)
-        ans_encode_kernel<true><<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
-    else
-        ans_encode_kernel<false><<<ctas, NZ_ENC_THREADS, 0, s>>>(count > 1 ? d_tasks : nullptr, count, tasks[0]);
+    CK(launch_encode(ctas >= kEncQueueMinCtas, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
+                     s));
     stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);
     CK(cudaGetLastError());
     // One readback for every tensor: table info[3], error bits, stream length.
@@ -1532,7 +1530,7 @@ int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* fr
     t.n = n;
     t.slot_bytes = slot;
     t.chunk_syms = chunk_symbols;
-    ans_encode_kernel<false><<<grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, 0, s>>>(nullptr, 1, t);
+    CK(launch_encode(false, grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, nullptr, 1, t, s));
     stream_scan_kernel<<<1, 1024, 0, s>>>(nullptr, t);
     CK(cudaGetLastError());
     uint32_t m[8];

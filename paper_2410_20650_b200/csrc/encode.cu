@@ -230,8 +230,15 @@ __global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restr
     for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
 }
 
-template __global__ void ans_encode_kernel<true>(const EncTask*, int, const __grid_constant__ EncTask);
-template __global__ void ans_encode_kernel<false>(const EncTask*, int, const __grid_constant__ EncTask);
+// K3 launcher (the template kernels stay in this translation unit).
+cudaError_t launch_encode(bool queue, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
+                          const EncTask& one, cudaStream_t s) {
+    if (queue)
+        ans_encode_kernel<true><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+    else
+        ans_encode_kernel<false><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+    return cudaGetLastError();
+}
 
 // dst[i] = *src[i]: one readback of scattered per-tensor result words.
 __global__ void gather_u32_kernel(const uint32_t* const* __restrict__ src, uint32_t* __restrict__ dst, int count) {
