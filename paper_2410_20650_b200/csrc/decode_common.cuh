@@ -138,10 +138,9 @@ __device__ __forceinline__ uint32_t scale_coef_bf16(uint32_t s) { return 0x3F80u
 //   k=1: x * (1 + 2^10 + 2^20 + 2^30) moves 2-bit field j of byte x to bits
 //        6-7 of byte j (the shifted copies do not overlap, so no carries);
 //   k=0: x * (1 + 2^9 + 2^18 + 2^27) moves bit 7-j to bit 7 of byte j.
-// Elements [0, split) take coefficient c0, the rest c1 (bf16 bits).
+// lossy_unpack8 returns the 8 normalized values as 4 bf16x2 words.
 template <int P>
-__device__ __forceinline__ uint4 lossy_merge8(uint32_t e0, uint32_t e1, uint32_t raw, uint32_t c0, uint32_t c1,
-                                              uint32_t split) {
+__device__ __forceinline__ uint4 lossy_unpack8(uint32_t e0, uint32_t e1, uint32_t raw) {
     uint32_t sa, sb;
     if constexpr (P == 3) {
         const uint32_t ev = raw & 0xF0F0F0F0u, od = (raw << 4) & 0xF0F0F0F0u;
@@ -156,6 +155,21 @@ __device__ __forceinline__ uint4 lossy_merge8(uint32_t e0, uint32_t e1, uint32_t
         sb = (((raw << 4) & 0xF0u) * 0x08040201u) & 0x80808080u;
     }
     const uint2 a = merge4(e0, sa), b = merge4(e1, sb);
+    return make_uint4(a.x, a.y, b.x, b.y);
+}
+
+// All 8 elements scaled by one coefficient, given as a bf16x2 pair (cp = c | c << 16).
+template <int P>
+__device__ __forceinline__ uint4 lossy_merge8_cp(uint32_t e0, uint32_t e1, uint32_t raw, uint32_t cp) {
+    const uint4 v = lossy_unpack8<P>(e0, e1, raw);
+    return make_uint4(bf16x2_mul(v.x, cp), bf16x2_mul(v.y, cp), bf16x2_mul(v.z, cp), bf16x2_mul(v.w, cp));
+}
+
+// Elements [0, split) take coefficient c0, the rest c1 (bf16 bits).
+template <int P>
+__device__ __forceinline__ uint4 lossy_merge8(uint32_t e0, uint32_t e1, uint32_t raw, uint32_t c0, uint32_t c1,
+                                              uint32_t split) {
+    const uint4 v = lossy_unpack8<P>(e0, e1, raw);
     uint32_t cp[4];
     if (split >= 8) {
         cp[0] = cp[1] = cp[2] = cp[3] = c0 | (c0 << 16);
@@ -164,8 +178,8 @@ __device__ __forceinline__ uint4 lossy_merge8(uint32_t e0, uint32_t e1, uint32_t
         for (int p = 0; p < 4; ++p)
             cp[p] = ((uint32_t)(2 * p) < split ? c0 : c1) | (((uint32_t)(2 * p + 1) < split ? c0 : c1) << 16);
     }
-    return make_uint4(bf16x2_mul(a.x, cp[0]), bf16x2_mul(a.y, cp[1]), bf16x2_mul(b.x, cp[2]),
-                      bf16x2_mul(b.y, cp[3]));
+    return make_uint4(bf16x2_mul(v.x, cp[0]), bf16x2_mul(v.y, cp[1]), bf16x2_mul(v.z, cp[2]),
+                      bf16x2_mul(v.w, cp[3]));
 }
 
 // (k+1)-bit item i of a packed MSB-first stream (bitfloat.hpp:156-162).

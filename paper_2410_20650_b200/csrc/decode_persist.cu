@@ -347,6 +347,12 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const uint32_t ubeg = cta * upc, uend = min(units, ubeg + upc);
     const bool single = d.flags & kFlagSingleSymbol;
     const bool fast_lossy = d.block_size >= 8 && !(d.flags & kFlagSlowLossy);
+    // lossy, power-of-two B >= 32K/8: the unit's scale bytes come from one
+    // load issued with the sign/mantissa prefetch (merge flavours 4..7)
+    const int unit_scales = (P != 7 && fast_lossy && d.log2_block != 0xFFFFFFFFu &&
+                             d.log2_block >= (uint32_t)LOG2K + 2)
+                                ? min((int)d.log2_block - (LOG2K + 2), 3)
+                                : -1;
 
     if (threadIdx.x == 0) {
         *reinterpret_cast<uint32_t*>(smem + 16) = ubeg + 2 * kPWarps;  // dynamic unit counter
@@ -445,6 +451,17 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
         const bool full = unit_syms == 32u * K;  // every unit but a tensor's last
         HB pre[G];
+        uint2 sw = make_uint2(0u, 0u);  // this unit's scale bytes (unit_scales >= 0)
+        if constexpr (P != 7) {
+            if (unit_scales >= 0) {
+                const uint64_t idx0 = sym0 >> d.log2_block;
+                if (unit_scales == 0) sw = __ldg(reinterpret_cast<const uint2*>(d.scales + idx0));
+                else if (unit_scales == 1) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + idx0));
+                else if (unit_scales == 2) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + (idx0 & ~3ull))) >>
+                                                  (8u * (uint32_t)(idx0 & 2u));
+                else sw.x = __ldg(d.scales + idx0);
+            }
+        }
         if (full) {
 #pragma unroll
             for (int gi = 0; gi < G; ++gi) pre[gi] = __ldcs(gb + lane + gi * 32);
@@ -516,12 +533,27 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
         // one fully unrolled loop per merge flavour, chosen once per unit
         auto merge_groups = [&](auto flavour, auto full_unit) {
-            constexpr int M = decltype(flavour)::value;  // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path
+            // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path,
+            // 4..7 lossy pow2 B with 8/4/2/1 scale bytes per unit (B >= 32K/8)
+            constexpr int M = decltype(flavour)::value;
             constexpr bool FULL = decltype(full_unit)::value;
             uint32_t blk0 = 0, rem0 = 0;
             if constexpr (M == 1) {
                 blk0 = (uint32_t)(sym0 >> d.log2_block);
                 rem0 = (uint32_t)sym0 & (d.block_size - 1u);
+            }
+            // M >= 4: a unit (32K elements, 32K-aligned) spans NB whole blocks
+            // and merge group gi (elements 256 gi .. +255 of the unit) lies in
+            // block gi * NB / G -- one broadcast load for the unit (`sw`, issued
+            // with the sign/mantissa prefetch before the decode), then each
+            // group's bf16x2 coefficient 0x3F80|s is one PRMT with a constant
+            // selector (scale bytes are < 128 on this path).  The load stays
+            // inside the scale section: it starts NB-aligned and sections are
+            // padded to 256 bytes.
+            uint32_t sw0 = 0, sw1 = 0;
+            if constexpr (M >= 4) {
+                sw0 = sw.x | 0x80808080u;
+                sw1 = sw.y | 0x80808080u;
             }
 #pragma unroll
             for (int gi = 0; gi < G; ++gi) {
@@ -533,6 +565,11 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                 const uint32_t e0 = er[0], e1 = er[1];
                 if constexpr (M == 0) {
                     __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                } else if constexpr (M >= 4) {
+                    constexpr int NB = 8 >> (M - 4);
+                    const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
+                    const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
+                    __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
                 } else if constexpr (M == 1) {
                     // power-of-two B >= 8: an aligned 8-group never straddles a block
                     const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
@@ -579,6 +616,12 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
             merge_unit(std::integral_constant<int, 0>{});
         } else if (!fast_lossy) {
             merge_unit(std::integral_constant<int, 3>{});
+        } else if (unit_scales >= 0) {
+            // scale bytes per unit: 32K / B = 2^(3 - unit_scales) (1 when B >= 32K)
+            if (unit_scales == 0) merge_unit(std::integral_constant<int, 4>{});
+            else if (unit_scales == 1) merge_unit(std::integral_constant<int, 5>{});
+            else if (unit_scales == 2) merge_unit(std::integral_constant<int, 6>{});
+            else merge_unit(std::integral_constant<int, 7>{});
         } else if (d.log2_block != 0xFFFFFFFFu) {
             merge_unit(std::integral_constant<int, 1>{});
         } else {

@@ -133,6 +133,21 @@ def test_gpu_lossy_matches_reference(nz, port, golden, case):
     assert sha(back) == rec["decoded_sha"]
 
 
+@pytest.mark.parametrize("block", [256, 512, 1024, 2048, 4096, 1 << 16])
+@pytest.mark.parametrize("k", [0, 1, 3])
+def test_gpu_lossy_pow2_blocks_match_oracle(nz, port, k, block):
+    """Power-of-two B >= 256: the decoder loads a unit's scale bytes once
+    (8/4/2/1 bytes per 2048-element unit) -- every B class, partial last
+    units and tensors shorter than one block, against the oracle."""
+    for i, n in enumerate([5 * 2048 + 7, 3 * 65536 + 1000, 300]):
+        v = port.gaussian_bf16(port.derive(77, 10 * k + i), n, 0.02 if i else 0.7)
+        blob = nz.compress_lossy(v, k, block)
+        f, sc, st, pk = port.compress_lossy(v, k, block)
+        assert blob.stream == st and (blob.scales == sc).all() and (blob.signmant == pk).all()
+        want = port.decompress_lossy(f, sc, st, pk, k, block, n)
+        assert (nz.decompress_lossy(blob) == want).all()
+
+
 @pytest.mark.parametrize("k", [0, 1, 3])
 def test_gpu_lossy_elementwise_exhaustive(nz, port, k):
     """Every finite bf16 pattern x every scale byte (65,280 x 256 pairs)
