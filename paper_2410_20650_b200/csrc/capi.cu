@@ -826,6 +826,7 @@ struct nzgpu_plan_s {
     uint32_t ctas = 0, upc = 1, win_cap_unit = 0;
     uint32_t* d_cta_prefix = nullptr;
     std::vector<uint64_t> tunits;  // work units per tensor
+    int ntiny = 0;                 // trailing tensors outside the resident-wave budget
     uint32_t max_ctas = 0;         // 0 = every resident CTA (nzgpu_plan_set_max_ctas)
     ~nzgpu_plan_s() {
         if (d_descs) cudaFree(d_descs);
@@ -848,13 +849,26 @@ std::vector<uint32_t> persist_geometry(nzgpu_plan_s* p) {
     if (!units) return cta_prefix;
     uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
     if (p->max_ctas) resident = std::min<uint64_t>(resident, p->max_ctas);
-    auto ctas_for = [&](uint64_t upc) {
+    auto ctas_all = [&](uint64_t upc) {
         uint64_t c = 0;
         for (uint64_t u : p->tunits) c += ceil_div(u, upc);
         return c;
     };
+    // Tiny tensors (the trailing p->ntiny, e.g. a layer's norms) are left out
+    // of the one-wave budget: their few units run as extra CTAs that the SMs
+    // pick up in the launch's tail instead of each holding an SM for the
+    // whole launch.
+    const size_t nbig = p->tunits.size() - (size_t)p->ntiny;
+    auto ctas_big = [&](uint64_t upc) {
+        uint64_t c = 0;
+        for (size_t i = 0; i < nbig; ++i) c += ceil_div(p->tunits[i], upc);
+        return c;
+    };
+    auto ctas_for = [&](uint64_t upc) { return p->ntiny ? ctas_big(upc) : ctas_all(upc); };
+    uint64_t bunits = 0;
+    for (size_t i = 0; i < nbig; ++i) bunits += p->tunits[i];
     const uint64_t umax = *std::max_element(p->tunits.begin(), p->tunits.end());
-    uint64_t lo = std::max<uint64_t>(1, ceil_div(units, resident)), hi = lo;
+    uint64_t lo = std::max<uint64_t>(1, ceil_div(p->ntiny ? bunits : units, resident)), hi = lo;
     while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
     hi = std::max(lo, std::min(hi, umax));
     while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
@@ -1042,7 +1056,33 @@ int nzgpu_plan_create(const nzgpu_blob* blobs, uint16_t* const* d_outs, int coun
     CK(cudaMalloc(&p->d_err, 16));
     CK(cudaMemset(p->d_err, 0, 16));
     uint64_t tiles = 0;
-    for (int i = 0; i < count; ++i) {
+    // Descriptor order: tensors with fewer units than 1/16 of a CTA's average
+    // share go last (see persist_geometry); each descriptor carries its own
+    // output, so the order is free.
+    std::vector<int> order;
+    {
+        uint64_t units = 0, wcap = 0;
+        for (int i = 0; i < count; ++i) {
+            nzgpu_blob_s* b = blobs[i];
+            if (!b) return NZGPU_INVALID_ARGUMENT;
+            units += ceil_div(ceil_div(b->n, 1ull << p->log2k), 32);
+            wcap = std::max<uint64_t>(wcap, b->max_window_unit);
+        }
+        const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, (uint32_t)wcap));
+        const uint64_t tiny_max = units / resident / 16;
+        std::vector<int> tiny;
+        for (int i = 0; i < count; ++i) {
+            const uint64_t u = ceil_div(ceil_div(blobs[i]->n, 1ull << p->log2k), 32);
+            (u <= tiny_max ? tiny : order).push_back(i);
+        }
+        if (order.empty()) std::swap(order, tiny);  // only tiny tensors: no special case
+        p->ntiny = 0;
+        for (int i : tiny) {
+            order.push_back(i);
+            if (blobs[i]->n) ++p->ntiny;
+        }
+    }
+    for (int i : order) {
         nzgpu_blob_s* b = blobs[i];
         if (!b || b->precision != p->precision || b->log2k != p->log2k || (b->flags & kFlagIrregular) ||
             (reinterpret_cast<uintptr_t>(d_outs[i]) & 15))
