@@ -257,11 +257,17 @@ def run_gpu(args):
     comp_elems = sum(b.n for _, gb in blobs for _, _, b in gb)
 
     # ---- per-layer grouped decode plans into one reused output buffer
+    # --overlap 1: consecutive layer plans alternate between two streams and
+    # two output buffers (the double buffer of Alg. 1's consumer, nn.hpp:286-318),
+    # so layer l+1's CTAs start on the SMs layer l's tail CTAs release; plan
+    # k+2 reuses plan k's buffer and follows it on the same stream.
     max_elems = max(sum(b.n for _, _, b in gb) for _, gb in blobs)
-    outbuf = torch.empty(max_elems + 64 * 16, dtype=torch.bfloat16, device=dev)
+    nbuf = 2 if args.overlap else 1
+    outbufs = [torch.empty(max_elems + 64 * 16, dtype=torch.bfloat16, device=dev) for _ in range(nbuf)]
     plans, bytes_algo, total_n, total_fp, index_bytes = [], 0, 0, 0, 0
     for gname, gb in blobs:
         outs, off = [], 0
+        outbuf = outbufs[len(plans) % nbuf]
         for _, _, b in gb:
             outs.append(outbuf[off:off + b.n])
             off += (b.n + 63) // 64 * 64  # keep every output 128-byte aligned
@@ -275,16 +281,23 @@ def run_gpu(args):
     launches_per_step = sum(p.launches for p in plans)
 
     # L2 (126 MB) is far smaller than one step's traffic (~26 GB): no flush needed.
-    def step(events=None):
-        for k, p in enumerate(plans):
-            if events is not None:
-                events[k][0].record(stream)
-            p.launch(stream)
-            if events is not None:
-                events[k][1].record(stream)
+    side = torch.cuda.Stream(device=dev) if args.overlap else stream
+    streams = (stream, side)
 
+    def step(events=None, overlap=bool(args.overlap)):
+        for k, p in enumerate(plans):
+            st = streams[k % 2] if overlap else stream
+            if events is not None:
+                events[k][0].record(st)
+            p.launch(st)
+            if events is not None:
+                events[k][1].record(st)
+
+    side.wait_stream(stream)
     for _ in range(args.warmup):
         step()
+        step(overlap=False)
+    stream.wait_stream(side)
     for p in plans:
         p.status(stream)
     torch.cuda.synchronize()
@@ -297,9 +310,16 @@ def run_gpu(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         start.record(stream)
+        side.wait_stream(stream)
         for s in range(args.steps):
-            step(ev[s])
+            step()
+        stream.wait_stream(side)
         stop.record(stream)
+        torch.cuda.synchronize()
+        # roofline pass: the same steps serialised on one stream, each launch
+        # bracketed by CUDA events on the stream it runs on
+        for s in range(args.steps):
+            step(ev[s], overlap=False)
         torch.cuda.synchronize()
     for p in plans:
         p.status(stream)  # every decode passed its checkpoint/desync checks
@@ -359,6 +379,9 @@ def run_gpu(args):
             "index_bytes_rank0": index_bytes,
             "ratio": round(2 * total_n / total_fp, 6),
             "l2": "no flush: one step moves >= 3.4 GB per GPU >> 126 MB L2",
+            "schedule": ("layer plans alternate between 2 streams and 2 output buffers (decode of layer l+1 "
+                         "starts on the SMs layer l's tail releases); roofline from a separate serialised pass"
+                         if args.overlap else "layer plans serialised on one stream, one output buffer"),
             "parallelism": (f"weak dp{world}: one model replica per GPU, no collective" if args.shard == "replica"
                             else f"strong: whole tensors LPT-sharded over {world} GPU(s), no collective"),
             "compress_s": round(t_compress, 2),
@@ -370,7 +393,10 @@ def run_gpu(args):
         },
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": f"{plans[0].kernel} (one launch per layer)"},
+                     "kernel": f"{plans[0].kernel} (one launch per layer)",
+                     "step_frac": round(value / max(world, 1) / peak, 4),
+                     "note": "achieved/frac: per-launch CUDA-event durations of a serialised pass (one stream); "
+                             "step_frac: the timed (overlapped) step's per-GPU GB/s over the same peak"},
         "clocks": clocks.summary(),
         "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e,
@@ -586,6 +612,8 @@ def main():
     ap.add_argument("--cpu-tensors", type=int, default=7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verify", type=int, default=1)
+    ap.add_argument("--overlap", type=int, default=1, choices=[0, 1],
+                    help="1: consecutive layer decodes on two streams / two output buffers")
     ap.add_argument("--compress-batch", type=int, default=1 << 31,
                     help="max elements per nzgpu_compress_batch call (temporaries ~3 B/element)")
     args = ap.parse_args()
