@@ -56,3 +56,20 @@ def test_b200_arm_line():
     # throughput = algorithmic bytes over the timed steps
     bytes_step = d["config"]["bytes_algo_per_step"]
     assert d["value"] == pytest.approx(bytes_step / (d["ms_per_step"] / 1e3) / 1e9, rel=0.01)
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    """N>1 reference arm: rank 0 alone runs and prints, the other ranks exit 0."""
+    from oracle.oracle import ref_available
+
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29537", os.path.join(ROOT, "bench.py"),
+                          "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-tensors", "1"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
