@@ -222,14 +222,20 @@ def run_gpu(args):
             print(f"[bench] compress_batch of {len(pending)} tensors: {(time.perf_counter() - tc) * 1e3:.1f} ms",
                   file=sys.stderr)
         for (gname, tname, shape, tidx, w), blob in zip(pending, out):
-            if args.verify and tidx < 10 and w.numel() > 4096:
-                back = torch.empty_like(w)
-                blob.decompress_into(back)
-                blob.status()
-                if args.precision == 7:
-                    assert torch.equal(back.view(torch.int16), w.view(torch.int16)), f"round trip {tname}"
+            blob.tidx = tidx
             by_group.setdefault(gname, []).append((tname, shape, blob))
         pending, pend_elems = [], 0
+
+    kinds = [kind for _, ts in groups for _, _, kind in ts]
+
+    def regen(tidx):
+        """Synthetic weight `tidx` (deterministic: regenerated for the check)."""
+        n = flat[tidx]
+        if kinds[tidx] == "norm":
+            return torch.ones(n, dtype=torch.bfloat16, device=dev)
+        salt = rank * 10007 if args.shard == "replica" else 0
+        gen.manual_seed(args.seed * 1000003 + salt + tidx)
+        return (torch.randn(n, device=dev, generator=gen) * 0.02).to(torch.bfloat16)
 
     for gname, tensors in groups:
         for tname, shape, kind in tensors:
@@ -239,13 +245,7 @@ def run_gpu(args):
             n = numel(shape)
             if pend_elems and pend_elems + n > args.compress_batch:
                 flush()
-            if kind == "norm":
-                w = torch.ones(n, dtype=torch.bfloat16, device=dev)
-            else:
-                salt = rank * 10007 if args.shard == "replica" else 0
-                gen.manual_seed(args.seed * 1000003 + salt + tensor_idx)
-                w = (torch.randn(n, device=dev, generator=gen) * 0.02).to(torch.bfloat16)
-            pending.append((gname, tname, shape, tensor_idx, w))
+            pending.append((gname, tname, shape, tensor_idx, regen(tensor_idx)))
             pend_elems += n
     flush()
     del workspace
@@ -264,14 +264,17 @@ def run_gpu(args):
     max_elems = max(sum(b.n for _, _, b in gb) for _, gb in blobs)
     nbuf = 2 if args.overlap else 1
     outbufs = [torch.empty(max_elems + 64 * 16, dtype=torch.bfloat16, device=dev) for _ in range(nbuf)]
-    plans, bytes_algo, total_n, total_fp, index_bytes = [], 0, 0, 0, 0
-    for gname, gb in blobs:
+
+    def make_plan(gb, outbuf):
         outs, off = [], 0
-        outbuf = outbufs[len(plans) % nbuf]
         for _, _, b in gb:
             outs.append(outbuf[off:off + b.n])
             off += (b.n + 63) // 64 * 64  # keep every output 128-byte aligned
-        plans.append(nz.DecodePlan([b for _, _, b in gb], outs))
+        return nz.DecodePlan([b for _, _, b in gb], outs), outs
+
+    plans, bytes_algo, total_n, total_fp, index_bytes = [], 0, 0, 0, 0
+    for gname, gb in blobs:
+        plans.append(make_plan(gb, outbufs[len(plans) % nbuf])[0])
         for _, shape, b in gb:
             i = b.info
             bytes_algo += int(i.payload_bytes) + 2 * b.n
@@ -283,21 +286,43 @@ def run_gpu(args):
     # L2 (126 MB) is far smaller than one step's traffic (~26 GB): no flush needed.
     side = torch.cuda.Stream(device=dev) if args.overlap else stream
     streams = (stream, side)
+    # Bounded run-ahead: plan k (stream k % 2) also waits for plan k-3 (the
+    # other stream's previous plan), so at most two adjacent layer plans are
+    # in flight -- layer l+1 fills layer l's tail; no stream runs whole
+    # layers ahead of the other.
+    done = [torch.cuda.Event() for _ in range(4)]
+    seq = [0]
 
-    def step(events=None, overlap=bool(args.overlap)):
-        for k, p in enumerate(plans):
+    def run_plans(ps, events=None, overlap=bool(args.overlap)):
+        for k, p in enumerate(ps):
             st = streams[k % 2] if overlap else stream
+            q = seq[0]
+            if overlap and q >= 3:
+                st.wait_event(done[(q - 3) % 4])
             if events is not None:
                 events[k][0].record(st)
             p.launch(st)
             if events is not None:
                 events[k][1].record(st)
+            if overlap:
+                done[q % 4].record(st)
+            seq[0] += 1
+
+    def join():
+        stream.wait_stream(side)
+        seq[0] = 0  # the next schedule starts with both streams drained
+
+    def step(events=None, overlap=bool(args.overlap)):
+        run_plans(plans, events, overlap)
 
     side.wait_stream(stream)
     for _ in range(args.warmup):
         step()
+        join()
+        side.wait_stream(stream)
         step(overlap=False)
-    stream.wait_stream(side)
+        side.wait_stream(stream)
+    join()
     for p in plans:
         p.status(stream)
     torch.cuda.synchronize()
@@ -313,7 +338,7 @@ def run_gpu(args):
         side.wait_stream(stream)
         for s in range(args.steps):
             step()
-        stream.wait_stream(side)
+        join()
         stop.record(stream)
         torch.cuda.synchronize()
         # roofline pass: the same steps serialised on one stream, each launch
@@ -325,17 +350,11 @@ def run_gpu(args):
         p.status(stream)  # every decode passed its checkpoint/desync checks
     elapsed = start.elapsed_time(stop) / 1e3
     kernel_time = sum(a.elapsed_time(b) for row in ev for a, b in row) / 1e3
-    t_max = elapsed
-    if dist:
-        t = torch.tensor([elapsed], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
+    from paper_2410_20650_b200.shard import reduce_timing
 
-    bytes_all = bytes_algo  # algorithmic bytes of every rank's tensors (sum over ranks)
+    t_max, bytes_all = elapsed, bytes_algo  # bytes_all: algorithmic bytes of every rank's tensors
     if dist:
-        bt = torch.tensor([float(bytes_algo)], dtype=torch.float64, device=dev)
-        dist.all_reduce(bt, op=dist.ReduceOp.SUM)
-        bytes_all = int(bt.item())
+        t_max, bytes_all = reduce_timing(dist, elapsed, bytes_algo, device=dev)
     value = bytes_all * args.steps / t_max / 1e9
     peak, peak_kind = load_peaks()
     achieved = bytes_algo * args.steps / kernel_time / 1e9  # per-launch bytes / launch time, aggregated
@@ -348,6 +367,20 @@ def run_gpu(args):
             # ncu DRAM bytes (read + write) per launch, over the same launch
             # time as `achieved`: directly comparable with it.
             traffic = round(achieved * float(tj["dram_bytes_per_algo_byte"]), 2)
+
+    # ---- output check, outside the timed region: every tensor of the model
+    # decoded once more through the same grouped plans on the same two-stream
+    # schedule, into distinct buffers, then compared (lossless: with the
+    # regenerated source; lossy: with the blob's single-tensor decode; one
+    # sampled tensor against the reference codec, oracle/_ref).
+    verified, sample = 0, None
+    if args.verify:
+        verified, sample = verify_outputs(args, nz, torch, blobs, make_plan, run_plans, join, regen, stream, dev,
+                                          rank)
+        if dist:
+            vt = torch.tensor([verified], dtype=torch.int64, device=dev)
+            dist.all_reduce(vt, op=dist.ReduceOp.SUM)
+            verified = int(vt.item())
 
     # ---- e2e through the reference-facing host API (host buffers in/out)
     e2e = run_e2e(args, nz, blobs, torch, dist)
@@ -378,6 +411,10 @@ def run_gpu(args):
             "bytes_algo_per_step": bytes_all,
             "index_bytes_rank0": index_bytes,
             "ratio": round(2 * total_n / total_fp, 6),
+            "device_ratio": round(2 * total_n / (total_fp + index_bytes), 6),
+            "device_ratio_note": "2n / (footprint + GPU side index): what HBM holds per decoded bf16 byte",
+            "verified_tensors": verified,
+            "verify": sample,
             "l2": "no flush: one step moves >= 3.4 GB per GPU >> 126 MB L2",
             "schedule": ("layer plans alternate between 2 streams and 2 output buffers (decode of layer l+1 "
                          "starts on the SMs layer l's tail releases); roofline from a separate serialised pass"
@@ -406,6 +443,82 @@ def run_gpu(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def verify_outputs(args, nz, torch, blobs, make_plan, run_plans, join, regen, stream, dev, rank):
+    """Decode every tensor once more through the same grouped plans and the
+    same two-stream schedule as the timed steps, but into distinct output
+    buffers (a window of layers at a time), then check each output:
+    lossless -> equal to the regenerated source tensor; lossy -> equal to the
+    blob's single-tensor decode.  One sampled tensor (rank 0) is also checked
+    against the reference codec (oracle/_ref, else the C restatement): its
+    compressed sections and its decoded values.  Returns (count, sample)."""
+    import hashlib
+
+    import numpy as np
+
+    def padded(gb):
+        return sum((b.n + 63) // 64 * 64 for _, _, b in gb)
+
+    budget = max(max(padded(gb) for _, gb in blobs), args.verify_elems)
+    checked, i = 0, 0
+    pick = None  # smallest non-norm tensor of this rank: the oracle sample
+    while i < len(blobs):
+        j, tot = i, 0
+        while j < len(blobs) and (j == i or tot + padded(blobs[j][1]) <= budget):
+            tot += padded(blobs[j][1])
+            j += 1
+        buf = torch.empty(tot + 64, dtype=torch.bfloat16, device=dev)
+        vplans, off = [], 0
+        for _, gb in blobs[i:j]:
+            p, outs = make_plan(gb, buf[off:off + padded(gb)])
+            off += padded(gb)
+            vplans.append((p, gb, outs))
+        torch.cuda.synchronize()
+        run_plans([p for p, _, _ in vplans])
+        join()
+        for p, _, _ in vplans:
+            p.status(stream)
+        torch.cuda.synchronize()
+        for _, gb, outs in vplans:
+            for (tname, shape, b), o in zip(gb, outs):
+                if args.precision == 7:
+                    want = regen(b.tidx)
+                else:
+                    want = torch.empty(b.n, dtype=torch.bfloat16, device=dev)
+                    b.decompress_into(want)
+                    b.status()
+                if not torch.equal(o.view(torch.int16), want.view(torch.int16)):
+                    raise AssertionError(f"decoded {tname} (tensor {b.tidx}) differs from its reference")
+                checked += 1
+                if b.n > 4096 and (pick is None or b.n < pick[2].n):
+                    pick = (tname, shape, b)
+        del vplans, buf
+        i = j
+    sample = None
+    if rank == 0 and pick is not None:
+        tname, shape, b = pick
+        ref, kind = reference_lib()
+        src = regen(b.tidx).view(torch.int16).cpu().numpy().view(np.uint16)
+        host = b.to_host()
+        got = torch.empty(b.n, dtype=torch.bfloat16, device=dev)
+        b.decompress_into(got)
+        b.status()
+        got = got.view(torch.int16).cpu().numpy().view(np.uint16)
+        if args.precision == 7:
+            f, st, m = ref.compress_lossless(src)
+            ok = host.stream == st and (host.freqs == f).all() and (host.signmant == m).all() and (got == src).all()
+        else:
+            f, sc, st, pk = ref.compress_lossy(src, args.precision, args.block)
+            want = ref.decompress_lossy(f, sc, st, pk, args.precision, args.block, src.size)
+            ok = (host.stream == st and (host.freqs == f).all() and (host.signmant == pk).all()
+                  and (host.scales == sc).all() and (got == want).all())
+        if not ok:
+            raise AssertionError(f"sampled tensor {tname} differs from the reference codec ({kind})")
+        sample = {"tensor": f"{tname} {tuple(shape)} (tensor {b.tidx})", "oracle": kind,
+                  "stream_sha256": hashlib.sha256(host.stream).hexdigest()[:16],
+                  "checks": "sections (table, stream, mantissas, scales) and decoded values equal the oracle's"}
+    return checked, sample
 
 
 def run_e2e(args, nz, blobs, torch, dist=None):
@@ -601,8 +714,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--precision", type=int, default=7, choices=[7, 3, 1, 0])
-    ap.add_argument("--model", choices=sorted(MODELS), default="8b",
-                    help="8b: BASELINE configs[1] (default); 70b: configs[3]")
+    ap.add_argument("--model", choices=sorted(MODELS), default=None,
+                    help="8b: BASELINE configs[1] (default at N=1); 70b: configs[3] (default at N>1, LPT-sharded)")
     ap.add_argument("--shard", choices=["replica", "lpt"], default=None,
                     help="replica: a model per GPU (weak, 8b default); lpt: one model sharded (strong, 70b default)")
     ap.add_argument("--block", type=int, default=512)
@@ -611,12 +724,27 @@ def main():
     ap.add_argument("--e2e-layers", type=int, default=4)
     ap.add_argument("--cpu-tensors", type=int, default=7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--verify", type=int, default=1)
+    ap.add_argument("--verify", type=int, default=1,
+                    help="after the timed region, check every decoded tensor (and one against oracle/_ref)")
+    ap.add_argument("--verify-elems", type=int, default=1 << 32,
+                    help="elements decoded per verification window (distinct output buffers)")
     ap.add_argument("--overlap", type=int, default=1, choices=[0, 1],
                     help="1: consecutive layer decodes on two streams / two output buffers")
     ap.add_argument("--compress-batch", type=int, default=1 << 31,
                     help="max elements per nzgpu_compress_batch call (temporaries ~3 B/element)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        sys.exit(spawn_local_ranks(args.gpus))
+    if world is not None and int(world) != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.model is None:
+        # N=1: BASELINE configs[1] (Llama-3-8B per-layer decode on 1 B200);
+        # N>1: configs[3] (Llama-3-70B sharded across 2/4/8 B200 by LPT)
+        args.model = "70b" if args.gpus > 1 else "8b"
     if args.shard is None:
         args.shard = "lpt" if args.model == "70b" else "replica"
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
@@ -624,6 +752,20 @@ def main():
         run_reference(args)
     else:
         run_gpu(args)
+
+
+def spawn_local_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: the same command as N local
+    ranks (torch.distributed.run, rendezvous on 127.0.0.1).  Only rank 0
+    prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 if __name__ == "__main__":

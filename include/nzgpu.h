@@ -166,7 +166,10 @@ int nzgpu_plan_launch_count(nzgpu_plan plan);
 int nzgpu_plan_kernel(nzgpu_plan plan);
 /* Cap the persistent decode at `max_ctas` CTAs (one per SM; 0 = all
  * resident), leaving the other SMs to concurrent work on another stream --
- * the layer-wise consumer decodes layer l+1 beside layer l's GEMM. */
+ * the layer-wise consumer decodes layer l+1 beside layer l's GEMM.  Every CTA
+ * of the launch (small tensors included) counts against the cap.  The call
+ * synchronises the device first: the schedule it rewrites is read by any
+ * launch of this plan still queued. */
 int nzgpu_plan_set_max_ctas(nzgpu_plan plan, uint32_t max_ctas);
 
 /* ---- host tier: the reference-facing calls (host buffers, synchronous) --- */

@@ -489,6 +489,13 @@ double orc_rng_gaussian(uint64_t seed, uint64_t index) {
     return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.141592653589793238462643383279502884 * u2);
 }
 
+/* Samples [start, start + n) of rng::gaussian_bf16 (rng.hpp:73-81): the
+ * generator is counter-based, so disjoint ranges can be filled in parallel. */
+void orc_gaussian_bf16_range(uint64_t seed, uint64_t start, uint64_t n, double sigma, uint16_t* out) {
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = orc_bf16_from_float((float)(sigma * orc_rng_gaussian(seed, start + i)));
+}
+
 void orc_gaussian_bf16(uint64_t seed, uint64_t n, double sigma, uint16_t* out) {
     for (uint64_t i = 0; i < n; ++i) out[i] = orc_bf16_from_float((float)(sigma * orc_rng_gaussian(seed, i)));
 }

@@ -117,6 +117,8 @@ uint64_t orc_rng_word(uint64_t seed, uint64_t counter);        /* rng.hpp:30-32 
 uint64_t orc_rng_derive(uint64_t seed, uint64_t tag);          /* rng.hpp:35-37 */
 double orc_rng_uniform(uint64_t seed, uint64_t counter);       /* rng.hpp:40-42 */
 double orc_rng_gaussian(uint64_t seed, uint64_t index);        /* rng.hpp:45-51 */
+void orc_gaussian_bf16_range(uint64_t seed, uint64_t start, uint64_t n, double sigma,
+                             uint16_t* out);   /* rng.hpp:73-81, samples [start, start+n) */
 void orc_gaussian_bf16(uint64_t seed, uint64_t n, double sigma,
                        uint16_t* out);                        /* rng.hpp:73-81 */
 uint32_t orc_crc32(const uint8_t* data, uint64_t n);           /* crc32.hpp:26-43 */

@@ -208,6 +208,23 @@ class Oracle:
         self._gauss(seed, n, sigma, _p(out))
         return out[:n]
 
+    def gaussian_bf16_parallel(self, seed: int, n: int, sigma: float = 0.02, threads: int = 0) -> np.ndarray:
+        """gaussian_bf16 filled by host threads over disjoint counter ranges
+        (the C restatement; ctypes releases the GIL).  Identical output."""
+        import concurrent.futures as cf
+
+        port = self if self.kind == "port" else Oracle("port")
+        f = port.lib.orc_gaussian_bf16_range
+        f.restype = None
+        f.argtypes = [_u64, _u64, _u64, _dbl, _vp]
+        out = np.zeros(max(n, 1), np.uint16)
+        threads = threads or min(64, os.cpu_count() or 1)
+        step = max(1 << 20, -(-n // threads))
+        base = out.ctypes.data
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda a: f(seed, a, min(step, n - a), sigma, base + 2 * a), range(0, n, step)))
+        return out[:n]
+
     def derive(self, seed: int, tag: int) -> int:
         return int(self._derive(seed, tag))
 

@@ -260,6 +260,7 @@ class DeviceBlob:
 
     # -- decode
     def decompress_into(self, out, stream=None) -> None:
+        _check_output(out, self.n, "decompress_into")
         rc = N.lib.nzgpu_decompress(self._h, C.c_void_p(out.data_ptr()), _stream_ptr(stream))
         N.check(rc, "decompress")
 
@@ -402,6 +403,23 @@ def read_nzt(data: bytes) -> Blob:
         return db.to_host()
     finally:
         db.free()
+
+
+def _check_output(out, n: int, what: str) -> None:
+    """The kernels write n bf16 with 16-byte stores through a raw pointer:
+    reject anything that would turn into an out-of-bounds device write."""
+    if not hasattr(out, "data_ptr") or not hasattr(out, "is_cuda"):
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if not out.is_cuda:
+        raise ValueError(f"{what}: output must be a CUDA tensor, got {out.device}")
+    if out.element_size() != 2:
+        raise ValueError(f"{what}: output must have 2-byte elements (bf16/int16), got {out.dtype}")
+    if not out.is_contiguous():
+        raise ValueError(f"{what}: output must be contiguous")
+    if out.numel() < n:
+        raise ValueError(f"{what}: output holds {out.numel()} elements, the blob decodes {n}")
+    if n and out.data_ptr() % 16:
+        raise ValueError(f"{what}: output must be 16-byte aligned")
 
 
 def _stream_ptr(stream):
@@ -602,6 +620,15 @@ class DecodePlan:
     def __init__(self, blobs: Sequence[DeviceBlob], outs):
         self.blobs = list(blobs)
         self.outs = list(outs)
+        if not self.blobs or len(self.outs) != len(self.blobs):
+            raise ValueError(f"DecodePlan: {len(self.blobs)} blobs but {len(self.outs)} outputs")
+        dev = None
+        for i, (b, o) in enumerate(zip(self.blobs, self.outs)):
+            _check_output(o, b.n, f"DecodePlan output {i}")
+            if dev is None:
+                dev = o.device
+            elif o.device != dev:
+                raise ValueError(f"DecodePlan output {i} is on {o.device}, the others on {dev}")
         hs = (C.c_void_p * len(blobs))(*[b.handle for b in blobs])
         ps = (C.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
         self._h = C.c_void_p()

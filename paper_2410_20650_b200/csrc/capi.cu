@@ -864,11 +864,14 @@ std::vector<uint32_t> persist_geometry(nzgpu_plan_s* p) {
         for (size_t i = 0; i < nbig; ++i) c += ceil_div(p->tunits[i], upc);
         return c;
     };
-    auto ctas_for = [&](uint64_t upc) { return p->ntiny ? ctas_big(upc) : ctas_all(upc); };
+    // Under an explicit cap (nzgpu_plan_set_max_ctas) every CTA counts: the
+    // caller promised the other SMs to concurrent work.
+    const bool tiny_outside = p->ntiny && !p->max_ctas;
+    auto ctas_for = [&](uint64_t upc) { return tiny_outside ? ctas_big(upc) : ctas_all(upc); };
     uint64_t bunits = 0;
     for (size_t i = 0; i < nbig; ++i) bunits += p->tunits[i];
     const uint64_t umax = *std::max_element(p->tunits.begin(), p->tunits.end());
-    uint64_t lo = std::max<uint64_t>(1, ceil_div(p->ntiny ? bunits : units, resident)), hi = lo;
+    uint64_t lo = std::max<uint64_t>(1, ceil_div(tiny_outside ? bunits : units, resident)), hi = lo;
     while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
     hi = std::max(lo, std::min(hi, umax));
     while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
@@ -1141,6 +1144,9 @@ int nzgpu_plan_launch_count(nzgpu_plan p) { return p && p->tiles ? 1 : 0; }
 
 int nzgpu_plan_set_max_ctas(nzgpu_plan p, uint32_t max_ctas) {
     if (!p) return NZGPU_INVALID_ARGUMENT;
+    // The schedule lives in device memory that in-flight launches of this plan
+    // read: wait for every queued launch (any stream) before rewriting it.
+    CK(cudaDeviceSynchronize());
     p->max_ctas = max_ctas;
     const std::vector<uint32_t> cta_prefix = persist_geometry(p);
     if (!cta_prefix.empty())

@@ -669,13 +669,8 @@ template <int LOG2K, int P>
 static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* cta_prefix, const DecodeDesc& one,
                             uint32_t ctas, uint32_t upc, uint32_t win_cap, cudaStream_t s) {
     const uint32_t smem = persist_smem(LOG2K, win_cap);
-    static uint32_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(decode_persist_kernel<LOG2K, P>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    static SmemAttr attr;  // per device: one process may drive several GPUs
+    if (cudaError_t e = attr.ensure((const void*)decode_persist_kernel<LOG2K, P>, smem)) return e;
     const MulConsts mc{1u};
     decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap, mc);
     return cudaGetLastError();

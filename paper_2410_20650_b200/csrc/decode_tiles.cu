@@ -461,13 +461,8 @@ template <int LOG2K, int P>
 static cudaError_t launch_decode_t(const DecodeDesc* descs, int ndesc, const uint64_t* prefix, const DecodeDesc& one,
                                    uint64_t tiles, uint32_t win_cap, cudaStream_t s) {
     const uint32_t smem = decode_smem_bytes(LOG2K, win_cap);
-    static uint32_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(decode_tiles_kernel<LOG2K, P>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured = smem;
-    }
+    static SmemAttr attr;  // per device: one process may drive several GPUs
+    if (cudaError_t e = attr.ensure((const void*)decode_tiles_kernel<LOG2K, P>, smem)) return e;
     decode_tiles_kernel<LOG2K, P><<<(unsigned)tiles, kDecodeThreads, smem, s>>>(descs, ndesc, prefix, one, win_cap);
     return cudaGetLastError();
 }

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace nzgpu {
 
 constexpr uint32_t kProbBits = 12;          // ans.hpp:30
@@ -166,5 +168,28 @@ __device__ __forceinline__ uint16_t bf16_from_float(float f) {
 }
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Per-device, thread-safe record of the dynamic shared-memory opt-in of one
+// kernel: the attribute is per (device, function), so a process that drives
+// several GPUs (one host thread per device) must set it on each of them.
+// Raising it concurrently from two threads is harmless (same call twice).
+struct SmemAttr {
+    static constexpr int kMaxDevices = 64;
+    std::atomic<uint32_t> configured[kMaxDevices] = {};
+
+    cudaError_t ensure(const void* func, uint32_t smem) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+        if (smem <= configured[dev].load(std::memory_order_acquire)) return cudaSuccess;
+        e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        uint32_t cur = configured[dev].load(std::memory_order_relaxed);
+        while (cur < smem && !configured[dev].compare_exchange_weak(cur, smem, std::memory_order_acq_rel)) {
+        }
+        return cudaSuccess;
+    }
+};
 
 }  // namespace nzgpu

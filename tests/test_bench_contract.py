@@ -73,3 +73,24 @@ def test_reference_arm_under_torchrun_prints_one_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_gpus_flag_spawns_local_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 local ranks
+    (the reference arm here, so it runs on CPU): one JSON line, n_gpus == 2,
+    and N>1 defaults to configs[3] (Llama-3-70B, LPT strong scaling)."""
+    from oracle.oracle import ref_available
+
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = run_bench("--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-tensors", "1",
+                  timeout=300)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == "strong" and "70B" in d["config"]["workload"]
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
