@@ -40,7 +40,7 @@ __global__ void pack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*, uint6
 __global__ void lossy_roundtrip_kernel(const uint16_t*, const uint8_t*, uint64_t, int, uint16_t*);
 __global__ void unpack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*);
 __global__ void seq_decode_kernel(const uint8_t*, const uint4*, const uint64_t*, uint32_t, uint64_t, const uint32_t*,
-                                  uint32_t, uint32_t, uint2*, uint8_t*, uint32_t*);
+                                  uint32_t, uint32_t, uint32_t*, uint32_t*, uint8_t*, uint8_t*, uint32_t*);
 __global__ void merge_plane_kernel(const uint8_t*, const uint8_t*, const uint8_t*, uint64_t, int, uint32_t,
                                    uint16_t*);
 cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int ndesc, const uint64_t* prefix,
@@ -92,7 +92,7 @@ using namespace nzgpu;
 namespace {
 
 constexpr uint32_t kIndexMagic = 0x58495A4Eu;  // "NZIX"
-constexpr uint32_t kIndexVersion = 2;  // 2: + max_window_unit
+constexpr uint32_t kIndexVersion = 3;  // 3: compact records (state, byte count, unit position)
 constexpr uint32_t kFlagIrregular = 2u;
 
 struct IndexHeader {
@@ -141,8 +141,7 @@ int status_from_bits(uint32_t bits) {
 int log2_of(uint32_t k) {
     switch (k) {
         case 64: return 6;
-        case 128: return 7;
-        case 256: return 8;
+        case 128: return 7;  // a sub-range's byte count must fit the index's count byte (K <= 128)
         default: return -1;
     }
 }
@@ -152,6 +151,11 @@ bool valid_precision(int p) { return p == 7 || p == 0 || p == 1 || p == 3; }
 uint64_t mant_bytes(uint64_t n, int p) { return (n * (uint64_t)(p + 1) + 7) / 8; }
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Side index region (nzgpu_internal.cuh): st u32[nsub] | base u32[units] |
+// cnt u8[nsub] -- the device layout and the exported bytes after the header.
+uint64_t index_units(uint64_t nsub) { return ceil_div(nsub, 32); }
+uint64_t index_region_bytes(uint64_t nsub) { return 4 * nsub + 4 * index_units(nsub) + nsub; }
 
 int device_ready() {
     int count = 0;
@@ -207,7 +211,7 @@ struct nzgpu_blob_s {
     uint4* chunk_info = nullptr;
     uint64_t* chunk_sym0 = nullptr;  // irregular framing only
     bool sym0_valid = false;          // chunk_sym0 filled (imported non-uniform framing)
-    uint2* ckpt = nullptr;
+    uint8_t* index = nullptr;  // side index region (index_region_bytes(nsub))
     uint32_t* err = nullptr;
     uint32_t* scratch_u32 = nullptr;  // 4 words: table info[3] + window
     // stream allocation
@@ -230,7 +234,9 @@ struct nzgpu_blob_s {
         d.stream = stream;
         d.mant = mant;
         d.scales = scales;
-        d.ckpt = ckpt;
+        d.ck_state = ck_state();
+        d.ck_base = ck_base();
+        d.ck_cnt = ck_cnt();
         d.chunk_info = chunk_info;
         d.lut = lut;
         d.out = out;
@@ -247,6 +253,9 @@ struct nzgpu_blob_s {
         return d;
     }
     uint64_t tiles() const { return decode_tiles_for(nsub); }
+    uint32_t* ck_state() const { return reinterpret_cast<uint32_t*>(index); }
+    uint32_t* ck_base() const { return ck_state() + nsub; }
+    uint8_t* ck_cnt() const { return reinterpret_cast<uint8_t*>(ck_base() + index_units(nsub)); }
 };
 
 namespace {
@@ -261,7 +270,7 @@ uint64_t blob_base_bytes(const nzgpu_blob_s* b, bool irregular) {
     cv.take(std::max<uint64_t>(b->scales_len, 1));
     cv.take(std::max<uint64_t>(b->nchunks, 1) * sizeof(uint4));
     cv.take(irregular ? std::max<uint64_t>(b->nchunks, 1) * 8 : 8);
-    cv.take(std::max<uint64_t>(b->nsub, 1) * sizeof(uint2) + 16);
+    cv.take(index_region_bytes(b->nsub) + 16);
     cv.take(64);
     return cv.size;
 }
@@ -274,7 +283,7 @@ int blob_alloc(nzgpu_blob_s* b, bool irregular, uint8_t* at = nullptr) {
     const uint64_t o_scales = cv.take(std::max<uint64_t>(b->scales_len, 1));
     const uint64_t o_info = cv.take(std::max<uint64_t>(b->nchunks, 1) * sizeof(uint4));
     const uint64_t o_sym0 = cv.take(irregular ? std::max<uint64_t>(b->nchunks, 1) * 8 : 8);
-    const uint64_t o_ckpt = cv.take(std::max<uint64_t>(b->nsub, 1) * sizeof(uint2) + 16);
+    const uint64_t o_index = cv.take(index_region_bytes(b->nsub) + 16);
     const uint64_t o_err = cv.take(64);
     if (at) {
         b->base = at;
@@ -288,7 +297,7 @@ int blob_alloc(nzgpu_blob_s* b, bool irregular, uint8_t* at = nullptr) {
     b->scales = p + o_scales;
     b->chunk_info = reinterpret_cast<uint4*>(p + o_info);
     b->chunk_sym0 = reinterpret_cast<uint64_t*>(p + o_sym0);
-    b->ckpt = reinterpret_cast<uint2*>(p + o_ckpt);
+    b->index = p + o_index;
     b->err = reinterpret_cast<uint32_t*>(p + o_err);
     b->scratch_u32 = b->err + 4;
     return NZGPU_OK;
@@ -447,7 +456,7 @@ int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
         seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
             b->stream, b->chunk_info, b->sym0_valid ? b->chunk_sym0 : nullptr, b->chunk_syms, b->nchunks, b->lut,
             b->flags & kFlagSingleSymbol, b->log2k,
-            nullptr, exps, b->err);
+            nullptr, nullptr, nullptr, exps, b->err);
         merge_plane_kernel<<<grid_for(b->n, 256), 256, 0, s>>>(exps, b->mant, b->scales, b->n, b->precision,
                                                                 b->block ? b->block : 1, d_out);
         CK(cudaGetLastError());
@@ -543,17 +552,17 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
         std::memcpy(&h, t->index, sizeof(h));
         have_index = h.magic == kIndexMagic && h.version == kIndexVersion && h.chunk_syms == S &&
                      h.interval == interval && h.n == t->n && h.nchunks == info.size() && h.nsub == b->nsub &&
-                     h.stream_len == t->stream_len && t->index_len == sizeof(h) + h.nsub * sizeof(uint2);
+                     h.stream_len == t->stream_len && t->index_len == sizeof(h) + index_region_bytes(h.nsub);
         if (have_index)
-            CK(cudaMemcpyAsync(b->ckpt, static_cast<const uint8_t*>(t->index) + sizeof(h), b->nsub * sizeof(uint2),
-                               cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(b->index, static_cast<const uint8_t*>(t->index) + sizeof(h),
+                               index_region_bytes(b->nsub), cudaMemcpyHostToDevice, s));
     }
     if (!have_index) {
         // K8: rebuild the checkpoint index by decoding every chunk once on
         // the GPU (full reference validation, ans.hpp:229-256).
         seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
-            b->stream, b->chunk_info, nullptr, S, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k, b->ckpt,
-            nullptr, b->err);
+            b->stream, b->chunk_info, nullptr, S, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k,
+            b->ck_state(), b->ck_base(), b->ck_cnt(), nullptr, b->err);
         CK(cudaGetLastError());
         rc = sync_status(s, b->err, true);
         if (rc) return rc;
@@ -704,7 +713,9 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         t.enc = enc;
         t.scratch = tmp + L.to[i].scratch;
         t.plen = reinterpret_cast<uint32_t*>(tmp + L.to[i].plen);
-        t.ckpt = irregular ? nullptr : b->ckpt;
+        t.ck_state = irregular ? nullptr : b->ck_state();
+        t.ck_base = irregular ? nullptr : b->ck_base();
+        t.ck_cnt = irregular ? nullptr : b->ck_cnt();
         t.err = b->err;
         t.chunk_info = b->chunk_info;
         t.hdr = tmp + L.to[i].hdr;
@@ -997,7 +1008,7 @@ int nzgpu_blob_info_get(nzgpu_blob b, nzgpu_blob_info* info) {
     info->stream_len = b->stream_len;
     info->mantissa_len = b->mant_len;
     info->scales_len = b->scales_len;
-    info->index_len = (b->flags & kFlagIrregular) ? 0 : sizeof(IndexHeader) + b->nsub * sizeof(uint2);
+    info->index_len = (b->flags & kFlagIrregular) ? 0 : sizeof(IndexHeader) + index_region_bytes(b->nsub);
     info->payload_bytes = b->stream_len + b->mant_len + b->scales_len + 512;
     info->d_stream = b->stream;
     info->d_freqs = b->freqs;
@@ -1026,7 +1037,7 @@ int nzgpu_blob_export(nzgpu_blob b, uint16_t* freqs, uint8_t* stream, uint8_t* m
                       b->max_window_unit, 0};
         std::memcpy(index, &h, sizeof(h));
         if (b->nsub)
-            CK(cudaMemcpy(static_cast<uint8_t*>(index) + sizeof(h), b->ckpt, b->nsub * sizeof(uint2),
+            CK(cudaMemcpy(static_cast<uint8_t*>(index) + sizeof(h), b->index, index_region_bytes(b->nsub),
                           cudaMemcpyDeviceToHost));
     }
     return NZGPU_OK;
@@ -1277,9 +1288,10 @@ struct HostCtx {
 };
 thread_local std::unique_ptr<HostCtx> g_host;
 
-// Host replica of tile_window() over the host copy of the index: the decode
-// kernel's shared-memory window size without a device round trip.
-uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint64_t nsub, uint32_t S, int log2k,
+// Host replica of tile_window() over the host copy of the index's unit
+// positions: the decode kernel's shared-memory window size without a device
+// round trip (ts = sub-ranges per tile/unit, a multiple of 32).
+uint32_t host_max_window(const std::vector<uint4>& info, const uint32_t* base, uint64_t nsub, uint32_t S, int log2k,
                          uint64_t ts) {
     const uint64_t spc = S >> log2k;
     // sub-range -> chunk by shift when S/K is a power of two (the default
@@ -1292,14 +1304,14 @@ uint32_t host_max_window(const std::vector<uint4>& info, const uint2* ckpt, uint
         const uint64_t subs = std::min<uint64_t>(ts, nsub - sub0);
         const uint4 c0 = info[chunk_of(sub0)];
         const uint64_t lim0 = c0.z >= 4 ? c0.z - 4 : 0;
-        const uint64_t e0 = in_chunk(sub0) == 0 ? lim0 : std::min<uint64_t>(ckpt[sub0].y, lim0);
-        const uint64_t a = ((uint64_t)c0.x | ((uint64_t)c0.y << 32)) + lim0 - e0;
-        const uint64_t jl = sub0 + subs - 1;
+        const uint64_t a = ((uint64_t)c0.x | ((uint64_t)c0.y << 32)) +
+                           (in_chunk(sub0) == 0 ? 0 : std::min<uint64_t>(base[sub0 >> 5], lim0));
+        const uint64_t jl = sub0 + subs - 1, jn = jl + 1;
         const uint4 c1 = info[chunk_of(jl)];
         const uint64_t lim1 = c1.z >= 4 ? c1.z - 4 : 0;
         const bool chunk_end = ((in_chunk(jl) + 1) << log2k) >= c1.w;
-        const uint64_t e1 = (jl + 1 < nsub && !chunk_end) ? std::min<uint64_t>(ckpt[jl + 1].y, lim1) : 0;
-        uint64_t b = ((uint64_t)c1.x | ((uint64_t)c1.y << 32)) + lim1 - e1;
+        uint64_t b = ((uint64_t)c1.x | ((uint64_t)c1.y << 32)) +
+                     ((jn < nsub && !chunk_end) ? std::min<uint64_t>(base[jn >> 5], lim1) : lim1);
         if (b < a) b = a;
         best = std::max<uint64_t>(best, align_up(b, 16) - (a & ~(uint64_t)15));
     }
@@ -1342,11 +1354,12 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     const int log2k = log2_of(h.interval);
     if (h.magic != kIndexMagic || h.version != kIndexVersion || log2k < 0 || h.chunk_syms != S || h.n != t->n ||
         h.nchunks != info.size() || h.stream_len != t->stream_len || S % h.interval ||
-        h.nsub != ceil_div(t->n, h.interval) || t->index_len != sizeof(h) + h.nsub * sizeof(uint2))
+        h.nsub != ceil_div(t->n, h.interval) || t->index_len != sizeof(h) + index_region_bytes(h.nsub))
         return 1;
     for (size_t c = 0; c < info.size(); ++c)
         if (c + 1 < info.size() ? info[c].w != S : (info[c].w == 0 || info[c].w > S)) return 1;
-    const uint2* ck = reinterpret_cast<const uint2*>(static_cast<const uint8_t*>(t->index) + sizeof(h));
+    const uint8_t* ix = static_cast<const uint8_t*>(t->index) + sizeof(h);
+    const uint32_t* ix_base = reinterpret_cast<const uint32_t*>(ix) + h.nsub;  // may be unaligned: memcpy'd below
 
     nzgpu_blob_s& b = *new (std::nothrow) nzgpu_blob_s;  // descriptor only; buffers belong to the slot
     std::unique_ptr<nzgpu_blob_s> guard(&b);
@@ -1369,7 +1382,7 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     const uint64_t o_freqs = cv.take(512), o_lut = cv.take(16384), o_mant = cv.take(b.mant_len + 16);
     const uint64_t o_scales = cv.take(std::max<uint64_t>(b.scales_len, 1));
     const uint64_t o_info = cv.take(info.size() * sizeof(uint4));
-    const uint64_t o_ckpt = cv.take(b.nsub * sizeof(uint2) + 16), o_scr = cv.take(64);
+    const uint64_t o_index = cv.take(index_region_bytes(b.nsub) + 16), o_scr = cv.take(64);
     cudaStream_t s = sl.s;
     clk.lap(0);  // parse + validate
     if (int rc = sl.main.ensure(cv.size, s)) return rc;
@@ -1381,7 +1394,7 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     b.mant = m + o_mant;
     b.scales = m + o_scales;
     b.chunk_info = reinterpret_cast<uint4*>(m + o_info);
-    b.ckpt = reinterpret_cast<uint2*>(m + o_ckpt);
+    b.index = m + o_index;
     b.scratch_u32 = reinterpret_cast<uint32_t*>(m + o_scr);
     b.stream = static_cast<uint8_t*>(sl.stream.p);
     b.err = sl.err;
@@ -1395,7 +1408,7 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     if (int rc = sl.stage_info(info, &info_pinned)) return rc;
     CK(cudaMemcpyAsync(b.chunk_info, info_pinned, info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
     if (int rc = sl.info_issued()) return rc;
-    CK(cudaMemcpyAsync(b.ckpt, ck, b.nsub * sizeof(uint2), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.index, ix, index_region_bytes(b.nsub), cudaMemcpyHostToDevice, s));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
     clk.lap(3);  // chunk table + index + LUT
@@ -1403,12 +1416,20 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
         // the index's hint when plausible (at most 2 bytes per symbol plus the
         // framing of the two chunks a unit can touch), else a scan
         const uint64_t bound = 64ull * h.interval + 64;
+        std::vector<uint32_t> units;  // the unit positions, aligned (the host index may not be)
+        auto unit_pos = [&]() -> const uint32_t* {
+            if (units.empty()) {
+                units.resize(index_units(b.nsub));
+                std::memcpy(units.data(), ix_base, units.size() * 4);
+            }
+            return units.data();
+        };
         b.max_window_unit = h.max_window_unit && h.max_window_unit <= bound
                                 ? h.max_window_unit
-                                : host_max_window(info, ck, b.nsub, S, log2k, 32);
+                                : host_max_window(info, unit_pos(), b.nsub, S, log2k, 32);
         // the tile window only matters when the persistent kernel cannot run
         if (!(use_persist() && persist_fits(log2k, b.max_window_unit)))
-            b.max_window = host_max_window(info, ck, b.nsub, S, log2k, decode_tile_subs());
+            b.max_window = host_max_window(info, unit_pos(), b.nsub, S, log2k, decode_tile_subs());
     }
     clk.lap(4);  // windows
     if (int rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), s)) return rc;

@@ -54,24 +54,45 @@ __device__ __forceinline__ void sub_to_chunk(const DecodeDesc& d, int log2k, uin
     }
 }
 
-// Absolute stream window [a, b) of renormalisation bytes a tile reads.
-__device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, uint32_t tile_subs, int log2k,
+// Absolute stream window [a, b) of the renormalisation bytes that sub-ranges
+// [sub0, sub0 + subs) read, for sub0 a multiple of 32 (a unit start) and
+// sub0 + subs a multiple of 32 or nsub: it starts at sub-range sub0's
+// position and ends where the next unit starts (when that unit begins inside
+// the last sub-range's chunk) or at that chunk's end.  O(1) in the index.
+__device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, uint32_t subs, int log2k,
                                             uint32_t nsub, uint64_t& a, uint64_t& b) {
     uint32_t c0, j0in, c1, jlin;
     sub_to_chunk(d, log2k, sub0, c0, j0in);
     const uint4 ci0 = d.chunk_info[c0];
     const uint32_t lim0 = ci0.z >= 4 ? ci0.z - 4 : 0;
-    const uint32_t e0 = j0in == 0 ? lim0 : min(d.ckpt[sub0].y, lim0);
-    a = chunk_offset(ci0) + lim0 - e0;
-    const uint32_t jl = sub0 + tile_subs - 1;
+    a = chunk_offset(ci0) + (j0in == 0 ? 0u : min(d.ck_base[sub0 >> 5], lim0));
+    const uint32_t jl = sub0 + subs - 1, jn = jl + 1;
     sub_to_chunk(d, log2k, jl, c1, jlin);
     const uint4 ci1 = d.chunk_info[c1];
     const uint32_t lim1 = ci1.z >= 4 ? ci1.z - 4 : 0;
-    const uint32_t jn = jl + 1;
     const bool chunk_end = ((uint64_t)(jlin + 1) << log2k) >= ci1.w;
-    const uint32_t e1 = (jn < nsub && !chunk_end) ? min(d.ckpt[jn].y, lim1) : 0;
-    b = chunk_offset(ci1) + lim1 - e1;
+    b = chunk_offset(ci1) + ((jn < nsub && !chunk_end) ? min(d.ck_base[jn >> 5], lim1) : lim1);
     if (b < a) b = a;
+}
+
+// Positions of the 32 sub-ranges of a warp unit (warp-collective: every lane
+// calls it).  `cnt` = this lane's consumed-byte count, `base` = the unit's
+// position record, `head` = this lane starts a chunk (its position is 0).
+// Returns this lane's start position relative to its chunk's payload start:
+// base (or 0 after a chunk head) plus the counts of the earlier lanes of the
+// same chunk segment.
+__device__ __forceinline__ uint32_t unit_lane_start(uint32_t cnt, uint32_t base, bool head, uint32_t lane) {
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t heads = __ballot_sync(0xFFFFFFFFu, head) & (0xFFFFFFFFu >> (31 - lane));  // heads at or below me
+    const int h = heads ? 31 - __clz(heads) : 0;
+    const uint32_t at_head = __shfl_sync(0xFFFFFFFFu, excl, h);
+    return heads ? excl - at_head : base + excl;
 }
 
 // bitwise c ? a : b in one LOP3

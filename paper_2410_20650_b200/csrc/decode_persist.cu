@@ -248,32 +248,42 @@ struct LaneJob {
 };
 
 // Raw index records of a lane's sub-range, loaded one unit ahead so the
-// global-memory latency never sits on a warp's critical path.
+// global-memory latency never sits on a warp's critical path: the chunk
+// record, the lane's state and the next sub-range's (its end state), its
+// consumed-byte count and the unit's position record (a broadcast load).
 struct RawRec {
     uint4 ci;
-    uint2 rec, nxt;
+    uint32_t st, st1, cnt, base;
 };
 
 template <int LOG2K>
 __device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint32_t nsub) {
-    RawRec r{make_uint4(0, 0, 0, 0), make_uint2(0, 0), make_uint2(0, 0)};
+    RawRec r{make_uint4(0, 0, 0, 0), 0u, 0u, 0u, 0u};
     if (j >= nsub) return r;
     uint32_t ch, jin;
     sub_to_chunk(d, LOG2K, j, ch, jin);
     r.ci = d.chunk_info[ch];
-    r.rec = d.ckpt[j];
-    if (j + 1 < nsub) r.nxt = d.ckpt[j + 1];
+    if (d.ck_state) {  // null for single-symbol tables (no index)
+        r.st = d.ck_state[j];
+        if (j + 1 < nsub) r.st1 = d.ck_state[j + 1];
+        r.cnt = d.ck_cnt[j];
+        r.base = d.ck_base[j >> 5];
+    }
     return r;
 }
 
+// Warp-collective (every lane calls it, also lanes past the tensor's end).
 template <int LOG2K>
 __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uint32_t nsub, bool single,
-                                            const RawRec& raw, uint32_t lo0) {
+                                            const RawRec& raw, uint32_t lo0, uint32_t lane) {
     constexpr int K = 1 << LOG2K;
     LaneJob L{kStateLow, kStateLow, 0u, 0u, 0u, 0u};
-    if (j >= nsub) return L;
-    uint32_t ch, jin;
-    sub_to_chunk(d, LOG2K, j, ch, jin);
+    const bool valid = j < nsub;
+    uint32_t ch = 0, jin = 0;
+    if (valid) sub_to_chunk(d, LOG2K, j, ch, jin);
+    // chunk-relative start of this lane (single-symbol tables read no bytes)
+    const uint32_t start = single ? 0u : unit_lane_start(valid ? raw.cnt : 0u, raw.base, valid && jin == 0, lane);
+    if (!valid) return L;
     const uint4 ci = raw.ci;
     const uint64_t off = chunk_offset(ci);
     const uint32_t len = ci.z, nsym = ci.w;
@@ -293,17 +303,16 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
         L.p0 = L.pe = ci.x - lo0 + limit;
         return L;
     }
-    const uint2 rec = raw.rec;
+    // The last sub-range of a chunk ends on the reference's end-of-chunk
+    // condition (x == 2^23 at len - 4, ans.hpp:252); the others on the next
+    // sub-range's state and position.
     const bool last = sym_in + K >= nsym;
-    const uint2 end = last ? make_uint2(kStateLow, 0u) : raw.nxt;
-    const uint32_t e_start = jin == 0 ? limit : rec.y;
-    if (jin != 0) L.x0 = rec.x;
-    L.xe = end.x;
-    if (e_start > limit || end.y > limit) L.err |= kErrDesync;
-    const uint32_t rel = ci.x - lo0 + limit;  // chunk offsets of one unit differ by < 2^32
-    L.p0 = rel - min(e_start, limit);
-    L.pe = rel - min(end.y, limit);
-    if (L.pe < L.p0) L.err |= kErrDesync;
+    if (jin != 0) L.x0 = raw.st;
+    L.xe = last ? kStateLow : raw.st1;
+    const uint32_t end = start + raw.cnt;
+    if (start > limit || end > limit || (last && end != limit)) L.err |= kErrDesync;
+    L.p0 = ci.x - lo0 + min(start, limit);  // chunk offsets of one unit differ by < 2^32
+    L.pe = ci.x - lo0 + min(end, limit);
     return L;
 }
 
@@ -381,7 +390,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     // whose 64-bit offset only lane 0 needs, for the TMA source).
     auto stage = [&](uint32_t u, int b, uint32_t& wa_out, const RawRec& raw) -> LaneJob {
         const uint32_t lo0 = __shfl_sync(0xFFFFFFFFu, raw.ci.x, 0);
-        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw, lo0);
+        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw, lo0, lane);
         const uint32_t a = __shfl_sync(0xFFFFFFFFu, L.p0, 0);
         const uint32_t last_lane = min(31u, nsub - u * 32 - 1);
         const uint32_t e = __shfl_sync(0xFFFFFFFFu, L.pe, last_lane);
@@ -695,7 +704,6 @@ cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* de
     switch (log2k) {
         case 6: return launch_pk<6>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
         case 7: return launch_pk<7>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
-        case 8: return launch_pk<8>(precision, descs, ndesc, cta_prefix, one, ctas, upc, win_cap, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -729,7 +737,6 @@ cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out
     switch (log2k) {
         case 6: unit_window_max_kernel<6><<<148, 256, 0, s>>>(d, out); break;
         case 7: unit_window_max_kernel<7><<<148, 256, 0, s>>>(d, out); break;
-        case 8: unit_window_max_kernel<8><<<148, 256, 0, s>>>(d, out); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

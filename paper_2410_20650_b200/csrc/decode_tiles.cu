@@ -236,10 +236,20 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
         cnt[c] = 0;
         x[c] = xe[c] = kStateLow;
         p[c] = pe[c] = sbase + kWinOff;
-        if (r < tile_subs) {
-            const uint32_t j = sub0 + r;
-            uint32_t ch, jin;
+        // every warp holds one 32-sub-range unit (sub0 and c*T are multiples
+        // of 32): lane positions from one warp scan of the count records
+        const uint32_t j = sub0 + r;
+        const bool valid = r < tile_subs;
+        uint32_t ch = 0, jin = 0, cb = 0, base = 0;
+        if (valid) {
             sub_to_chunk(d, LOG2K, j, ch, jin);
+            if (!single) {
+                cb = d.ck_cnt[j];
+                base = d.ck_base[j >> 5];
+            }
+        }
+        const uint32_t start = single ? 0u : unit_lane_start(cb, base, valid && jin == 0, tid & 31u);
+        if (valid) {
             const uint4 ci = d.chunk_info[ch];
             const uint64_t off = chunk_offset(ci);
             const uint32_t len = ci.z, nsym = ci.w;
@@ -261,15 +271,14 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
                 if (jin == 0 && len >= 4 && (x[c] != kStateLow || len != 4))
                     errs |= x[c] < kStateLow ? kErrTruncated : kErrDesync;
             } else {
-                const uint2 rec = d.ckpt[j];
                 const bool last = sym_in + K >= nsym;
-                const uint2 end = last ? make_uint2(kStateLow, 0u) : d.ckpt[j + 1];
-                const uint32_t e_start = jin == 0 ? limit : rec.y;
-                if (jin != 0) x[c] = rec.x;
-                xe[c] = end.x;
-                const int64_t p0 = (int64_t)(off + limit - e_start) - (int64_t)wa;
-                const int64_t p1 = (int64_t)(off + limit - min(end.y, limit)) - (int64_t)wa;
-                if (e_start > limit || end.y > limit || p0 < 0 || p0 > (int64_t)win_cap || p1 < p0)
+                if (jin != 0) x[c] = d.ck_state[j];
+                xe[c] = last ? kStateLow : d.ck_state[j + 1];
+                const uint32_t end = start + cb;
+                const int64_t p0 = (int64_t)(off + min(start, limit)) - (int64_t)wa;
+                const int64_t p1 = (int64_t)(off + min(end, limit)) - (int64_t)wa;
+                if (start > limit || end > limit || (last && end != limit) || p0 < 0 || p1 > (int64_t)win_cap ||
+                    p1 < p0)
                     errs |= kErrDesync;
                 else {
                     p[c] = sbase + kWinOff + (uint32_t)p0;
@@ -485,7 +494,6 @@ cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int
     switch (log2k) {
         case 6: return launch_decode_k<6>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
         case 7: return launch_decode_k<7>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
-        case 8: return launch_decode_k<8>(precision, descs, ndesc, prefix, one, tiles, win_cap, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -505,7 +513,6 @@ cudaError_t launch_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cud
     switch (log2k) {
         case 6: window_max_kernel<6><<<148, 256, 0, s>>>(d, out); break;
         case 7: window_max_kernel<7><<<148, 256, 0, s>>>(d, out); break;
-        case 8: window_max_kernel<8><<<148, 256, 0, s>>>(d, out); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -11,9 +11,12 @@
 // Renormalisation bytes are emitted in reverse consumption order, so they
 // are written backwards from the end of a per-chunk scratch slot; the
 // payload (ans.hpp:222-223) is then contiguous and in decoder order.
-// Every K symbols the encoder also records {state, bytes emitted so far} --
-// the checkpoint side index that lets the decoder split a chunk into
-// independent sub-ranges.
+// Every K symbols the encoder also records the side index that lets the
+// decoder split a chunk into independent sub-ranges (nzgpu_internal.cuh):
+// the state, the bytes the sub-range consumes (emitted since the previous
+// checkpoint, which in reverse order is the NEXT sub-range), and for every
+// 32nd sub-range its decoder position -- known only once the chunk is done
+// (len - 4 - bytes emitted from there on), so it is fixed up at the end.
 //
 // K4 restates serialize_stream (ans.hpp:306-316): an exclusive scan of
 // (8 + len) over chunks, then a copy of every payload behind its header.
@@ -45,7 +48,10 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     __syncthreads();
     const uint64_t n = t.n;
     const uint32_t chunk_syms = t.chunk_syms, log2_interval = t.log2k;
-    uint2* const ckpt = t.ckpt;
+    uint32_t* const ck_state = t.ck_state;
+    uint32_t* const ck_base = t.ck_base;
+    uint8_t* const ck_cnt = t.ck_cnt;
+    uint32_t e_prev = 0;  // bytes emitted at the previous (later) checkpoint
     const uint64_t nchunks = ceil_div(n, chunk_syms);
     const uint64_t c = (blockIdx.x - t.cta0) * (uint64_t)blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
@@ -94,10 +100,16 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
         // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
         const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
         x = q * (kProbScale - e.freq) + (x + e.cum);
-        if (may_ckpt && ckpt && (i & kmask) == 0) ckpt[(begin + i) >> log2_interval] = make_uint2(x, emitted);
+        if (may_ckpt && ck_state && (i & kmask) == 0) {
+            const uint64_t j = (begin + i) >> log2_interval;
+            ck_state[j] = x;
+            ck_cnt[j] = (uint8_t)(emitted - e_prev);  // <= 1.5K + 2 < 256 for K <= 128
+            e_prev = emitted;
+            if ((j & 31) == 0) ck_base[j >> 5] = emitted;  // fixed up below
+        }
     };
     uint32_t i = len;
-    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (!ckpt || (kmask & 15) == 15)) {
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (!ck_state || (kmask & 15) == 15)) {
         // 16 symbols per aligned load, walked backwards in registers; with
         // K a multiple of 16 only the block's first symbol can be a checkpoint
         for (const uint32_t top = len & ~15u; i > top;) {
@@ -133,6 +145,11 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie below
     // the payload start, inside the slot.
     if (QUEUE && qc) *--wo = __byte_perm(qhi, 0, 0x0123) << (32 - 8 * qc);
+    if (ck_state) {
+        // unit bases of this chunk: position = (len - 4) - bytes emitted after it
+        const uint64_t j0 = begin >> log2_interval, j1 = (begin + len - 1) >> log2_interval;
+        for (uint64_t u = (j0 + 31) >> 5; (u << 5) <= j1; ++u) ck_base[u] = emitted - ck_base[u];
+    }
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
     t.plen[c] = emitted + 4;

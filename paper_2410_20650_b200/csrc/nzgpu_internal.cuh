@@ -5,14 +5,21 @@
 //   payload = renormalisation bytes in decoder order || LE32(final state)
 // Table: 256 x u16 frequencies summing to 4096 (ans.hpp:111-118).
 //
-// Side index (ours; NOT part of the reference format or the ratio):
-//   ckpt[j] = {state, E} for global symbol j*K, where state is the decoder
-//   state before symbol j*K (= the encoder state after encoding it) and E is
-//   the number of renormalisation bytes that follow the decoder's position
-//   there (bytes the encoder emitted for symbols j*K..end of chunk).  The
-//   decoder position of sub-range j is (len-4) - E; the sentinel after the
-//   last sub-range of a chunk is {2^23, 0}, which is exactly the reference's
-//   end-of-chunk check (ans.hpp:252).
+// Side index (ours; NOT part of the reference format or the ratio), one
+// record set per sub-range j of K symbols (global symbols [jK, jK+K)) and per
+// warp unit u of 32 consecutive sub-ranges:
+//   st[j]   u32  decoder state before symbol jK (= the encoder state after
+//                encoding it);
+//   cnt[j]  u8   renormalisation bytes sub-range j consumes (<= 1.5K + 2, so
+//                a byte for K <= 128);
+//   base[u] u32  decoder byte position (from its chunk's payload start) of
+//                sub-range 32u.
+// A lane's position is its chunk's payload start plus base (or 0 for the
+// first sub-range of a chunk) plus the counts of the lanes before it in the
+// same chunk: one warp prefix scan.  A sub-range must end on the next
+// sub-range's state and position; the last one of a chunk on (2^23, len-4),
+// the reference's end-of-chunk check (ans.hpp:252).  5 bytes per K symbols +
+// 4 per 32K: 0.080 B/element at K = 64, 0.041 at K = 128.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -68,7 +75,9 @@ struct EncTask {
     const EncSym* enc;       // 256 encoder constants
     uint8_t* scratch;        // nchunks slots of slot_bytes (16-B aligned)
     uint32_t* plen;          // payload length per chunk
-    uint2* ckpt;             // checkpoint index, or nullptr
+    uint32_t* ck_state;      // side index (st[], cnt[], base[]), or nullptr
+    uint32_t* ck_base;
+    uint8_t* ck_cnt;
     uint32_t* err;           // sticky error word
     uint4* chunk_info;       // K4 out: {off lo, off hi, len, nsym}
     uint8_t* hdr;            // K4 out: the stream's leading u32 chunk count
@@ -95,7 +104,9 @@ struct DecodeDesc {
     const uint8_t* stream;        // serialized stream (reference layout), 16-B aligned + 16 B pad
     const uint8_t* mant;          // lossless: n bytes (s<<7|m); lossy: packed (k+1)-bit items
     const uint8_t* scales;        // lossy block scale bytes
-    const uint2* ckpt;            // {state, E} per K symbols
+    const uint32_t* ck_state;     // side index: state per sub-range
+    const uint32_t* ck_base;      //   position of sub-range 32u in its chunk
+    const uint8_t* ck_cnt;        //   renormalisation bytes per sub-range
     const uint4* chunk_info;      // {payload offset lo, hi, len, nsym} per chunk
     const uint32_t* lut;          // 4096 packed decode entries
     uint16_t* out;                // bf16 output, 16-B aligned

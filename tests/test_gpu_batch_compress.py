@@ -97,10 +97,13 @@ def test_gpu_compress_batch_errors(nz, port):
     assert (b.decompress().view(torch.int16).cpu().numpy().view(np.uint16) == good).all()
 
 
-@pytest.mark.parametrize("chunk,interval", [(65536, 128), (65536, 256), (131072, 0), (1 << 14, 64), (100000, 0)])
+@pytest.mark.parametrize("chunk,interval", [(65536, 128), (3 * 4096, 128), (131072, 0), (1 << 14, 64), (2560, 64),
+                                            (100000, 0)])
 def test_gpu_compress_batch_chunk_and_interval(nz, port, chunk, interval):
     """Non-default chunk sizes S and checkpoint strides K, including an S no
-    stride divides (100000: reference framing, sequential decode, no index)."""
+    stride divides (100000: reference framing, sequential decode, no index)
+    and S/K = 40 (2560/64: 32-sub-range warp units straddle chunks, so the
+    index's position scan restarts mid-unit)."""
     import torch
 
     ts = [port.gaussian_bf16(port.derive(21, i), n, 0.02) for i, n in enumerate([5, 70001, 3 * 131072 + 9, 1 << 20])]

@@ -54,13 +54,50 @@ def test_gpu_decodes_reference_produced_streams(nz, port, case):
     assert (nz.decompress_lossless(blob) == v).all()
 
 
-@pytest.mark.parametrize("interval", [64, 128, 256])
+@pytest.mark.parametrize("interval", [64, 128])
 def test_gpu_checkpoint_intervals(nz, port, interval):
     v = port.gaussian_bf16(123, 3 * 65536 + 777, 0.02)
     blob = nz.compress_lossless(v, interval=interval)
     f, s, sm = port.compress_lossless(v)
     assert blob.stream == s and (blob.signmant == sm).all()
     assert (nz.decompress_lossless(blob) == v).all()
+    # compact side index: 56-byte header + 5 bytes per sub-range + 4 per unit
+    nsub = -(-v.size // interval)
+    assert len(blob.index) == 56 + 5 * nsub + 4 * (-(-nsub // 32))
+    assert len(blob.index) / v.size < (0.0802 if interval == 64 else 0.0412)
+
+
+def test_gpu_interval_256_rejected(nz, port):
+    """A sub-range's renormalisation byte count is one index byte, which
+    bounds K at 128 (<= 1.5 K + 2 bytes per sub-range)."""
+    v = port.gaussian_bf16(123, 70001, 0.02)
+    with pytest.raises(ValueError):
+        nz.compress_lossless(v, interval=256)
+
+
+@pytest.mark.parametrize("what", ["state", "count", "base"])
+def test_gpu_corrupt_index_is_a_format_error(nz, port, what):
+    """A damaged side index (not part of the reference format) must surface
+    as the reference's FormatError -- every sub-range has to land exactly on
+    the next one's state and position -- never as a wrong decode."""
+    v = port.gaussian_bf16(77, 1 << 20, 0.02)
+    blob = nz.compress_lossless(v)
+    ix = bytearray(blob.index)
+    nsub = (1 << 20) // 64
+    units = nsub // 32
+    j = 12345  # a sub-range in the middle of a chunk (chunk 12, not its first)
+    if what == "state":
+        off = 56 + 4 * j
+        ix[off] ^= 0x40
+    elif what == "count":
+        off = 56 + 4 * nsub + 4 * units + j
+        ix[off] = (ix[off] + 3) & 0xFF
+    else:
+        off = 56 + 4 * nsub + 4 * (j // 32)
+        ix[off] ^= 0x08
+    bad = nz.LosslessBlob(blob.meta, blob.freqs, blob.stream, blob.signmant, index=bytes(ix))
+    with pytest.raises(nz.FormatError):
+        nz.decompress_batch([bad])
 
 
 @pytest.mark.parametrize("dist", ["gaussian", "uniform", "laplace"])
