@@ -181,6 +181,9 @@ int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint3
  * GPU decode, D2H of the bf16 result.  Staging buffers are cached by the
  * library; pinned host memory gives full PCIe bandwidth. */
 int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out);
+/* Decode a device blob into host memory (GPU decode on a private stream,
+ * then D2H; pinned or pageable `out`, n bf16).  Synchronous. */
+int nzgpu_blob_decompress_host(nzgpu_blob blob, uint16_t* out);
 /* Same for `count` tensors, pipelined across two CUDA streams (H2D of tensor
  * i+1 overlaps decode of i and D2H of i-1). */
 int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t* const* outs);

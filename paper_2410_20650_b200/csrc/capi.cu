@@ -40,7 +40,7 @@ __global__ void pack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*, uint6
 __global__ void lossy_roundtrip_kernel(const uint16_t*, const uint8_t*, uint64_t, int, uint16_t*);
 __global__ void unpack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*);
 __global__ void seq_decode_kernel(const uint8_t*, const uint4*, const uint64_t*, uint32_t, uint64_t, const uint32_t*,
-                                  uint32_t, uint32_t, uint32_t*, uint32_t*, uint8_t*, uint8_t*, uint32_t*);
+                                  uint32_t, uint32_t, uint32_t*, uint32_t*, uint16_t*, uint8_t*, uint32_t*);
 __global__ void merge_plane_kernel(const uint8_t*, const uint8_t*, const uint8_t*, uint64_t, int, uint32_t,
                                    uint16_t*);
 cudaError_t launch_decode(int log2k, int precision, const DecodeDesc* descs, int ndesc, const uint64_t* prefix,
@@ -153,9 +153,9 @@ uint64_t mant_bytes(uint64_t n, int p) { return (n * (uint64_t)(p + 1) + 7) / 8;
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // Side index region (nzgpu_internal.cuh): st u32[nsub] | base u32[units] |
-// cnt u8[nsub] -- the device layout and the exported bytes after the header.
+// off u16[nsub] -- the device layout and the exported bytes after the header.
 uint64_t index_units(uint64_t nsub) { return ceil_div(nsub, 32); }
-uint64_t index_region_bytes(uint64_t nsub) { return 4 * nsub + 4 * index_units(nsub) + nsub; }
+uint64_t index_region_bytes(uint64_t nsub) { return 4 * nsub + 4 * index_units(nsub) + 2 * nsub; }
 
 int device_ready() {
     int count = 0;
@@ -236,7 +236,7 @@ struct nzgpu_blob_s {
         d.scales = scales;
         d.ck_state = ck_state();
         d.ck_base = ck_base();
-        d.ck_cnt = ck_cnt();
+        d.ck_off = ck_off();
         d.chunk_info = chunk_info;
         d.lut = lut;
         d.out = out;
@@ -255,7 +255,7 @@ struct nzgpu_blob_s {
     uint64_t tiles() const { return decode_tiles_for(nsub); }
     uint32_t* ck_state() const { return reinterpret_cast<uint32_t*>(index); }
     uint32_t* ck_base() const { return ck_state() + nsub; }
-    uint8_t* ck_cnt() const { return reinterpret_cast<uint8_t*>(ck_base() + index_units(nsub)); }
+    uint16_t* ck_off() const { return reinterpret_cast<uint16_t*>(ck_base() + index_units(nsub)); }
 };
 
 namespace {
@@ -562,7 +562,7 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
         // the GPU (full reference validation, ans.hpp:229-256).
         seq_decode_kernel<<<grid_for(b->nchunks, 128, 1u << 30), 128, 0, s>>>(
             b->stream, b->chunk_info, nullptr, S, b->nchunks, b->lut, b->flags & kFlagSingleSymbol, b->log2k,
-            b->ck_state(), b->ck_base(), b->ck_cnt(), nullptr, b->err);
+            b->ck_state(), b->ck_base(), b->ck_off(), nullptr, b->err);
         CK(cudaGetLastError());
         rc = sync_status(s, b->err, true);
         if (rc) return rc;
@@ -715,7 +715,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         t.plen = reinterpret_cast<uint32_t*>(tmp + L.to[i].plen);
         t.ck_state = irregular ? nullptr : b->ck_state();
         t.ck_base = irregular ? nullptr : b->ck_base();
-        t.ck_cnt = irregular ? nullptr : b->ck_cnt();
+        t.ck_off = irregular ? nullptr : b->ck_off();
         t.err = b->err;
         t.chunk_info = b->chunk_info;
         t.hdr = tmp + L.to[i].hdr;
@@ -1499,6 +1499,22 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
 }
 
 int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out) { return nzgpu_decompress_host_batch(t, 1, &out); }
+
+int nzgpu_blob_decompress_host(nzgpu_blob b, uint16_t* out) {
+    if (!b || (!out && b->n)) return NZGPU_INVALID_ARGUMENT;
+    if (b->n == 0) return NZGPU_OK;
+    StreamGuard sg{StreamGuard::Own{}};
+    uint16_t* d = nullptr;
+    CK(cudaMallocAsync(&d, align_up(b->n * 2, 16) + 16, sg.s));
+    int rc = decode_blob(b, d, sg.s);
+    if (!rc) {
+        const cudaError_t e = cudaMemcpyAsync(out, d, b->n * 2, cudaMemcpyDeviceToHost, sg.s);
+        if (e != cudaSuccess) rc = fail_cuda(e, "cudaMemcpyAsync");
+    }
+    cudaFreeAsync(d, sg.s);
+    const int st = sync_status(sg.s, b->err, true);
+    return rc ? rc : st;
+}
 
 int nzgpu_host_release(void) {
     if (g_host) {

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(128) seq_decode_kernel(const uint8_t* __restri
                                                          uint32_t chunk_syms, uint64_t nchunks,
                                                          const uint32_t* __restrict__ lut_g, uint32_t flags,
                                                          uint32_t log2k, uint32_t* __restrict__ ck_state,
-                                                         uint32_t* __restrict__ ck_base, uint8_t* __restrict__ ck_cnt,
+                                                         uint32_t* __restrict__ ck_base, uint16_t* __restrict__ ck_off,
                                                          uint8_t* __restrict__ exps, uint32_t* __restrict__ err) {
     __shared__ uint32_t lut[4096];
     for (int i = threadIdx.x; i < 4096; i += blockDim.x) lut[i] = lut_g[i];
@@ -39,18 +39,16 @@ __global__ void __launch_bounds__(128) seq_decode_kernel(const uint8_t* __restri
     uint32_t pos = 0;
     const uint32_t kmask = (1u << log2k) - 1u;
     const bool single = flags & kFlagSingleSymbol;
-    // side index (nzgpu_internal.cuh): state, consumed-byte count and unit
-    // position of every sub-range, recorded as the chunk decodes forward
-    uint32_t pos_prev = 0;
-    uint64_t j_prev = ~0ull;
+    // side index (nzgpu_internal.cuh): state, unit position and offset of
+    // every sub-range, recorded as the chunk decodes forward
+    const uint64_t j0 = base >> log2k;  // the chunk's first sub-range
     for (uint32_t i = 0; i < nsym; ++i) {
         if (ck_state && ((base + i) & kmask) == 0) {
-            const uint64_t j = (base + i) >> log2k;
+            const uint64_t j = (base + i) >> log2k, u = j >> 5;
             ck_state[j] = x;
-            if (j_prev != ~0ull) ck_cnt[j_prev] = (uint8_t)(pos - pos_prev);
-            if ((j & 31) == 0) ck_base[j >> 5] = pos;
-            j_prev = j;
-            pos_prev = pos;
+            if ((j & 31) == 0) ck_base[u] = pos;
+            const bool anchored = (u << 5) >= j0;
+            ck_off[j] = (uint16_t)(pos - (anchored ? ck_base[u] : 0u));
         }
         const uint32_t slot = x & (kProbScale - 1);
         const uint32_t v = lut[slot];
@@ -66,10 +64,7 @@ __global__ void __launch_bounds__(128) seq_decode_kernel(const uint8_t* __restri
         if (exps) exps[base + i] = (uint8_t)(v & 0xFFu);
     }
     if (x != kStateLow || pos != limit) atomicOr(err, kErrDesync);  // ans.hpp:252-254
-    if (ck_state && j_prev != ~0ull) {
-        if (pos - pos_prev > 255u) atomicOr(err, kErrLength);  // only K > 128 can overflow a count byte
-        ck_cnt[j_prev] = (uint8_t)(pos - pos_prev);
-    }
+
 }
 
 // Merge of a global exponent plane with the mantissa plane (irregular-

@@ -75,26 +75,6 @@ __device__ __forceinline__ void tile_window(const DecodeDesc& d, uint32_t sub0, 
     if (b < a) b = a;
 }
 
-// Positions of the 32 sub-ranges of a warp unit (warp-collective: every lane
-// calls it).  `cnt` = this lane's consumed-byte count, `base` = the unit's
-// position record, `head` = this lane starts a chunk (its position is 0).
-// Returns this lane's start position relative to its chunk's payload start:
-// base (or 0 after a chunk head) plus the counts of the earlier lanes of the
-// same chunk segment.
-__device__ __forceinline__ uint32_t unit_lane_start(uint32_t cnt, uint32_t base, bool head, uint32_t lane) {
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-    }
-    const uint32_t excl = incl - cnt;
-    const uint32_t heads = __ballot_sync(0xFFFFFFFFu, head) & (0xFFFFFFFFu >> (31 - lane));  // heads at or below me
-    const int h = heads ? 31 - __clz(heads) : 0;
-    const uint32_t at_head = __shfl_sync(0xFFFFFFFFu, excl, h);
-    return heads ? excl - at_head : base + excl;
-}
-
 // bitwise c ? a : b in one LOP3
 __device__ __forceinline__ uint32_t bitsel(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;

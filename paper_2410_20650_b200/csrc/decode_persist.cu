@@ -249,11 +249,14 @@ struct LaneJob {
 
 // Raw index records of a lane's sub-range, loaded one unit ahead so the
 // global-memory latency never sits on a warp's critical path: the chunk
-// record, the lane's state and the next sub-range's (its end state), its
-// consumed-byte count and the unit's position record (a broadcast load).
+// record, the lane's state and the next sub-range's (its end state), and its
+// chunk-relative start / end positions (nzgpu_internal.cuh: the offset plus
+// the unit position for anchored lanes; the end is the next sub-range's
+// start, for lane 31 the next unit's position).  The last sub-range of a
+// chunk ends at len - 4 instead (lane_job).
 struct RawRec {
     uint4 ci;
-    uint32_t st, st1, cnt, base;
+    uint32_t st, st1, start, end;
 };
 
 template <int LOG2K>
@@ -264,26 +267,26 @@ __device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint
     sub_to_chunk(d, LOG2K, j, ch, jin);
     r.ci = d.chunk_info[ch];
     if (d.ck_state) {  // null for single-symbol tables (no index)
+        const uint32_t lane = j & 31u;
+        const uint32_t ref = jin >= lane ? d.ck_base[j >> 5] : 0u;  // anchored lanes add the unit position
         r.st = d.ck_state[j];
-        if (j + 1 < nsub) r.st1 = d.ck_state[j + 1];
-        r.cnt = d.ck_cnt[j];
-        r.base = d.ck_base[j >> 5];
+        r.start = d.ck_off[j] + ref;
+        if (j + 1 < nsub) {
+            r.st1 = d.ck_state[j + 1];
+            r.end = d.ck_off[j + 1] + (lane == 31u ? d.ck_base[(j >> 5) + 1] : ref);
+        }
     }
     return r;
 }
 
-// Warp-collective (every lane calls it, also lanes past the tensor's end).
 template <int LOG2K>
 __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uint32_t nsub, bool single,
-                                            const RawRec& raw, uint32_t lo0, uint32_t lane) {
+                                            const RawRec& raw, uint32_t lo0) {
     constexpr int K = 1 << LOG2K;
     LaneJob L{kStateLow, kStateLow, 0u, 0u, 0u, 0u};
-    const bool valid = j < nsub;
-    uint32_t ch = 0, jin = 0;
-    if (valid) sub_to_chunk(d, LOG2K, j, ch, jin);
-    // chunk-relative start of this lane (single-symbol tables read no bytes)
-    const uint32_t start = single ? 0u : unit_lane_start(valid ? raw.cnt : 0u, raw.base, valid && jin == 0, lane);
-    if (!valid) return L;
+    if (j >= nsub) return L;
+    uint32_t ch, jin;
+    sub_to_chunk(d, LOG2K, j, ch, jin);
     const uint4 ci = raw.ci;
     const uint64_t off = chunk_offset(ci);
     const uint32_t len = ci.z, nsym = ci.w;
@@ -309,9 +312,9 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
     const bool last = sym_in + K >= nsym;
     if (jin != 0) L.x0 = raw.st;
     L.xe = last ? kStateLow : raw.st1;
-    const uint32_t end = start + raw.cnt;
-    if (start > limit || end > limit || (last && end != limit)) L.err |= kErrDesync;
-    L.p0 = ci.x - lo0 + min(start, limit);  // chunk offsets of one unit differ by < 2^32
+    const uint32_t end = last ? limit : raw.end;
+    if (raw.start > limit || end > limit) L.err |= kErrDesync;
+    L.p0 = ci.x - lo0 + min(raw.start, limit);  // chunk offsets of one unit differ by < 2^32
     L.pe = ci.x - lo0 + min(end, limit);
     return L;
 }
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     // whose 64-bit offset only lane 0 needs, for the TMA source).
     auto stage = [&](uint32_t u, int b, uint32_t& wa_out, const RawRec& raw) -> LaneJob {
         const uint32_t lo0 = __shfl_sync(0xFFFFFFFFu, raw.ci.x, 0);
-        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw, lo0, lane);
+        LaneJob L = lane_job<LOG2K>(d, u * 32 + lane, nsub, single, raw, lo0);
         const uint32_t a = __shfl_sync(0xFFFFFFFFu, L.p0, 0);
         const uint32_t last_lane = min(31u, nsub - u * 32 - 1);
         const uint32_t e = __shfl_sync(0xFFFFFFFFu, L.pe, last_lane);

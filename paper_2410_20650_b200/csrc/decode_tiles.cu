@@ -236,19 +236,10 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
         cnt[c] = 0;
         x[c] = xe[c] = kStateLow;
         p[c] = pe[c] = sbase + kWinOff;
-        // every warp holds one 32-sub-range unit (sub0 and c*T are multiples
-        // of 32): lane positions from one warp scan of the count records
         const uint32_t j = sub0 + r;
         const bool valid = r < tile_subs;
-        uint32_t ch = 0, jin = 0, cb = 0, base = 0;
-        if (valid) {
-            sub_to_chunk(d, LOG2K, j, ch, jin);
-            if (!single) {
-                cb = d.ck_cnt[j];
-                base = d.ck_base[j >> 5];
-            }
-        }
-        const uint32_t start = single ? 0u : unit_lane_start(cb, base, valid && jin == 0, tid & 31u);
+        uint32_t ch = 0, jin = 0;
+        if (valid) sub_to_chunk(d, LOG2K, j, ch, jin);
         if (valid) {
             const uint4 ci = d.chunk_info[ch];
             const uint64_t off = chunk_offset(ci);
@@ -271,14 +262,18 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
                 if (jin == 0 && len >= 4 && (x[c] != kStateLow || len != 4))
                     errs |= x[c] < kStateLow ? kErrTruncated : kErrDesync;
             } else {
+                // positions as in decode_persist.cu lane_job (nzgpu_internal.cuh)
+                const uint32_t lane = j & 31u;
+                const uint32_t ref = jin >= lane ? d.ck_base[j >> 5] : 0u;
+                const uint32_t start = d.ck_off[j] + ref;
                 const bool last = sym_in + K >= nsym;
                 if (jin != 0) x[c] = d.ck_state[j];
                 xe[c] = last ? kStateLow : d.ck_state[j + 1];
-                const uint32_t end = start + cb;
+                const uint32_t end =
+                    last ? limit : d.ck_off[j + 1] + (lane == 31u ? d.ck_base[(j >> 5) + 1] : ref);
                 const int64_t p0 = (int64_t)(off + min(start, limit)) - (int64_t)wa;
                 const int64_t p1 = (int64_t)(off + min(end, limit)) - (int64_t)wa;
-                if (start > limit || end > limit || (last && end != limit) || p0 < 0 || p1 > (int64_t)win_cap ||
-                    p1 < p0)
+                if (start > limit || end > limit || p0 < 0 || p1 > (int64_t)win_cap || p1 < p0)
                     errs |= kErrDesync;
                 else {
                     p[c] = sbase + kWinOff + (uint32_t)p0;

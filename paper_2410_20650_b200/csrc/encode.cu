@@ -13,10 +13,11 @@
 // payload (ans.hpp:222-223) is then contiguous and in decoder order.
 // Every K symbols the encoder also records the side index that lets the
 // decoder split a chunk into independent sub-ranges (nzgpu_internal.cuh):
-// the state, the bytes the sub-range consumes (emitted since the previous
-// checkpoint, which in reverse order is the NEXT sub-range), and for every
-// 32nd sub-range its decoder position -- known only once the chunk is done
-// (len - 4 - bytes emitted from there on), so it is fixed up at the end.
+// the state, and the decoder byte positions -- known only once the chunk is
+// done, so the backward pass records each sub-range's consumed bytes (emitted
+// since the previous checkpoint, which in reverse order is the NEXT
+// sub-range) and a forward pass over the chunk's sub-ranges turns them into
+// unit positions and offsets at the end.
 //
 // K4 restates serialize_stream (ans.hpp:306-316): an exclusive scan of
 // (8 + len) over chunks, then a copy of every payload behind its header.
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     const uint32_t chunk_syms = t.chunk_syms, log2_interval = t.log2k;
     uint32_t* const ck_state = t.ck_state;
     uint32_t* const ck_base = t.ck_base;
-    uint8_t* const ck_cnt = t.ck_cnt;
+    uint16_t* const ck_off = t.ck_off;
     uint32_t e_prev = 0;  // bytes emitted at the previous (later) checkpoint
     const uint64_t nchunks = ceil_div(n, chunk_syms);
     const uint64_t c = (blockIdx.x - t.cta0) * (uint64_t)blockDim.x + threadIdx.x;
@@ -103,9 +104,8 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
         if (may_ckpt && ck_state && (i & kmask) == 0) {
             const uint64_t j = (begin + i) >> log2_interval;
             ck_state[j] = x;
-            ck_cnt[j] = (uint8_t)(emitted - e_prev);  // <= 1.5K + 2 < 256 for K <= 128
+            ck_off[j] = (uint16_t)(emitted - e_prev);  // consumed bytes, <= 1.5K + 2; positions below
             e_prev = emitted;
-            if ((j & 31) == 0) ck_base[j >> 5] = emitted;  // fixed up below
         }
     };
     uint32_t i = len;
@@ -146,9 +146,17 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     // the payload start, inside the slot.
     if (QUEUE && qc) *--wo = __byte_perm(qhi, 0, 0x0123) << (32 - 8 * qc);
     if (ck_state) {
-        // unit bases of this chunk: position = (len - 4) - bytes emitted after it
+        // forward over the chunk's sub-ranges: byte counts -> positions
         const uint64_t j0 = begin >> log2_interval, j1 = (begin + len - 1) >> log2_interval;
-        for (uint64_t u = (j0 + 31) >> 5; (u << 5) <= j1; ++u) ck_base[u] = emitted - ck_base[u];
+        uint32_t pos = 0;
+        for (uint64_t j = j0; j <= j1; ++j) {
+            const uint32_t c = ck_off[j];
+            const uint64_t u = j >> 5;
+            if ((j & 31) == 0) ck_base[u] = pos;
+            const bool anchored = (u << 5) >= j0;  // the unit's first sub-range is in this chunk
+            ck_off[j] = (uint16_t)(pos - (anchored ? ck_base[u] : 0u));
+            pos += c;
+        }
     }
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;

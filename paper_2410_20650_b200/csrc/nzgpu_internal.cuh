@@ -10,16 +10,17 @@
 // warp unit u of 32 consecutive sub-ranges:
 //   st[j]   u32  decoder state before symbol jK (= the encoder state after
 //                encoding it);
-//   cnt[j]  u8   renormalisation bytes sub-range j consumes (<= 1.5K + 2, so
-//                a byte for K <= 128);
 //   base[u] u32  decoder byte position (from its chunk's payload start) of
-//                sub-range 32u.
-// A lane's position is its chunk's payload start plus base (or 0 for the
-// first sub-range of a chunk) plus the counts of the lanes before it in the
-// same chunk: one warp prefix scan.  A sub-range must end on the next
-// sub-range's state and position; the last one of a chunk on (2^23, len-4),
-// the reference's end-of-chunk check (ans.hpp:252).  5 bytes per K symbols +
-// 4 per 32K: 0.080 B/element at K = 64, 0.041 at K = 128.
+//                sub-range 32u;
+//   off[j]  u16  decoder byte position of sub-range j relative to base[u]
+//                when sub-range 32u lies in j's chunk ("anchored"), else
+//                relative to j's chunk start (a unit that straddles chunks).
+// So a lane's position is one load and one add -- no warp scan -- and its end
+// position is the next sub-range's (off[j+1], or base[u+1] for lane 31).
+// Offsets stay below 31 * (1.5K + 2) < 2^16.  A sub-range must end on the
+// next sub-range's state and position; the last one of a chunk on
+// (2^23, len-4), the reference's end-of-chunk check (ans.hpp:252).  6 bytes
+// per K symbols + 4 per 32K: 0.096 B/element at K = 64, 0.048 at K = 128.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -77,7 +78,7 @@ struct EncTask {
     uint32_t* plen;          // payload length per chunk
     uint32_t* ck_state;      // side index (st[], cnt[], base[]), or nullptr
     uint32_t* ck_base;
-    uint8_t* ck_cnt;
+    uint16_t* ck_off;
     uint32_t* err;           // sticky error word
     uint4* chunk_info;       // K4 out: {off lo, off hi, len, nsym}
     uint8_t* hdr;            // K4 out: the stream's leading u32 chunk count
@@ -106,7 +107,7 @@ struct DecodeDesc {
     const uint8_t* scales;        // lossy block scale bytes
     const uint32_t* ck_state;     // side index: state per sub-range
     const uint32_t* ck_base;      //   position of sub-range 32u in its chunk
-    const uint8_t* ck_cnt;        //   renormalisation bytes per sub-range
+    const uint16_t* ck_off;       //   sub-range position within the unit / chunk
     const uint4* chunk_info;      // {payload offset lo, hi, len, nsym} per chunk
     const uint32_t* lut;          // 4096 packed decode entries
     uint16_t* out;                // bf16 output, 16-B aligned

@@ -1,6 +1,17 @@
-"""GPU: the `neuzip` CLI (proj/tools/neuzip.cpp analyze / compress /
-decompress / bench) built on the drop-in headers: same CSV output, same files,
-same exit codes (2 usage/format, 3 NaN/Inf, 4 checksum)."""
+"""GPU: the `neuzip` CLI (tools/neuzip_cli.cpp) against text and files the
+REFERENCE codec produces (oracle/_ref: the unmodified reference headers;
+the C restatement where it is not built) -- not against this repo's own API.
+
+Pinned per subcommand of proj/tools/neuzip.cpp:
+  analyze     CSV = the reference's analyze_tensor doubles (entropy.hpp:89-94)
+              formatted %.6g, histogram bins = numpy counts (neuzip.cpp:40-65);
+  compress    the .nzt file is byte-identical to the reference's write_nzt,
+              and the footprint CSV is the reference blob's section sizes
+              (tensorstore.hpp:242-287, neuzip.cpp:67-96);
+  decompress  lossless: the original .bft back; lossy: the reference's
+              decompress_lossy values (neuzip.cpp:98-115);
+  exit codes  2 usage / FormatError, 3 NonFiniteError, 4 ChecksumError
+              (neuzip.cpp:324-339)."""
 import os
 import struct
 import subprocess
@@ -23,6 +34,13 @@ def nz():
     return nz
 
 
+@pytest.fixture(scope="module")
+def refc():
+    from oracle.oracle import Oracle, ref_available
+
+    return Oracle("ref") if ref_available() else Oracle("port")
+
+
 def bft(values, shape):
     return b"BFT1" + struct.pack("<B", len(shape)) + b"".join(struct.pack("<Q", d) for d in shape) + \
         np.ascontiguousarray(values, "<u2").tobytes()
@@ -32,61 +50,99 @@ def run(*args):
     return subprocess.run([CLI, *args], capture_output=True, text=True)
 
 
-def fmt6(x):
+def g6(x):
     return "%.6g" % x
 
 
-def test_gpu_cli_compress_decompress_analyze(nz, port, tmp_path):
+def footprint_lines(n, stream_len, mant_len, scales_len, ndim):
+    header = 35 + 8 * ndim
+    total = stream_len + mant_len + scales_len + 512 + header
+    return ["section,bytes", f"exponent,{stream_len}", f"mantissa,{mant_len}", f"scales,{scales_len}", "table,512",
+            f"header,{header}", f"total,{total}", f"raw,{2 * n}", f"ratio,{g6(2 * n / total)}"]
+
+
+def test_gpu_cli_lossless_against_reference(nz, port, refc, tmp_path):
+    shape = (300, 1000)
     v = port.gaussian_bf16(5, 300 * 1000, 0.02)
     src = tmp_path / "w.bft"
-    src.write_bytes(bft(v, (300, 1000)))
+    src.write_bytes(bft(v, shape))
     out = tmp_path / "w.nzt"
     r = run("compress", str(src), str(out))
     assert r.returncode == 0, r.stderr
-    blob = nz.compress_lossless(v, nz.TensorMeta((300, 1000)))
-    assert out.read_bytes() == nz.write_nzt(blob)
-    fp = nz.footprint(blob)
-    lines = r.stdout.splitlines()
-    assert lines[0] == "section,bytes" and f"total,{fp.total()}" in lines and f"raw,{2 * v.size}" in lines
-    assert f"ratio,{fmt6(2 * v.size / fp.total())}" in lines
+    assert out.read_bytes() == refc.write_nzt_lossless(v, shape)
+    f, s, m = refc.compress_lossless(v)
+    assert r.stdout.splitlines() == footprint_lines(v.size, len(s), m.size, 0, 2)
     back = tmp_path / "back.bft"
     r = run("decompress", str(out), str(back))
     assert r.returncode == 0, r.stderr
     assert back.read_bytes() == src.read_bytes()
+
+
+def test_gpu_cli_analyze_against_reference(nz, refc, port, tmp_path):
+    v = port.gaussian_bf16(9, 65536 * 3 + 11, 0.05)
+    src = tmp_path / "a.bft"
+    src.write_bytes(bft(v, (v.size,)))
     r = run("analyze", str(src), "--hist")
     assert r.returncode == 0, r.stderr
-    rep = nz.analyze_tensor(v)
-    lines = r.stdout.splitlines()
-    assert lines[:6] == ["component,entropy_bits,capacity_bits", f"sign,{fmt6(rep.h_sign)},1",
-                         f"exponent,{fmt6(rep.h_exp)},8", f"mantissa,{fmt6(rep.h_mant)},7",
-                         f"ideal_ratio,{fmt6(rep.ideal_ratio)},", f"exponent_only_ratio,{fmt6(rep.exponent_only_ratio)},"]
-    assert len(lines) == 6 + 2 + 256 + 128
+    hs, he, hm, ideal, exp_only = refc.entropy_report(v)
+    want = ["component,entropy_bits,capacity_bits", f"sign,{g6(hs)},1", f"exponent,{g6(he)},8",
+            f"mantissa,{g6(hm)},7", f"ideal_ratio,{g6(ideal)},", f"exponent_only_ratio,{g6(exp_only)},"]
+    sign = np.bincount(v >> 15, minlength=2)
+    exp = np.bincount((v >> 7) & 0xFF, minlength=256)
+    mant = np.bincount(v & 0x7F, minlength=128)
+    want += [f"hist_sign_{i},{c}," for i, c in enumerate(sign)]
+    want += [f"hist_exp_{i},{c}," for i, c in enumerate(exp)]
+    want += [f"hist_mant_{i},{c}," for i, c in enumerate(mant)]
+    assert r.stdout.splitlines() == want
 
 
-def test_gpu_cli_lossy_and_exit_codes(nz, port, tmp_path):
-    v = port.gaussian_bf16(6, 70000, 0.02)
+@pytest.mark.parametrize("k,block", [(3, 64), (0, 512), (1, 100)])
+def test_gpu_cli_lossy_against_reference(nz, port, refc, tmp_path, k, block):
+    v = port.gaussian_bf16(6 + k, 70000, 0.02)
     src = tmp_path / "w.bft"
     src.write_bytes(bft(v, (70000,)))
     out = tmp_path / "w.nzt"
-    assert run("compress", str(src), str(out), "-p", "3", "--block-size", "64").returncode == 0
-    blob = nz.compress_lossy(v, 3, 64)
-    assert out.read_bytes() == nz.write_nzt(blob)
+    r = run("compress", str(src), str(out), "-p", str(k), "--block-size", str(block))
+    assert r.returncode == 0, r.stderr
+    assert out.read_bytes() == refc.write_nzt_lossy(v, (70000,), k, block)
+    f, sc, s, pk = refc.compress_lossy(v, k, block)
+    assert r.stdout.splitlines() == footprint_lines(v.size, len(s), pk.size, sc.size, 1)
     back = tmp_path / "back.bft"
     assert run("decompress", str(out), str(back)).returncode == 0
-    got = np.frombuffer(back.read_bytes()[13 + 8 * 0:], "<u2")[-v.size:]
-    assert (got == nz.decompress_lossy(blob)).all()
-    bad = bytearray(out.read_bytes())
+    got = np.frombuffer(back.read_bytes()[5 + 8:], "<u2")
+    assert (got == refc.decompress_lossy(f, sc, s, pk, k, block, v.size)).all()
+
+
+def test_gpu_cli_exit_codes(nz, port, refc, tmp_path):
+    v = port.gaussian_bf16(6, 70000, 0.02)
+    src = tmp_path / "w.bft"
+    src.write_bytes(bft(v, (70000,)))
+    good = refc.write_nzt_lossy(v, (70000,), 3, 64)  # a file the REFERENCE wrote
+    back = tmp_path / "back.bft"
+    (tmp_path / "good.nzt").write_bytes(good)
+    assert run("decompress", str(tmp_path / "good.nzt"), str(back)).returncode == 0
+    bad = bytearray(good)
     bad[len(bad) // 2] ^= 1
     (tmp_path / "bad.nzt").write_bytes(bytes(bad))
     assert run("decompress", str(tmp_path / "bad.nzt"), str(back)).returncode == 4  # ChecksumError
     (tmp_path / "magic.nzt").write_bytes(b"NZT9" + bytes(bad[4:]))
     assert run("decompress", str(tmp_path / "magic.nzt"), str(back)).returncode == 2  # FormatError
+    (tmp_path / "short.nzt").write_bytes(good[:100])
+    assert run("decompress", str(tmp_path / "short.nzt"), str(back)).returncode == 2
     nan = v.copy()
     nan[7] = 0x7FC0
     (tmp_path / "nan.bft").write_bytes(bft(nan, (70000,)))
+    out = tmp_path / "o.nzt"
     assert run("compress", str(tmp_path / "nan.bft"), str(out), "-p", "0").returncode == 3  # NonFiniteError
-    assert run("compress", str(src), str(out), "-p", "2").returncode == 2  # usage
+    assert run("compress", str(src), str(out), "-p", "2").returncode == 2  # not in {0,1,3,7}
+    assert run("compress", str(src), str(out), "--block-size", "0", "-p", "3").returncode == 2
+    assert run("compress", str(src)).returncode == 2
+    (tmp_path / "trunc.bft").write_bytes(bft(v, (70001,)))
+    assert run("compress", str(tmp_path / "trunc.bft"), str(out)).returncode == 2
     assert run("frobnicate").returncode == 2
+    assert run("analyze", str(src), "--bogus").returncode == 2
+    assert run("train-demo").returncode == 2
+    assert run("--help").returncode == 0
 
 
 def test_gpu_cli_bench(nz):
@@ -94,4 +150,8 @@ def test_gpu_cli_bench(nz):
     assert r.returncode == 0, r.stderr
     lines = r.stdout.splitlines()
     assert lines[0] == "direction,size_bytes,gib_per_s" and len(lines) == 5
+    assert [l.split(",")[:2] for l in lines[1:]] == [["compress", "100000"], ["decompress", "100000"],
+                                                       ["compress", "1000000"], ["decompress", "1000000"]]
     assert all(float(l.split(",")[2]) > 0 for l in lines[1:])
+    assert run("bench", "--sizes", "100").returncode == 2
+    assert run("bench", "--trials", "0").returncode == 2

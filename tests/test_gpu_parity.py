@@ -61,21 +61,21 @@ def test_gpu_checkpoint_intervals(nz, port, interval):
     f, s, sm = port.compress_lossless(v)
     assert blob.stream == s and (blob.signmant == sm).all()
     assert (nz.decompress_lossless(blob) == v).all()
-    # compact side index: 56-byte header + 5 bytes per sub-range + 4 per unit
+    # compact side index: 56-byte header + 6 bytes per sub-range + 4 per unit
     nsub = -(-v.size // interval)
-    assert len(blob.index) == 56 + 5 * nsub + 4 * (-(-nsub // 32))
-    assert len(blob.index) / v.size < (0.0802 if interval == 64 else 0.0412)
+    assert len(blob.index) == 56 + 6 * nsub + 4 * (-(-nsub // 32))
+    assert (len(blob.index) - 56) / v.size < (0.0959 if interval == 64 else 0.0480)
 
 
 def test_gpu_interval_256_rejected(nz, port):
-    """A sub-range's renormalisation byte count is one index byte, which
-    bounds K at 128 (<= 1.5 K + 2 bytes per sub-range)."""
+    """The decoder's checkpoint strides are 64 and 128 symbols (a unit of
+    32 sub-ranges then spans <= 31 * (1.5 K + 2) bytes: 16-bit offsets)."""
     v = port.gaussian_bf16(123, 70001, 0.02)
     with pytest.raises(ValueError):
         nz.compress_lossless(v, interval=256)
 
 
-@pytest.mark.parametrize("what", ["state", "count", "base"])
+@pytest.mark.parametrize("what", ["state", "offset", "base"])
 def test_gpu_corrupt_index_is_a_format_error(nz, port, what):
     """A damaged side index (not part of the reference format) must surface
     as the reference's FormatError -- every sub-range has to land exactly on
@@ -89,8 +89,8 @@ def test_gpu_corrupt_index_is_a_format_error(nz, port, what):
     if what == "state":
         off = 56 + 4 * j
         ix[off] ^= 0x40
-    elif what == "count":
-        off = 56 + 4 * nsub + 4 * units + j
+    elif what == "offset":
+        off = 56 + 4 * nsub + 4 * units + 2 * j
         ix[off] = (ix[off] + 3) & 0xFF
     else:
         off = 56 + 4 * nsub + 4 * (j // 32)

@@ -44,7 +44,7 @@ def main():
     for kern, name in ((0, "persist"), (1, "tiles")):
         t = np.array(res[kern])
         print(f"{name:8s} n={n} prec={prec} K={K} median={np.median(t)*1e6:.1f}us min={t.min()*1e6:.1f}us "
-              f"GB/s(med)={algo/np.median(t)/1e9:.1f} frac={algo/np.median(t)/6536.4e9:.3f}", flush=True)
+              f"GB/s(med)={algo/np.median(t)/1e9:.1f} frac={algo/np.median(t)/6545.6e9:.3f}", flush=True)
 
 
 main()

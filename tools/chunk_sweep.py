@@ -23,12 +23,18 @@ import torch
 import paper_2410_20650_b200 as nz
 from tests import inputs
 
-PEAK = 6536.4
+PEAK = 6545.6  # MEASURED_PEAKS.json hbm_gbs
 
 
 def tensors(n):
-    g = torch.Generator(device="cuda").manual_seed(42)
-    gauss = (torch.randn(n, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    # Gaussian: rng::gaussian_bf16(42, n, 0.02) (rng.hpp:73-81) -- the
+    # reference's own generator (its C restatement, oracle/, used here only
+    # to produce the input weights), so the ratios can be checked against the
+    # survey's probe P10 (1.51646 -> 1.51666 over S).
+    from oracle.oracle import Oracle
+
+    g = Oracle("port").gaussian_bf16_parallel(42, n, 0.02)
+    gauss = torch.from_numpy(g.view(np.int16)).cuda().view(torch.bfloat16)
     uni = torch.from_numpy(inputs.bf16_uniform(n, 7, math.sqrt(3.0) * 0.02).view(np.int16)).cuda()
     lap = torch.from_numpy(inputs.bf16_laplace(n, 11, 0.02 / math.sqrt(2.0)).view(np.int16)).cuda()
     return {"gaussian": gauss, "uniform": uni.view(torch.bfloat16), "laplace": lap.view(torch.bfloat16)}

@@ -17,7 +17,7 @@ import torch
 import paper_2410_20650_b200 as nz
 from paper_2410_20650_b200 import nzgpu as N
 
-PEAK = 6536.4
+PEAK = 6545.6  # MEASURED_PEAKS.json hbm_gbs
 
 
 def dev_crc(t, n):

@@ -34,7 +34,7 @@ def main():
             info = blob.info
             algo = info.payload_bytes + 2 * n
             print(f"prec={prec} K={K} n={n} compress={tc*1e3:.1f}ms decode={t*1e6:.1f}us "
-                  f"algoGB/s={algo/t/1e9:.1f} frac={algo/t/6536.4e9:.3f} bf16GB/s={2*n/t/1e9:.1f} "
+                  f"algoGB/s={algo/t/1e9:.1f} frac={algo/t/6545.6e9:.3f} bf16GB/s={2*n/t/1e9:.1f} "
                   f"ratio={2*n/(info.payload_bytes+35+8):.4f} win={info.max_window}", flush=True)
             plan.free(); blob.free()
 
