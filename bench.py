@@ -439,6 +439,8 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if rank == 0:
+        if args.dropin and args.model == "8b" and args.precision == 7:
+            line["e2e_dropin"] = run_dropin_bench()
         line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if dist:
@@ -589,6 +591,25 @@ def run_e2e(args, nz, blobs, torch, dist=None):
             f"buffers), all ranks concurrently: sum of bytes / max time"}
 
 
+def run_dropin_bench():
+    """The reference-signature C++ API (include/neuzip/tensorstore.hpp) on
+    one Llama-3-8B layer, host vectors in and out (tools/dropin_bench.cpp):
+    `fresh` = std::vector<Bf16> decompress_lossless(blob) as the reference
+    declares it (a new value-initialised vector per call); `reused` =
+    decompress_lossless_into(blob, vec) into vectors kept across calls."""
+    exe = os.path.join(ROOT, "paper_2410_20650_b200", "dropin_bench")
+    try:
+        out = subprocess.run([exe, "3"], capture_output=True, text=True, timeout=600)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"value": d["fresh_gbs"], "unit": "GB/s", "reused": d["reused_gbs"], "ok": d["ok"],
+                "sample": "Llama-3-8B layer projections q,k,v,o,gate,up,down ("
+                          f"{d['elements']} elements), C++ drop-in decompress_lossless per tensor, median of "
+                          f"{d['reps']}; value = fresh std::vector per call (the reference signature), reused = "
+                          "decompress_lossless_into a kept vector"}
+    except Exception as e:  # reported, never required
+        return {"value": None, "unit": "GB/s", "error": repr(e)[:200]}
+
+
 # ------------------------------------------------------ CPU reference arm ---
 def cpu_sample(args):
     """Bounded sample of the workload for the CPU: the first layer's tensors
@@ -722,6 +743,7 @@ def main():
     ap.add_argument("--interval", type=int, default=0, help="checkpoint stride K (0 = auto)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--e2e-layers", type=int, default=4)
+    ap.add_argument("--dropin", type=int, default=1, help="also time the C++ drop-in host API (rank 0, 8B lossless)")
     ap.add_argument("--cpu-tensors", type=int, default=7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verify", type=int, default=1,

@@ -111,19 +111,26 @@ inline FrequencyTable table_from(const std::vector<std::uint16_t>& f) {
     return FrequencyTable::from_frequencies(a);
 }
 
-inline std::vector<Bf16> gpu_decompress(const TensorMeta& meta, const AnsStream& stream,
-                                        const std::vector<std::uint8_t>& mant, int precision, std::uint32_t block,
-                                        const std::vector<std::uint8_t>* scales,
-                                        const std::vector<std::uint8_t>& index) {
-    const std::vector<std::uint8_t> bytes = serialize_stream(stream);
-    const std::uint64_t n = meta.element_count();
-    nzgpu_host_tensor t{};
-    t.n = n;
+// Decode through nzgpu_decompress_host_sections: the AnsStream's chunk
+// payloads are gathered straight into pinned staging (no serialize_stream
+// copy), and the bf16 result is copied out of a pinned D2H ring by worker
+// threads into `out` (n values).
+inline void gpu_decompress_into(const TensorMeta& meta, const AnsStream& stream, const std::vector<std::uint8_t>& mant,
+                                int precision, std::uint32_t block, const std::vector<std::uint8_t>* scales,
+                                const std::vector<std::uint8_t>& index, Bf16* out) {
+    std::vector<nzgpu_chunk_view> views(stream.chunks.size());
+    for (std::size_t c = 0; c < views.size(); ++c) {
+        const AnsChunk& ch = stream.chunks[c];
+        if (ch.payload.size() > 0xFFFFFFFFull) throw FormatError("ans stream: chunk payload too large");
+        views[c] = nzgpu_chunk_view{ch.payload.data(), static_cast<std::uint32_t>(ch.payload.size()), ch.symbol_count};
+    }
+    nzgpu_host_sections t{};
+    t.n = meta.element_count();
     t.precision = precision;
     t.block_size = block;
     t.freqs = stream.table.frequencies().data();
-    t.stream = bytes.data();
-    t.stream_len = bytes.size();
+    t.chunks = views.data();
+    t.nchunks = views.size();
     t.mantissas = mant.data();
     t.mantissa_len = mant.size();
     if (scales) {
@@ -132,8 +139,18 @@ inline std::vector<Bf16> gpu_decompress(const TensorMeta& meta, const AnsStream&
     }
     t.index = index.empty() ? nullptr : index.data();
     t.index_len = index.size();
-    std::vector<Bf16> out(n);
-    check(nzgpu_decompress_host(&t, reinterpret_cast<std::uint16_t*>(out.data())), "decompress");
+    check(nzgpu_decompress_host_sections(&t, reinterpret_cast<std::uint16_t*>(out)), "decompress");
+}
+
+inline std::vector<Bf16> gpu_decompress(const TensorMeta& meta, const AnsStream& stream,
+                                        const std::vector<std::uint8_t>& mant, int precision, std::uint32_t block,
+                                        const std::vector<std::uint8_t>* scales,
+                                        const std::vector<std::uint8_t>& index) {
+    // A fresh vector is value-initialised (and its pages first touched) by
+    // one thread before the decode writes it: for large tensors that, not the
+    // GPU or PCIe, bounds this signature (the *_into overloads reuse memory).
+    std::vector<Bf16> out(meta.element_count());
+    gpu_decompress_into(meta, stream, mant, precision, block, scales, index, out.data());
     return out;
 }
 
@@ -161,6 +178,15 @@ inline LosslessBlob compress_lossless(std::span<const Bf16> values) {
 inline std::vector<Bf16> decompress_lossless(const LosslessBlob& blob) {
     return detail::gpu_decompress(blob.meta, blob.exp_stream, blob.signmant, kLosslessPrecision, 0, nullptr,
                                   blob.gpu_index);
+}
+
+// Extension (not in the reference API): decode into a caller-owned vector,
+// reusing its capacity -- no page faults when the buffer is recycled, so the
+// host path runs at PCIe rate.  `out` is resized to the element count.
+inline void decompress_lossless_into(const LosslessBlob& blob, std::vector<Bf16>& out) {
+    out.resize(blob.meta.element_count());
+    detail::gpu_decompress_into(blob.meta, blob.exp_stream, blob.signmant, kLosslessPrecision, 0, nullptr,
+                                blob.gpu_index, out.data());
 }
 
 namespace detail {
@@ -193,6 +219,13 @@ inline LossyBlob compress_lossy(std::span<const Bf16> values, int k, std::uint32
 inline std::vector<Bf16> decompress_lossy(const LossyBlob& blob) {
     return detail::gpu_decompress(blob.meta, blob.exp_stream, blob.signmant, blob.precision, blob.block_size,
                                   &blob.scales, blob.gpu_index);
+}
+
+// Extension: decompress_lossy into a caller-owned vector (see decompress_lossless_into).
+inline void decompress_lossy_into(const LossyBlob& blob, std::vector<Bf16>& out) {
+    out.resize(blob.meta.element_count());
+    detail::gpu_decompress_into(blob.meta, blob.exp_stream, blob.signmant, blob.precision, blob.block_size,
+                                &blob.scales, blob.gpu_index, out.data());
 }
 
 struct Footprint {  // tensorstore.hpp:242-253

@@ -181,6 +181,42 @@ int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint3
  * GPU decode, D2H of the bf16 result.  Staging buffers are cached by the
  * library; pinned host memory gives full PCIe bandwidth. */
 int nzgpu_decompress_host(const nzgpu_host_tensor* t, uint16_t* out);
+/* One chunk of an AnsStream as the reference holds it (AnsChunk,
+ * ans.hpp:159-168: its own payload vector), so callers need not serialize
+ * the stream first. */
+typedef struct nzgpu_chunk_view {
+    const uint8_t* payload;
+    uint32_t len;             /* payload bytes (renormalisation bytes + LE32 state) */
+    uint32_t nsym;            /* AnsChunk::symbol_count                          */
+} nzgpu_chunk_view;
+
+/* A host tensor with the exponent stream as chunk views (the drop-in
+ * LosslessBlob / LossyBlob layout); other fields as nzgpu_host_tensor. */
+typedef struct nzgpu_host_sections {
+    uint64_t n;
+    int32_t precision;
+    uint32_t block_size;
+    const uint16_t* freqs;
+    const nzgpu_chunk_view* chunks;
+    uint64_t nchunks;
+    const uint8_t* mantissas;
+    uint64_t mantissa_len;
+    const uint8_t* scales;
+    uint64_t scales_len;
+    const void* index;
+    uint64_t index_len;
+} nzgpu_host_sections;
+
+/* Decompress a host tensor given as sections into host memory `out`
+ * (pageable or pinned, n bf16): the chunk payloads, planes and index are
+ * gathered straight into pinned staging by host worker threads, sent H2D
+ * and decoded; the bf16 result comes back D2H in slices that worker threads
+ * copy into `out` while the next slice is in flight.  Staging is cached per
+ * calling thread (nzgpu_host_release frees it).  Tensors without a usable
+ * side index or with irregular framing take the general (validating) path.
+ * Same results and errors as nzgpu_decompress_host. */
+int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out);
+
 /* Decode a device blob into host memory (GPU decode on a private stream,
  * then D2H; pinned or pageable `out`, n bf16).  Synchronous. */
 int nzgpu_blob_decompress_host(nzgpu_blob blob, uint16_t* out);

@@ -69,27 +69,35 @@ def build(verbose: bool = False, defines=(), lib: str = LIB) -> str:
             raise RuntimeError(f"link failed:\n{out.stdout}\n{out.stderr}")
     if lib == LIB:
         build_cli()
+        build_tool(DROPIN_BENCH_SRC, DROPIN_BENCH)
     return lib
 
 
 CLI_SRC = os.path.join(HERE, "..", "tools", "neuzip_cli.cpp")
 CLI = os.path.join(HERE, "neuzip")
+DROPIN_BENCH_SRC = os.path.join(HERE, "..", "tools", "dropin_bench.cpp")
+DROPIN_BENCH = os.path.join(HERE, "dropin_bench")
+
+
+def build_tool(src: str, exe: str) -> str:
+    """A host tool on the drop-in headers, linked against the in-tree
+    libnzgpu.so (rpath $ORIGIN)."""
+    deps = [src, LIB, os.path.join(HERE, "..", "include", "nzgpu.h")] + [
+        os.path.join(HERE, "..", "include", "neuzip", f) for f in os.listdir(os.path.join(HERE, "..", "include", "neuzip"))]
+    if os.path.exists(exe) and all(os.path.getmtime(exe) >= os.path.getmtime(d) for d in deps):
+        return exe
+    cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-Wall", "-Wextra", "-I", os.path.join(HERE, "..", "include"),
+           src, "-o", exe, "-L", HERE, "-lnzgpu", "-Wl,-rpath,$ORIGIN"]
+    out = subprocess.run(cmd, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"{os.path.basename(exe)} build failed:\n{out.stdout}\n{out.stderr}")
+    return exe
 
 
 def build_cli() -> str:
     """The `neuzip` command-line tool (analyze / compress / decompress /
-    bench, proj/tools/neuzip.cpp) on the drop-in headers, linked against the
-    in-tree libnzgpu.so (rpath $ORIGIN)."""
-    deps = [CLI_SRC, LIB] + [os.path.join(HERE, "..", "include", "neuzip", f)
-                             for f in os.listdir(os.path.join(HERE, "..", "include", "neuzip"))]
-    if os.path.exists(CLI) and all(os.path.getmtime(CLI) >= os.path.getmtime(d) for d in deps):
-        return CLI
-    cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-Wall", "-Wextra", "-I", os.path.join(HERE, "..", "include"),
-           CLI_SRC, "-o", CLI, "-L", HERE, "-lnzgpu", "-Wl,-rpath,$ORIGIN"]
-    out = subprocess.run(cmd, capture_output=True, text=True)
-    if out.returncode != 0:
-        raise RuntimeError(f"neuzip CLI build failed:\n{out.stdout}\n{out.stderr}")
-    return CLI
+    bench, proj/tools/neuzip.cpp) on the C ABI and the drop-in headers."""
+    return build_tool(CLI_SRC, CLI)
 
 
 if __name__ == "__main__":

@@ -14,8 +14,11 @@
 #include <cstring>
 #include <string>
 #include <memory>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/nzgpu.h"
@@ -1274,8 +1277,134 @@ struct HostSlot {
 #endif
 constexpr int kHostSlots = NZ_HOST_SLOTS;
 
+// Grow-only pinned host buffer (cudaMallocHost costs ~0.4 ms per MB, so it
+// is kept per thread across calls).
+struct PinnedBuf {
+    void* p = nullptr;
+    uint64_t cap = 0;
+    int ensure(uint64_t bytes) {
+        if (cap >= bytes) return NZGPU_OK;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        const uint64_t want = align_up(std::max<uint64_t>(bytes + bytes / 4, 1 << 20), 1 << 20);
+        CK(cudaMallocHost(&p, want));
+        cap = want;
+        return NZGPU_OK;
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+// Host worker threads for the copies between pageable user memory and pinned
+// staging: one thread moves pinned -> pageable at ~14 GB/s and faults fresh
+// pages at ~2 GB/s; eight reach ~50-75 GB/s and ~20 GB/s (measured on the
+// B200 box, profiles/r02_hostpath.txt).  A process-wide pool; run() executes
+// f(0..parts-1) on the workers and the caller and returns when all are done.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool pool(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
+        return pool;
+    }
+    int threads() const { return (int)workers_.size() + 1; }
+    void run(int parts, const std::function<void(int)>& f) {
+        if (parts <= 1 || workers_.empty()) {
+            for (int i = 0; i < parts; ++i) f(i);
+            return;
+        }
+        std::lock_guard<std::mutex> one_region(run_mu_);  // callers from several threads queue here
+        std::unique_lock<std::mutex> lk(mu_);
+        job_ = &f;
+        parts_ = parts;
+        next_ = 0;
+        left_ = parts;
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        work();
+        lk.lock();
+        done_cv_.wait(lk, [&] { return left_ == 0; });
+        job_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (std::thread& t : workers_) t.join();
+    }
+
+private:
+    explicit HostPool(unsigned n) {
+        for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void work() {
+        for (;;) {
+            int i;
+            const std::function<void(int)>* f;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!job_ || next_ >= parts_) return;
+                i = next_++;
+                f = job_;
+            }
+            (*f)(i);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--left_ == 0) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, run_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* job_ = nullptr;
+    int parts_ = 0, next_ = 0, left_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// memcpy split over the host pool above ~4 MB.
+void par_memcpy(void* dst, const void* src, uint64_t bytes) {
+    constexpr uint64_t kPiece = 2ull << 20;
+    if (bytes < 2 * kPiece) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    HostPool& pool = HostPool::get();
+    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 4, ceil_div(bytes, kPiece));
+    const uint64_t step = align_up(ceil_div(bytes, (uint64_t)parts), 64);
+    pool.run(parts, [&](int i) {
+        const uint64_t a = (uint64_t)i * step;
+        if (a < bytes)
+            std::memcpy(static_cast<uint8_t*>(dst) + a, static_cast<const uint8_t*>(src) + a,
+                        std::min(step, bytes - a));
+    });
+}
+
 struct HostCtx {
     HostSlot slot[kHostSlots];
+    // nzgpu_decompress_host_sections: gathered inputs and the D2H ring
+    static constexpr int kOutRing = 3;
+    PinnedBuf in, ring[kOutRing];
+    cudaEvent_t ring_ev[kOutRing] = {};
+    ~HostCtx() {
+        for (cudaEvent_t& e : ring_ev)
+            if (e) cudaEventDestroy(e);
+    }
     int init() {
         for (HostSlot& sl : slot) {
             if (!sl.s) CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
@@ -1283,6 +1412,8 @@ struct HostCtx {
             for (auto& ev : sl.info_done)
                 if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         }
+        for (cudaEvent_t& e : ring_ev)
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         return NZGPU_OK;
     }
 };
@@ -1514,6 +1645,205 @@ int nzgpu_blob_decompress_host(nzgpu_blob b, uint16_t* out) {
     cudaFreeAsync(d, sg.s);
     const int st = sync_status(sg.s, b->err, true);
     return rc ? rc : st;
+}
+
+namespace {
+
+// Serialize chunk views (serialize_stream, ans.hpp:306-316) into `dst`,
+// chunk headers and payloads copied by the host pool; fills the chunk table.
+void gather_stream(const nzgpu_host_sections* t, uint8_t* dst, std::vector<uint4>& info) {
+    info.resize(t->nchunks);
+    uint64_t pos = 4;
+    for (uint64_t c = 0; c < t->nchunks; ++c) {
+        pos += 8;
+        info[c] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), t->chunks[c].len, t->chunks[c].nsym);
+        pos += t->chunks[c].len;
+    }
+    const uint32_t cnt = (uint32_t)t->nchunks;
+    std::memcpy(dst, &cnt, 4);
+    HostPool& pool = HostPool::get();
+    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 4, std::max<uint64_t>(1, t->nchunks / 16));
+    const uint64_t per = ceil_div(t->nchunks, (uint64_t)parts);
+    pool.run(parts, [&](int i) {
+        for (uint64_t c = i * per; c < std::min(t->nchunks, (i + 1) * per); ++c) {
+            const uint64_t at = ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32));
+            std::memcpy(dst + at - 8, &info[c].w, 4);
+            std::memcpy(dst + at - 4, &info[c].z, 4);
+            if (info[c].z) std::memcpy(dst + at, t->chunks[c].payload, info[c].z);
+        }
+    });
+}
+
+// General path of the sections call: serialize, then the validating host tier.
+int sections_general(const nzgpu_host_sections* t, uint16_t* out) {
+    uint64_t len = 4;
+    for (uint64_t c = 0; c < t->nchunks; ++c) len += 8 + (uint64_t)t->chunks[c].len;
+    std::vector<uint8_t> stream(len);
+    std::vector<uint4> info;
+    gather_stream(t, stream.data(), info);
+    nzgpu_host_tensor h{};
+    h.n = t->n;
+    h.precision = t->precision;
+    h.block_size = t->block_size;
+    h.freqs = t->freqs;
+    h.stream = stream.data();
+    h.stream_len = len;
+    h.mantissas = t->mantissas;
+    h.mantissa_len = t->mantissa_len;
+    h.scales = t->scales;
+    h.scales_len = t->scales_len;
+    h.index = t->index;
+    h.index_len = t->index_len;
+    return nzgpu_decompress_host_batch(&h, 1, &out);
+}
+
+}  // namespace
+
+int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) {
+    if (!t || !valid_precision(t->precision) || !t->freqs || (t->nchunks && !t->chunks) || (t->n && !out))
+        return NZGPU_INVALID_ARGUMENT;
+    if (int rc = device_ready()) return rc;
+    // Fast path only for what the side index describes: uniform framing, a
+    // matching v3 index, consistent sections (tensorstore.hpp:115-117,
+    // :218-227).  Everything else -- including every malformed input, so the
+    // error is reported exactly as the reference would -- goes general.
+    IndexHeader h{};
+    bool fast = t->index && t->index_len >= sizeof(h) && t->nchunks > 0 && t->n > 0;
+    uint64_t stream_len = 4, total = 0;
+    for (uint64_t c = 0; c < t->nchunks; ++c) {
+        stream_len += 8 + (uint64_t)t->chunks[c].len;
+        total += t->chunks[c].nsym;
+        if (t->chunks[c].len && !t->chunks[c].payload) return NZGPU_INVALID_ARGUMENT;
+    }
+    uint32_t sum = 0, single = 0xFFFFFFFFu;
+    for (int i = 0; i < 256; ++i) {
+        sum += t->freqs[i];
+        if (t->freqs[i] == kProbScale) single = (uint32_t)i;
+    }
+    fast = fast && total == t->n && sum == kProbScale && t->mantissa_len == mant_bytes(t->n, t->precision) &&
+           (t->precision == 7 || (t->block_size && t->scales_len == ceil_div(t->n, t->block_size)));
+    int log2k = -1;
+    uint32_t S = 0;
+    if (fast) {
+        std::memcpy(&h, t->index, sizeof(h));
+        S = t->nchunks == 1 && t->chunks[0].nsym <= h.chunk_syms ? h.chunk_syms : t->chunks[0].nsym;
+        log2k = log2_of(h.interval);
+        fast = h.magic == kIndexMagic && h.version == kIndexVersion && log2k >= 0 && h.chunk_syms == S &&
+               h.n == t->n && h.nchunks == t->nchunks && h.stream_len == stream_len && S % h.interval == 0 &&
+               h.nsub == ceil_div(t->n, h.interval) && t->index_len == sizeof(h) + index_region_bytes(h.nsub);
+        for (uint64_t c = 0; fast && c < t->nchunks; ++c) {
+            const uint32_t w = t->chunks[c].nsym;
+            fast = c + 1 < t->nchunks ? w == S : (w != 0 && w <= S);
+        }
+    }
+    if (!fast) return sections_general(t, out);
+
+    if (!g_host) g_host.reset(new HostCtx);
+    HostCtx& hc = *g_host;
+    if (int rc = hc.init()) return rc;
+    HostSlot& sl = hc.slot[0];
+    cudaStream_t s = sl.s;
+    CK(cudaStreamSynchronize(s));  // the slot's buffers and the pinned staging are free
+    CK(cudaMemsetAsync(sl.err, 0, 64, s));
+
+    nzgpu_blob_s& b = *new (std::nothrow) nzgpu_blob_s;  // descriptor over the slot's buffers
+    std::unique_ptr<nzgpu_blob_s> guard(&b);
+    b.owns = false;
+    b.n = t->n;
+    b.precision = t->precision;
+    b.block = t->precision == 7 ? 0 : t->block_size;
+    b.interval = h.interval;
+    b.log2k = log2k;
+    b.chunk_syms = S;
+    b.nchunks = t->nchunks;
+    b.nsub = h.nsub;
+    b.mant_len = t->mantissa_len;
+    b.scales_len = t->precision == 7 ? 0 : t->scales_len;
+    b.stream_len = stream_len;
+    uint32_t wide = 0;
+    if (t->precision != 7)
+        for (uint64_t i = 0; i < t->scales_len; ++i) wide |= t->scales[i] & 0x80u;
+    b.flags = (single != 0xFFFFFFFFu ? kFlagSingleSymbol : 0u) | (t->freqs[255] ? kFlagHas255 : 0u) |
+              (wide ? kFlagWideScale : 0u);
+    b.single_symbol = single != 0xFFFFFFFFu ? single : 0u;
+
+    // pinned staging: stream | mantissas | scales | index region | chunk table | table
+    Carve in;
+    const uint64_t i_stream = in.take(stream_len), i_mant = in.take(b.mant_len), i_scales = in.take(b.scales_len);
+    const uint64_t i_index = in.take(index_region_bytes(b.nsub)), i_info = in.take(b.nchunks * sizeof(uint4));
+    const uint64_t i_freqs = in.take(512);
+    if (int rc = hc.in.ensure(in.size)) return rc;
+    uint8_t* stage = static_cast<uint8_t*>(hc.in.p);
+    std::vector<uint4> info;
+    gather_stream(t, stage + i_stream, info);
+    par_memcpy(stage + i_mant, t->mantissas, b.mant_len);
+    if (b.scales_len) par_memcpy(stage + i_scales, t->scales, b.scales_len);
+    par_memcpy(stage + i_index, static_cast<const uint8_t*>(t->index) + sizeof(h), index_region_bytes(b.nsub));
+    std::memcpy(stage + i_info, info.data(), info.size() * sizeof(uint4));
+    std::memcpy(stage + i_freqs, t->freqs, 512);
+
+    Carve cv;
+    const uint64_t o_freqs = cv.take(512), o_lut = cv.take(16384), o_mant = cv.take(b.mant_len + 16);
+    const uint64_t o_scales = cv.take(std::max<uint64_t>(b.scales_len, 1));
+    const uint64_t o_info = cv.take(b.nchunks * sizeof(uint4));
+    const uint64_t o_index = cv.take(index_region_bytes(b.nsub) + 16), o_scr = cv.take(64);
+    if (int rc = sl.main.ensure(cv.size, s)) return rc;
+    if (int rc = sl.stream.ensure(align_up(stream_len, 16) + 32, s)) return rc;
+    if (int rc = sl.out.ensure(align_up(t->n * 2, 16) + 16, s)) return rc;
+    uint8_t* m = static_cast<uint8_t*>(sl.main.p);
+    b.freqs = reinterpret_cast<uint16_t*>(m + o_freqs);
+    b.lut = reinterpret_cast<uint32_t*>(m + o_lut);
+    b.mant = m + o_mant;
+    b.scales = m + o_scales;
+    b.chunk_info = reinterpret_cast<uint4*>(m + o_info);
+    b.index = m + o_index;
+    b.scratch_u32 = reinterpret_cast<uint32_t*>(m + o_scr);
+    b.stream = static_cast<uint8_t*>(sl.stream.p);
+    b.err = sl.err;
+    CK(cudaMemcpyAsync(b.stream, stage + i_stream, stream_len, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.mant, stage + i_mant, b.mant_len, cudaMemcpyHostToDevice, s));
+    if (b.scales_len) CK(cudaMemcpyAsync(b.scales, stage + i_scales, b.scales_len, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.index, stage + i_index, index_region_bytes(b.nsub), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.chunk_info, stage + i_info, b.nchunks * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.freqs, stage + i_freqs, 512, cudaMemcpyHostToDevice, s));
+    build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
+    CK(cudaGetLastError());
+    if (!(b.flags & kFlagSingleSymbol)) {
+        const uint32_t* base = reinterpret_cast<const uint32_t*>(stage + i_index) + b.nsub;  // aligned copy
+        const uint64_t bound = 64ull * h.interval + 64;
+        b.max_window_unit = h.max_window_unit && h.max_window_unit <= bound
+                                ? h.max_window_unit
+                                : host_max_window(info, base, b.nsub, S, log2k, 32);
+        if (!(use_persist() && persist_fits(log2k, b.max_window_unit)))
+            b.max_window = host_max_window(info, base, b.nsub, S, log2k, decode_tile_subs());
+    }
+    uint16_t* d_out = static_cast<uint16_t*>(sl.out.p);
+    if (int rc = decode_blob(&b, d_out, s)) return rc;
+
+    // bf16 back in slices through a pinned ring: the worker threads copy
+    // slice k into `out` while the DMA engine brings slice k + 1..
+    constexpr uint64_t kSlice = 32ull << 20;
+    const uint64_t bytes = t->n * 2, nslices = ceil_div(bytes, kSlice);
+    for (int r = 0; r < HostCtx::kOutRing; ++r)
+        if (int rc = hc.ring[r].ensure(std::min(kSlice, bytes))) return rc;
+    auto issue = [&](uint64_t k) -> int {
+        const int r = (int)(k % HostCtx::kOutRing);
+        const uint64_t a = k * kSlice, len = std::min(kSlice, bytes - a);
+        CK(cudaMemcpyAsync(hc.ring[r].p, reinterpret_cast<uint8_t*>(d_out) + a, len, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(hc.ring_ev[r], s));
+        return NZGPU_OK;
+    };
+    for (uint64_t k = 0; k < std::min<uint64_t>(nslices, HostCtx::kOutRing); ++k)
+        if (int rc = issue(k)) return rc;
+    for (uint64_t k = 0; k < nslices; ++k) {
+        const int r = (int)(k % HostCtx::kOutRing);
+        CK(cudaEventSynchronize(hc.ring_ev[r]));
+        const uint64_t a = k * kSlice;
+        par_memcpy(reinterpret_cast<uint8_t*>(out) + a, hc.ring[r].p, std::min(kSlice, bytes - a));
+        if (k + HostCtx::kOutRing < nslices)
+            if (int rc = issue(k + HostCtx::kOutRing)) return rc;
+    }
+    return sync_status(s, sl.err, true);
 }
 
 int nzgpu_host_release(void) {

@@ -249,31 +249,37 @@ struct LaneJob {
 
 // Raw index records of a lane's sub-range, loaded one unit ahead so the
 // global-memory latency never sits on a warp's critical path: the chunk
-// record, the lane's state and the next sub-range's (its end state), and its
-// chunk-relative start / end positions (nzgpu_internal.cuh: the offset plus
-// the unit position for anchored lanes; the end is the next sub-range's
-// start, for lane 31 the next unit's position).  The last sub-range of a
-// chunk ends at len - 4 instead (lane_job).
+// record, the lane's state and the next sub-range's (its end state), and the
+// terms of its chunk-relative start / end positions (nzgpu_internal.cuh: the
+// offset plus the unit position for anchored lanes; the end is the next
+// sub-range's start, for lane 31 the next unit's position).  The last
+// sub-range of a chunk ends at len - 4 instead (lane_job).
 struct RawRec {
     uint4 ci;
-    uint32_t st, st1, start, end;
+    uint32_t st, st1, off, off1, ref;
 };
 
+// Only loads here (their results are consumed a unit later, in lane_job):
+// the unit position comes from a predicated load rather than a select, so no
+// instruction waits on a load in this function.  Lane 31's end is the next
+// unit's position (the next sub-range is that unit's lane 0, offset 0), which
+// it loads into `off1`.
 template <int LOG2K>
 __device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint32_t nsub) {
-    RawRec r{make_uint4(0, 0, 0, 0), 0u, 0u, 0u, 0u};
+    RawRec r{make_uint4(0, 0, 0, 0), 0u, 0u, 0u, 0u, 0u};
     if (j >= nsub) return r;
     uint32_t ch, jin;
     sub_to_chunk(d, LOG2K, j, ch, jin);
     r.ci = d.chunk_info[ch];
     if (d.ck_state) {  // null for single-symbol tables (no index)
         const uint32_t lane = j & 31u;
-        const uint32_t ref = jin >= lane ? d.ck_base[j >> 5] : 0u;  // anchored lanes add the unit position
         r.st = d.ck_state[j];
-        r.start = d.ck_off[j] + ref;
+        r.off = d.ck_off[j];
+        if (jin >= lane) r.ref = d.ck_base[j >> 5];  // anchored: the unit position
         if (j + 1 < nsub) {
             r.st1 = d.ck_state[j + 1];
-            r.end = d.ck_off[j + 1] + (lane == 31u ? d.ck_base[(j >> 5) + 1] : ref);
+            if (lane == 31u) r.off1 = d.ck_base[(j >> 5) + 1];
+            else r.off1 = d.ck_off[j + 1];
         }
     }
     return r;
@@ -312,9 +318,10 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
     const bool last = sym_in + K >= nsym;
     if (jin != 0) L.x0 = raw.st;
     L.xe = last ? kStateLow : raw.st1;
-    const uint32_t end = last ? limit : raw.end;
-    if (raw.start > limit || end > limit) L.err |= kErrDesync;
-    L.p0 = ci.x - lo0 + min(raw.start, limit);  // chunk offsets of one unit differ by < 2^32
+    const uint32_t start = raw.off + raw.ref;
+    const uint32_t end = last ? limit : raw.off1 + ((j & 31u) == 31u ? 0u : raw.ref);
+    if (start > limit || end > limit) L.err |= kErrDesync;
+    L.p0 = ci.x - lo0 + min(start, limit);  // chunk offsets of one unit differ by < 2^32
     L.pe = ci.x - lo0 + min(end, limit);
     return L;
 }

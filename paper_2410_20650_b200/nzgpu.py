@@ -89,6 +89,29 @@ class HostTensor(C.Structure):
     ]
 
 
+class ChunkView(C.Structure):
+    """nzgpu_chunk_view: one AnsChunk (ans.hpp:159-164)."""
+    _fields_ = [("payload", C.c_void_p), ("len", C.c_uint32), ("nsym", C.c_uint32)]
+
+
+class HostSections(C.Structure):
+    """nzgpu_host_sections: a host tensor with the stream as chunk views."""
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("precision", C.c_int32),
+        ("block_size", C.c_uint32),
+        ("freqs", C.c_void_p),
+        ("chunks", C.POINTER(ChunkView)),
+        ("nchunks", C.c_uint64),
+        ("mantissas", C.c_void_p),
+        ("mantissa_len", C.c_uint64),
+        ("scales", C.c_void_p),
+        ("scales_len", C.c_uint64),
+        ("index", C.c_void_p),
+        ("index_len", C.c_uint64),
+    ]
+
+
 class BlobInfo(C.Structure):
     _fields_ = [
         ("n", C.c_uint64),
@@ -129,6 +152,7 @@ SIGNATURES = {
     "nzgpu_blob_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "nzgpu_blob_import": (_i, [_p(HostTensor), _u32, _vp, _p(_vp)]),
     "nzgpu_blob_decompress_host": (_i, [_vp, _vp]),
+    "nzgpu_decompress_host_sections": (_i, [_p(HostSections), _vp]),
     "nzgpu_plan_create": (_i, [_p(_vp), _p(_vp), _i, _p(_vp)]),
     "nzgpu_plan_launch": (_i, [_vp, _vp]),
     "nzgpu_plan_status": (_i, [_vp, _vp]),
@@ -169,7 +193,10 @@ def _load() -> C.CDLL:
             "(the codec has no CPU fallback)"
         )
     L = C.CDLL(LIB_PATH)
+    variant = "NZGPU_LIB" in os.environ  # dev A/B of an older build may lack newer entry points
     for name, (res, args) in SIGNATURES.items():
+        if variant and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

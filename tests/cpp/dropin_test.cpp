@@ -173,6 +173,21 @@ int main() {
         LosslessBlob no_index = big;  // as if the stream came from the reference
         no_index.gpu_index.clear();
         CHECK(decompress_lossless(no_index) == g);
+        {  // buffer-reuse extension: same values, twice into one vector
+            std::vector<Bf16> reuse(17, Bf16{0x1234});
+            decompress_lossless_into(big, reuse);
+            CHECK(reuse == g);
+            std::fill(reuse.begin(), reuse.end(), Bf16{0});
+            decompress_lossless_into(big, reuse);
+            CHECK(reuse == g);
+            LosslessBlob stale = big;  // index from another tensor: FormatError, never a wrong decode
+            stale.gpu_index[56 + 4 * 1000] ^= 0x5A;
+            CHECK(throws<FormatError>([&] { decompress_lossless_into(stale, reuse); }));
+            const LossyBlob lb3 = compress_lossy(g, 3, 512);
+            std::vector<Bf16> lossy_into;
+            decompress_lossy_into(lb3, lossy_into);
+            CHECK(lossy_into == decompress_lossy(lb3));
+        }
 
         LosslessBlob bad_meta = compress_lossless(std::span(g).first(1000));
         bad_meta.meta.shape = {999};
