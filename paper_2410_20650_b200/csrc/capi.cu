@@ -31,6 +31,8 @@ cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, uns
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
+cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTask& one, uint64_t total_units,
+                                  cudaStream_t s);
 cudaError_t launch_encode(bool queue, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
                           const EncTask& one, cudaStream_t s);
 __global__ void stream_scan_kernel(const EncTask*, const __grid_constant__ EncTask);
@@ -685,6 +687,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     std::vector<EncTask> tasks(count);
     std::vector<TableTask> tables(count);
     uint32_t ctas = 0;
+    uint64_t units = 0;  // warp units of every tensor's side index (index_finalize_kernel)
     for (int i = 0; i < count; ++i) {
         nzgpu_blob_s* b = bs[i];
         const uint64_t n = ns[i];
@@ -728,6 +731,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         t.chunk_syms = chunk_syms;
         t.log2k = (uint32_t)log2k;
         t.cta0 = ctas;
+        t.unit0 = units;
+        if (!irregular) units += index_units(b->nsub);
         const uint64_t c = ceil_div(b->nchunks, NZ_ENC_THREADS);
         if (ctas + c >= (1ull << 31)) return NZGPU_INVALID_ARGUMENT;
         ctas += (uint32_t)c;
@@ -744,6 +749,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
     CK(launch_encode(ctas >= kEncQueueMinCtas, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
                      s));
+    if (!irregular) CK(launch_index_finalize(count > 1 ? d_tasks : nullptr, count, tasks[0], units, s));
     stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);
     CK(cudaGetLastError());
     // One readback for every tensor: table info[3], error bits, stream length.

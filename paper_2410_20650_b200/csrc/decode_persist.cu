@@ -259,6 +259,15 @@ struct RawRec {
     uint32_t st, st1, off, off1, ref;
 };
 
+// 16-bit index load zero-extended by the load itself (a C++ u16 -> u32
+// conversion made ptxas mask the value right after the load, which then
+// waited on it: long-scoreboard stalls at ~8 % of the kernel).
+__device__ __forceinline__ uint32_t ldg_u16(const uint16_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u16 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 // Only loads here (their results are consumed a unit later, in lane_job):
 // the unit position comes from a predicated load rather than a select, so no
 // instruction waits on a load in this function.  Lane 31's end is the next
@@ -270,16 +279,16 @@ __device__ __forceinline__ RawRec load_raw(const DecodeDesc& d, uint32_t j, uint
     if (j >= nsub) return r;
     uint32_t ch, jin;
     sub_to_chunk(d, LOG2K, j, ch, jin);
-    r.ci = d.chunk_info[ch];
+    r.ci = __ldg(d.chunk_info + ch);
     if (d.ck_state) {  // null for single-symbol tables (no index)
         const uint32_t lane = j & 31u;
-        r.st = d.ck_state[j];
-        r.off = d.ck_off[j];
-        if (jin >= lane) r.ref = d.ck_base[j >> 5];  // anchored: the unit position
+        r.st = __ldg(d.ck_state + j);
+        r.off = ldg_u16(d.ck_off + j);
+        if (jin >= lane) r.ref = __ldg(d.ck_base + (j >> 5));  // anchored: the unit position
         if (j + 1 < nsub) {
-            r.st1 = d.ck_state[j + 1];
-            if (lane == 31u) r.off1 = d.ck_base[(j >> 5) + 1];
-            else r.off1 = d.ck_off[j + 1];
+            r.st1 = __ldg(d.ck_state + j + 1);
+            if (lane == 31u) r.off1 = __ldg(d.ck_base + (j >> 5) + 1);
+            else r.off1 = ldg_u16(d.ck_off + j + 1);
         }
     }
     return r;

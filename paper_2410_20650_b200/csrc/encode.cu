@@ -21,6 +21,8 @@
 //
 // K4 restates serialize_stream (ans.hpp:306-316): an exclusive scan of
 // (8 + len) over chunks, then a copy of every payload behind its header.
+#include <algorithm>
+
 #include "nzgpu_internal.cuh"
 
 namespace nzgpu {
@@ -52,7 +54,6 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     uint32_t* const ck_state = t.ck_state;
     uint32_t* const ck_base = t.ck_base;
     uint16_t* const ck_off = t.ck_off;
-    uint32_t e_prev = 0;  // bytes emitted at the previous (later) checkpoint
     const uint64_t nchunks = ceil_div(n, chunk_syms);
     const uint64_t c = (blockIdx.x - t.cta0) * (uint64_t)blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
@@ -104,8 +105,11 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
         if (may_ckpt && ck_state && (i & kmask) == 0) {
             const uint64_t j = (begin + i) >> log2_interval;
             ck_state[j] = x;
-            ck_off[j] = (uint16_t)(emitted - e_prev);  // consumed bytes, <= 1.5K + 2; positions below
-            e_prev = emitted;
+            // positions are final only once the chunk's length is known:
+            // record -E_j (mod 2^16) and, for unit starts, E_j itself;
+            // index_finalize_kernel adds the right reference (E_32u or len-4)
+            ck_off[j] = (uint16_t)(0u - emitted);
+            if ((j & 31) == 0) ck_base[j >> 5] = emitted;
         }
     };
     uint32_t i = len;
@@ -145,22 +149,50 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie below
     // the payload start, inside the slot.
     if (QUEUE && qc) *--wo = __byte_perm(qhi, 0, 0x0123) << (32 - 8 * qc);
-    if (ck_state) {
-        // forward over the chunk's sub-ranges: byte counts -> positions
-        const uint64_t j0 = begin >> log2_interval, j1 = (begin + len - 1) >> log2_interval;
-        uint32_t pos = 0;
-        for (uint64_t j = j0; j <= j1; ++j) {
-            const uint32_t c = ck_off[j];
-            const uint64_t u = j >> 5;
-            if ((j & 31) == 0) ck_base[u] = pos;
-            const bool anchored = (u << 5) >= j0;  // the unit's first sub-range is in this chunk
-            ck_off[j] = (uint16_t)(pos - (anchored ? ck_base[u] : 0u));
-            pos += c;
-        }
-    }
     // ans.hpp:223: final state little-endian at the tail (aligned store).
     *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
     t.plen[c] = emitted + 4;
+}
+
+// Side index positions after K3 (nzgpu_internal.cuh).  The encoder walks a
+// chunk backwards, so it records E_j (renormalisation bytes from sub-range j
+// to the chunk end) as -E_j mod 2^16 in off[j] and E_32u in base[u]; with
+// the chunk lengths known, one warp per unit turns them into
+//   base[u] = (len - 4) - E_32u                  (position of sub-range 32u)
+//   off[j]  = E_32u - E_j       anchored lanes   (position - base[u])
+//   off[j]  = (len' - 4) - E_j  other lanes      (position in their chunk)
+// -- independent per unit, so the serial encoder chains carry none of it.
+__global__ void __launch_bounds__(256) index_finalize_kernel(const EncTask* __restrict__ tasks, int ntasks,
+                                                             const __grid_constant__ EncTask one,
+                                                             uint64_t total_units) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < total_units; w += warps) {
+        const EncTask* tp = &one;
+        if (tasks) {
+            int lo = 0, hi = ntasks - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (tasks[mid].unit0 <= w) lo = mid; else hi = mid - 1;
+            }
+            tp = tasks + lo;
+        }
+        const EncTask& t = *tp;
+        const uint64_t u = w - t.unit0;
+        const uint64_t nsub = ceil_div(t.n, 1ull << t.log2k);
+        const uint64_t j = (u << 5) + lane;
+        const uint32_t log2_spc_k = t.log2k;  // symbols -> chunk via the symbol index
+        const uint64_t c0 = ((u << 5) << log2_spc_k) / t.chunk_syms;
+        const uint32_t e32 = t.ck_base[u];
+        const uint32_t total0 = t.plen[c0] - 4u;
+        if (j < nsub) {
+            const uint64_t c = (j << log2_spc_k) / t.chunk_syms;
+            const uint32_t add = c == c0 ? e32 : t.plen[c] - 4u;
+            t.ck_off[j] = (uint16_t)(t.ck_off[j] + add);
+        }
+        __syncwarp();
+        if (lane == 0) t.ck_base[u] = total0 - e32;
+    }
 }
 
 // Exclusive scan of (8 + len) over chunks -> chunk_info {off_lo, off_hi,
@@ -253,6 +285,14 @@ __global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restr
         d[w] = mis ? __funnelshift_r(lo, hi, 8 * mis) : lo;
     }
     for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTask& one, uint64_t total_units,
+                                  cudaStream_t s) {
+    if (!total_units) return cudaSuccess;
+    const uint64_t blocks = std::min<uint64_t>(ceil_div(total_units, 8), 148 * 16);
+    index_finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(tasks, ntasks, one, total_units);
+    return cudaGetLastError();
 }
 
 // K3 launcher (the template kernels stay in this translation unit).

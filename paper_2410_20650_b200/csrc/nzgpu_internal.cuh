@@ -89,6 +89,7 @@ struct EncTask {
     uint32_t log2k;
     uint32_t cta0;           // first K3 CTA of this tensor in the launch
     uint32_t pad_;
+    uint64_t unit0;          // first warp unit of this tensor in the index-finalize launch
 };
 
 // One tensor of a batched table build (K2): histogram in, tables out.

@@ -325,3 +325,4 @@ def test_encoder_exact_division_identity():
         assert ((x + q * np.uint64(4096 - f) + cum) == ((x // np.uint64(f)) << np.uint64(12)) + x % np.uint64(f) + cum).all()
 
 
+
