@@ -38,7 +38,9 @@ constexpr int kPUnroll = NZ_PUNROLL;
 constexpr int kPThreads = kPWarps * 32;
 constexpr uint32_t kPHeader = 128;  // LUT mbarrier
 
-__host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(log2k); }
+// exponent tile of a warp: 32 rows of (at most) 64 symbols (K = 128 is merged
+// in two halves through the same tile)
+__host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(log2k > 6 ? 6 : log2k); }
 
 // Per-warp region: its 2 mbarriers (16 B), the exponent tile (32 padded
 // rows) and 2 payload windows -- every per-warp address is the region base
@@ -342,8 +344,15 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                                                                       DecodeDesc one, uint32_t upc,
                                                                       uint32_t win_cap, MulConsts mc) {
     constexpr int K = 1 << LOG2K;
-    constexpr uint32_t RW = exps_row_words(LOG2K);
-    constexpr int G = K / 8;  // 8-element merge groups per lane per unit
+    // K = 128 sub-ranges are decoded and merged in two 64-symbol halves
+    // through one 64-symbol exponent tile (the unit's window and the lane's
+    // ANS state carry over), so shared memory and the merge are those of K = 64
+    // while the per-unit work (index records, window TMA, hand-out) is spread
+    // over twice the symbols.
+    constexpr int KH = K > 64 ? 64 : K;
+    constexpr int HALVES = K / KH;
+    constexpr uint32_t RW = exps_row_words(LOG2K > 6 ? 6 : LOG2K);
+    constexpr int G = KH / 8;  // 8-element merge groups per lane per half
     using HB = typename HalfBits<P>::T;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -472,201 +481,434 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         } else {
             unn = uend;
         }
-        const uint64_t sym0 = (uint64_t)u * 32 * K;
-        const uint32_t unit_syms = (uint32_t)min((uint64_t)32 * K, d.n - sym0);
-        const uint32_t groups = unit_syms >> 3;
-        // sign/mantissa words of this unit: in flight during the decode
-        const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
-        const bool full = unit_syms == 32u * K;  // every unit but a tensor's last
-        HB pre[G];
-        uint2 sw = make_uint2(0u, 0u);  // this unit's scale bytes (unit_scales >= 0)
-        if constexpr (P != 7) {
-            if (unit_scales >= 0) {
-                const uint64_t idx0 = sym0 >> d.log2_block;
-                if (unit_scales == 0) sw = __ldg(reinterpret_cast<const uint2*>(d.scales + idx0));
-                else if (unit_scales == 1) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + idx0));
-                else if (unit_scales == 2) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + (idx0 & ~3ull))) >>
-                                                  (8u * (uint32_t)(idx0 & 2u));
-                else sw.x = __ldg(d.scales + idx0);
+        if constexpr (HALVES == 1) {
+            const uint64_t sym0 = (uint64_t)u * 32 * K;
+            const uint32_t unit_syms = (uint32_t)min((uint64_t)32 * K, d.n - sym0);
+            const uint32_t groups = unit_syms >> 3;
+            // sign/mantissa words of this unit: in flight during the decode
+            const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
+            const bool full = unit_syms == 32u * K;  // every unit but a tensor's last
+            HB pre[G];
+            uint2 sw = make_uint2(0u, 0u);  // this unit's scale bytes (unit_scales >= 0)
+            if constexpr (P != 7) {
+                if (unit_scales >= 0) {
+                    const uint64_t idx0 = sym0 >> d.log2_block;
+                    if (unit_scales == 0) sw = __ldg(reinterpret_cast<const uint2*>(d.scales + idx0));
+                    else if (unit_scales == 1) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + idx0));
+                    else if (unit_scales == 2) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + (idx0 & ~3ull))) >>
+                                                      (8u * (uint32_t)(idx0 & 2u));
+                    else sw.x = __ldg(d.scales + idx0);
+                }
             }
-        }
-        if (full) {
-#pragma unroll
-            for (int gi = 0; gi < G; ++gi) pre[gi] = __ldcs(gb + lane + gi * 32);
-        } else {
-#pragma unroll
-            for (int gi = 0; gi < G; ++gi) {
-                const uint32_t g = lane + gi * 32;
-                if (g < groups) pre[gi] = __ldcs(gb + g);
+            if (full) {
+    #pragma unroll
+                for (int gi = 0; gi < G; ++gi) pre[gi] = __ldcs(gb + lane + gi * 32);
+            } else {
+    #pragma unroll
+                for (int gi = 0; gi < G; ++gi) {
+                    const uint32_t g = lane + gi * 32;
+                    if (g < groups) pre[gi] = __ldcs(gb + g);
+                }
             }
-        }
-        err |= cur.err;
-        uint32_t* row = exps + lane * RW;
-        if (single) {
-            const uint32_t wv = d.single_symbol * 0x01010101u;
-            for (uint32_t k = 0; k < (cur.cnt + 3) / 4; ++k) row[k] = wv;
-        } else {
-            const uint32_t t2 = p_wait_token(my_bar0 + 8 * b, (i >> 1) & 1);
-            if (!cur.err && cur.cnt) {
-                const uint32_t wbase = winbuf0 + b * winstride + t2;
-                uint32_t x = cur.x0;
-                const uint32_t p = wbase + (cur.p0 - wa_cur);
-#if NZ_PBYTES
-                uint32_t q = p, o8 = 0, w0 = 0, w1 = 0;
-#elif NZ_FLO
-                uint32_t q = p & ~3u, o8 = (p & 3u) * 0x1100u + 0x100u;  // PRMT selector nibbles 3,2 = k, k+1
-                uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
-#else
-                uint32_t q = p & ~3u, o8 = (p & 3u) * 0x11u + 0x10u;  // PRMT selector k | (k+1) << 4
-                uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
-#endif
-                if (cur.cnt == (uint32_t)K) {
-#pragma unroll kPUnroll
-                    for (uint32_t k = 0; k < (uint32_t)K / 4; ++k) {
-                        uint32_t v0, v1, v2, v3;
-                        NZP_STEP_A(lutt, x, q, o8, w0, w1, v0);
-                        NZP_STEP(lutt, x, q, o8, w0, w1, v1);
-                        NZP_STEP_A(lutt, x, q, o8, w0, w1, v2);
-                        NZP_STEP(lutt, x, q, o8, w0, w1, v3);
-                        row[k] = __byte_perm(__byte_perm(v0, v1, 0x0040), __byte_perm(v2, v3, 0x0040), 0x5410);
-                    }
-                } else {
-                    uint32_t word = 0;
-                    for (uint32_t k = 0; k < cur.cnt; ++k) {
-                        uint32_t v;
-                        NZP_STEP(lutt, x, q, o8, w0, w1, v);
-                        word |= (v & 0xFFu) << (8 * (k & 3));
-                        if ((k & 3) == 3 || k + 1 == cur.cnt) {
-                            row[k >> 2] = word;
-                            word = 0;
+            err |= cur.err;
+            uint32_t* row = exps + lane * RW;
+            if (single) {
+                const uint32_t wv = d.single_symbol * 0x01010101u;
+                for (uint32_t k = 0; k < (cur.cnt + 3) / 4; ++k) row[k] = wv;
+            } else {
+                const uint32_t t2 = p_wait_token(my_bar0 + 8 * b, (i >> 1) & 1);
+                if (!cur.err && cur.cnt) {
+                    const uint32_t wbase = winbuf0 + b * winstride + t2;
+                    uint32_t x = cur.x0;
+                    const uint32_t p = wbase + (cur.p0 - wa_cur);
+    #if NZ_PBYTES
+                    uint32_t q = p, o8 = 0, w0 = 0, w1 = 0;
+    #elif NZ_FLO
+                    uint32_t q = p & ~3u, o8 = (p & 3u) * 0x1100u + 0x100u;  // PRMT selector nibbles 3,2 = k, k+1
+                    uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
+    #else
+                    uint32_t q = p & ~3u, o8 = (p & 3u) * 0x11u + 0x10u;  // PRMT selector k | (k+1) << 4
+                    uint32_t w0 = p_lds32(q), w1 = p_lds32(q + 4);
+    #endif
+                    if (cur.cnt == (uint32_t)K) {
+    #pragma unroll kPUnroll
+                        for (uint32_t k = 0; k < (uint32_t)K / 4; ++k) {
+                            uint32_t v0, v1, v2, v3;
+                            NZP_STEP_A(lutt, x, q, o8, w0, w1, v0);
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v1);
+                            NZP_STEP_A(lutt, x, q, o8, w0, w1, v2);
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v3);
+                            row[k] = __byte_perm(__byte_perm(v0, v1, 0x0040), __byte_perm(v2, v3, 0x0040), 0x5410);
+                        }
+                    } else {
+                        uint32_t word = 0;
+                        for (uint32_t k = 0; k < cur.cnt; ++k) {
+                            uint32_t v;
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v);
+                            word |= (v & 0xFFu) << (8 * (k & 3));
+                            if ((k & 3) == 3 || k + 1 == cur.cnt) {
+                                row[k >> 2] = word;
+                                word = 0;
+                            }
                         }
                     }
+                    const uint32_t pend = wbase + (cur.pe - wa_cur);
+    #if NZ_PBYTES
+                    const uint32_t pos = q;
+    #elif NZ_FLO
+                    const uint32_t pos = q + (o8 >> 12);
+    #else
+                    const uint32_t pos = q + (o8 & 0xFu);
+    #endif
+                    if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
                 }
-                const uint32_t pend = wbase + (cur.pe - wa_cur);
-#if NZ_PBYTES
-                const uint32_t pos = q;
-#elif NZ_FLO
-                const uint32_t pos = q + (o8 >> 12);
-#else
-                const uint32_t pos = q + (o8 & 0xFu);
-#endif
-                if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
             }
-        }
-        __syncwarp();
-        // ---- merge this unit: 8-element groups, one coalesced 16-B store per lane
-        // group g = lane + 32 gi starts at element 8g: row (8g) / K, word ((8g) % K) / 4,
-        // i.e. a per-lane base plus a compile-time stride per gi (K <= 256)
-        uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
-        const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
-        // one fully unrolled loop per merge flavour, chosen once per unit
-        auto merge_groups = [&](auto flavour, auto full_unit) {
-            // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path,
-            // 4..7 lossy pow2 B with 8/4/2/1 scale bytes per unit (B >= 32K/8)
-            constexpr int M = decltype(flavour)::value;
-            constexpr bool FULL = decltype(full_unit)::value;
-            uint32_t blk0 = 0, rem0 = 0;
-            if constexpr (M == 1) {
-                blk0 = (uint32_t)(sym0 >> d.log2_block);
-                rem0 = (uint32_t)sym0 & (d.block_size - 1u);
-            }
-            // M >= 4: a unit (32K elements, 32K-aligned) spans NB whole blocks
-            // and merge group gi (elements 256 gi .. +255 of the unit) lies in
-            // block gi * NB / G -- one broadcast load for the unit (`sw`, issued
-            // with the sign/mantissa prefetch before the decode), then each
-            // group's bf16x2 coefficient 0x3F80|s is one PRMT with a constant
-            // selector (scale bytes are < 128 on this path).  The load stays
-            // inside the scale section: it starts NB-aligned and sections are
-            // padded to 256 bytes.
-            uint32_t sw0 = 0, sw1 = 0;
-            if constexpr (M >= 4) {
-                sw0 = sw.x | 0x80808080u;
-                sw1 = sw.y | 0x80808080u;
-            }
-#pragma unroll
-            for (int gi = 0; gi < G; ++gi) {
-                const uint32_t g = lane + gi * 32;
-                if (!FULL && g >= groups) break;
-                const HB s = pre[gi];
-                const uint32_t e = g << 3;
-                const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
-                const uint32_t e0 = er[0], e1 = er[1];
-                if constexpr (M == 0) {
-                    __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
-                } else if constexpr (M >= 4) {
-                    constexpr int NB = 8 >> (M - 4);
-                    const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
-                    const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
-                    __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
-                } else if constexpr (M == 1) {
-                    // power-of-two B >= 8: an aligned 8-group never straddles a block
-                    const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
-                    __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c, c, 8));
-                } else if constexpr (M == 2) {
-                    const uint64_t gidx = sym0 + e;
-                    const uint64_t b0 = gidx / d.block_size;
-                    const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * d.block_size - gidx);
-                    const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
-                    const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
-                    __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c0, c1, split));
-                } else {
-                    constexpr uint32_t W = P + 1;
-                    uint32_t bits;
-                    if constexpr (W == 4) bits = __byte_perm(hb_raw(s), 0, 0x0123);
-                    else if constexpr (W == 2) bits = __byte_perm(hb_raw(s), 0, 0x0144);
-                    else bits = hb_raw(s) << 24;
-                    const uint32_t B = d.block_size;
-                    const uint64_t gidx = sym0 + e;
-                    const uint64_t b0 = gidx / B;
-                    const float c0 = scale_coef(__ldg(d.scales + b0));
-                    const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
-                    const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
-                    const uint32_t ew[2] = {e0, e1};
-                    uint32_t res[4];
-#pragma unroll
-                    for (int qq = 0; qq < 8; ++qq) {
-                        const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
-                        const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
-                        float c = qq < (int)split ? c0 : c1;
-                        if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
-                        const uint32_t h = lossy_rebuild(item, ex, P, c);
-                        if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
+            __syncwarp();
+            // ---- merge this unit: 8-element groups, one coalesced 16-B store per lane
+            // group g = lane + 32 gi starts at element 8g: row (8g) / K, word ((8g) % K) / 4,
+            // i.e. a per-lane base plus a compile-time stride per gi (K <= 256)
+            uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
+            const uint32_t* erow = exps + (lane >> (LOG2K - 3)) * RW + (lane & ((K >> 3) - 1)) * 2;
+            // one fully unrolled loop per merge flavour, chosen once per unit
+            auto merge_groups = [&](auto flavour, auto full_unit) {
+                // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path,
+                // 4..7 lossy pow2 B with 8/4/2/1 scale bytes per unit (B >= 32K/8)
+                constexpr int M = decltype(flavour)::value;
+                constexpr bool FULL = decltype(full_unit)::value;
+                uint32_t blk0 = 0, rem0 = 0;
+                if constexpr (M == 1) {
+                    blk0 = (uint32_t)(sym0 >> d.log2_block);
+                    rem0 = (uint32_t)sym0 & (d.block_size - 1u);
+                }
+                // M >= 4: a unit (32K elements, 32K-aligned) spans NB whole blocks
+                // and merge group gi (elements 256 gi .. +255 of the unit) lies in
+                // block gi * NB / G -- one broadcast load for the unit (`sw`, issued
+                // with the sign/mantissa prefetch before the decode), then each
+                // group's bf16x2 coefficient 0x3F80|s is one PRMT with a constant
+                // selector (scale bytes are < 128 on this path).  The load stays
+                // inside the scale section: it starts NB-aligned and sections are
+                // padded to 256 bytes.
+                uint32_t sw0 = 0, sw1 = 0;
+                if constexpr (M >= 4) {
+                    sw0 = sw.x | 0x80808080u;
+                    sw1 = sw.y | 0x80808080u;
+                }
+    #pragma unroll
+                for (int gi = 0; gi < G; ++gi) {
+                    const uint32_t g = lane + gi * 32;
+                    if (!FULL && g >= groups) break;
+                    const HB s = pre[gi];
+                    const uint32_t e = g << 3;
+                    const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
+                    const uint32_t e0 = er[0], e1 = er[1];
+                    if constexpr (M == 0) {
+                        __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                    } else if constexpr (M >= 4) {
+                        constexpr int NB = 8 >> (M - 4);
+                        const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
+                        const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
+                        __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
+                    } else if constexpr (M == 1) {
+                        // power-of-two B >= 8: an aligned 8-group never straddles a block
+                        const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
+                        __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c, c, 8));
+                    } else if constexpr (M == 2) {
+                        const uint64_t gidx = sym0 + e;
+                        const uint64_t b0 = gidx / d.block_size;
+                        const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * d.block_size - gidx);
+                        const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
+                        const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
+                        __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c0, c1, split));
+                    } else {
+                        constexpr uint32_t W = P + 1;
+                        uint32_t bits;
+                        if constexpr (W == 4) bits = __byte_perm(hb_raw(s), 0, 0x0123);
+                        else if constexpr (W == 2) bits = __byte_perm(hb_raw(s), 0, 0x0144);
+                        else bits = hb_raw(s) << 24;
+                        const uint32_t B = d.block_size;
+                        const uint64_t gidx = sym0 + e;
+                        const uint64_t b0 = gidx / B;
+                        const float c0 = scale_coef(__ldg(d.scales + b0));
+                        const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
+                        const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+                        const uint32_t ew[2] = {e0, e1};
+                        uint32_t res[4];
+    #pragma unroll
+                        for (int qq = 0; qq < 8; ++qq) {
+                            const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
+                            const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
+                            float c = qq < (int)split ? c0 : c1;
+                            if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
+                            const uint32_t h = lossy_rebuild(item, ex, P, c);
+                            if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
+                        }
+                        __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
                     }
-                    __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
+                }
+            };
+            auto merge_unit = [&](auto flavour) {
+                if (full) merge_groups(flavour, std::true_type{});
+                else merge_groups(flavour, std::false_type{});
+            };
+            if constexpr (P == 7) {
+                merge_unit(std::integral_constant<int, 0>{});
+            } else if (!fast_lossy) {
+                merge_unit(std::integral_constant<int, 3>{});
+            } else if (unit_scales >= 0) {
+                // scale bytes per unit: 32K / B = 2^(3 - unit_scales) (1 when B >= 32K)
+                if (unit_scales == 0) merge_unit(std::integral_constant<int, 4>{});
+                else if (unit_scales == 1) merge_unit(std::integral_constant<int, 5>{});
+                else if (unit_scales == 2) merge_unit(std::integral_constant<int, 6>{});
+                else merge_unit(std::integral_constant<int, 7>{});
+            } else if (d.log2_block != 0xFFFFFFFFu) {
+                merge_unit(std::integral_constant<int, 1>{});
+            } else {
+                merge_unit(std::integral_constant<int, 2>{});
+            }
+            for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
+                const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
+                const uint64_t gidx = sym0 + ii;
+                if constexpr (P == 7) {
+                    const uint32_t sm = __ldg(d.mant + gidx);
+                    d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
+                } else {
+                    d.out[gidx] = lossy_rebuild(packed_item(d.mant, gidx, P), ex, P,
+                                                scale_coef(__ldg(d.scales + gidx / d.block_size)));
                 }
             }
-        };
-        auto merge_unit = [&](auto flavour) {
-            if (full) merge_groups(flavour, std::true_type{});
-            else merge_groups(flavour, std::false_type{});
-        };
-        if constexpr (P == 7) {
-            merge_unit(std::integral_constant<int, 0>{});
-        } else if (!fast_lossy) {
-            merge_unit(std::integral_constant<int, 3>{});
-        } else if (unit_scales >= 0) {
-            // scale bytes per unit: 32K / B = 2^(3 - unit_scales) (1 when B >= 32K)
-            if (unit_scales == 0) merge_unit(std::integral_constant<int, 4>{});
-            else if (unit_scales == 1) merge_unit(std::integral_constant<int, 5>{});
-            else if (unit_scales == 2) merge_unit(std::integral_constant<int, 6>{});
-            else merge_unit(std::integral_constant<int, 7>{});
-        } else if (d.log2_block != 0xFFFFFFFFu) {
-            merge_unit(std::integral_constant<int, 1>{});
+            __syncwarp();
         } else {
-            merge_unit(std::integral_constant<int, 2>{});
-        }
-        for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
-            const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
-            const uint64_t gidx = sym0 + ii;
-            if constexpr (P == 7) {
-                const uint32_t sm = __ldg(d.mant + gidx);
-                d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
-            } else {
-                d.out[gidx] = lossy_rebuild(packed_item(d.mant, gidx, P), ex, P,
-                                            scale_coef(__ldg(d.scales + gidx / d.block_size)));
+            const uint64_t sym0 = (uint64_t)u * 32 * K;
+            const uint32_t unit_syms = (uint32_t)min((uint64_t)32 * K, d.n - sym0);
+            // sign/mantissa words of this unit: in flight during the decode
+            const HB* gb = reinterpret_cast<const HB*>(d.mant + sym0 * (P + 1) / 8);
+            const bool full = unit_syms == 32u * K;  // every unit but a tensor's last
+            uint2 sw = make_uint2(0u, 0u);  // this unit's scale bytes (unit_scales >= 0)
+            if constexpr (P != 7) {
+                if (unit_scales >= 0) {
+                    const uint64_t idx0 = sym0 >> d.log2_block;
+                    if (unit_scales == 0) sw = __ldg(reinterpret_cast<const uint2*>(d.scales + idx0));
+                    else if (unit_scales == 1) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + idx0));
+                    else if (unit_scales == 2) sw.x = __ldg(reinterpret_cast<const uint32_t*>(d.scales + (idx0 & ~3ull))) >>
+                                                      (8u * (uint32_t)(idx0 & 2u));
+                    else sw.x = __ldg(d.scales + idx0);
+                }
             }
+            err |= cur.err;
+            uint32_t* row = exps + lane * RW;
+            // Element offset (within the unit) of merge group gi of this lane in
+            // half h: group g = lane + 32 gi covers 8 elements of sub-range row
+            // r = g / 8 (lane = row of the exponent tile), KH-symbol half h.  For
+            // K = 64 (one half) this is simply 8 g.
+            auto grp = [&](int gi, int h) -> uint32_t {  // element offset / 8
+                if constexpr (HALVES == 1) return (uint32_t)(lane + 32 * gi);
+                else return (uint32_t)(((lane >> 3) + 4 * gi) * (K / 8) + h * (KH / 8) + (lane & 7));
+            };
+            const uint32_t groups = unit_syms >> 3;
+            // decoder state, carried across the halves of a K = 128 unit
+            bool dec = false;
+            uint32_t x = 0, q = 0, o8 = 0, w0 = 0, w1 = 0, wbase = 0;
+            if (!single) {
+                const uint32_t t2 = p_wait_token(my_bar0 + 8 * b, (i >> 1) & 1);
+                dec = !cur.err && cur.cnt;
+                if (dec) {
+                    wbase = winbuf0 + b * winstride + t2;
+                    x = cur.x0;
+                    const uint32_t p = wbase + (cur.p0 - wa_cur);
+    #if NZ_PBYTES
+                    q = p;
+    #elif NZ_FLO
+                    q = p & ~3u;
+                    o8 = (p & 3u) * 0x1100u + 0x100u;  // PRMT selector nibbles 3,2 = k, k+1
+                    w0 = p_lds32(q);
+                    w1 = p_lds32(q + 4);
+    #else
+                    q = p & ~3u;
+                    o8 = (p & 3u) * 0x11u + 0x10u;  // PRMT selector k | (k+1) << 4
+                    w0 = p_lds32(q);
+                    w1 = p_lds32(q + 4);
+    #endif
+                }
+            }
+    #pragma unroll
+            for (int h = 0; h < HALVES; ++h) {
+                HB pre[G];
+                if (full) {
+    #pragma unroll
+                    for (int gi = 0; gi < G; ++gi) pre[gi] = __ldcs(gb + grp(gi, h));
+                } else {
+    #pragma unroll
+                    for (int gi = 0; gi < G; ++gi) {
+                        const uint32_t g = grp(gi, h);
+                        if (g < groups) pre[gi] = __ldcs(gb + g);
+                    }
+                }
+                // this lane's symbols in half h
+                const uint32_t hcnt = cur.cnt > (uint32_t)(h * KH) ? min((uint32_t)KH, cur.cnt - (uint32_t)(h * KH)) : 0u;
+                if (single) {
+                    const uint32_t wv = d.single_symbol * 0x01010101u;
+                    for (uint32_t k = 0; k < (hcnt + 3) / 4; ++k) row[k] = wv;
+                } else if (dec) {
+#if NZ_FLO && !NZ_PBYTES
+                    // the register window is the two words at q (an invariant of
+                    // NZP_STEP): reload rather than keep it live across the merge
+                    if (h > 0) {
+                        w0 = p_lds32(q);
+                        w1 = p_lds32(q + 4);
+                    }
+#endif
+                    if (hcnt == (uint32_t)KH) {
+    #pragma unroll kPUnroll
+                        for (uint32_t k = 0; k < (uint32_t)KH / 4; ++k) {
+                            uint32_t v0, v1, v2, v3;
+                            NZP_STEP_A(lutt, x, q, o8, w0, w1, v0);
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v1);
+                            NZP_STEP_A(lutt, x, q, o8, w0, w1, v2);
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v3);
+                            row[k] = __byte_perm(__byte_perm(v0, v1, 0x0040), __byte_perm(v2, v3, 0x0040), 0x5410);
+                        }
+                    } else if (hcnt) {
+                        uint32_t word = 0;
+                        for (uint32_t k = 0; k < hcnt; ++k) {
+                            uint32_t v;
+                            NZP_STEP(lutt, x, q, o8, w0, w1, v);
+                            word |= (v & 0xFFu) << (8 * (k & 3));
+                            if ((k & 3) == 3 || k + 1 == hcnt) {
+                                row[k >> 2] = word;
+                                word = 0;
+                            }
+                        }
+                    }
+                    if (h == HALVES - 1) {
+                        const uint32_t pend = wbase + (cur.pe - wa_cur);
+    #if NZ_PBYTES
+                        const uint32_t pos = q;
+    #elif NZ_FLO
+                        const uint32_t pos = q + (o8 >> 12);
+    #else
+                        const uint32_t pos = q + (o8 & 0xFu);
+    #endif
+                        if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
+                    }
+                }
+                __syncwarp();
+            // ---- merge this half: 8-element groups, one coalesced 16-B store per lane
+            // group g = lane + 32 gi: exponent-tile row g / 8, words 2 (g % 8), +1,
+            // i.e. a per-lane base plus a compile-time stride per gi
+            uint4* out = reinterpret_cast<uint4*>(d.out + sym0);
+            const uint32_t* erow = exps + (lane >> 3) * RW + (lane & 7) * 2;
+            // one fully unrolled loop per merge flavour, chosen once per unit
+            auto merge_groups = [&](auto flavour, auto full_unit) {
+                // 0 lossless, 1 lossy pow2 B, 2 lossy any B, 3 float path,
+                // 4..7 lossy pow2 B with 8/4/2/1 scale bytes per unit (B >= 128K)
+                constexpr int M = decltype(flavour)::value;
+                constexpr bool FULL = decltype(full_unit)::value;
+                uint32_t blk0 = 0, rem0 = 0;
+                if constexpr (M == 1) {
+                    blk0 = (uint32_t)(sym0 >> d.log2_block);
+                    rem0 = (uint32_t)sym0 & (d.block_size - 1u);
+                }
+                // M >= 4: a unit (32K elements, 32K-aligned) spans NB whole blocks
+                // and merge group gi (tile rows 4 gi .. 4 gi + 3, i.e. unit elements
+                // 4 gi K .. 4 (gi + 1) K - 1 with B >= 4K) lies in block gi * NB / G
+                // -- one broadcast load for the unit (`sw`, issued with the
+                // sign/mantissa prefetch before the decode), then each group's
+                // bf16x2 coefficient 0x3F80|s is one PRMT with a constant selector
+                // (scale bytes are < 128 on this path).  The load stays inside the
+                // scale section: it starts NB-aligned and sections are padded to
+                // 256 bytes.
+                uint32_t sw0 = 0, sw1 = 0;
+                if constexpr (M >= 4) {
+                    sw0 = sw.x | 0x80808080u;
+                    sw1 = sw.y | 0x80808080u;
+                }
+    #pragma unroll
+                for (int gi = 0; gi < G; ++gi) {
+                    const uint32_t g = grp(gi, h);
+                    if (!FULL && g >= groups) continue;
+                    const uint32_t e = g << 3;
+                    const HB s = pre[gi];
+                    const uint32_t* er = erow + gi * (4 * RW);
+                    const uint32_t e0 = er[0], e1 = er[1];
+                    if constexpr (M == 0) {
+                        __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                    } else if constexpr (M >= 4) {
+                        constexpr int NB = 8 >> (M - 4);
+                        const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
+                        const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
+                        __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
+                    } else if constexpr (M == 1) {
+                        // power-of-two B >= 8: an aligned 8-group never straddles a block
+                        const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
+                        __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c, c, 8));
+                    } else if constexpr (M == 2) {
+                        const uint64_t gidx = sym0 + e;
+                        const uint64_t b0 = gidx / d.block_size;
+                        const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * d.block_size - gidx);
+                        const uint32_t c0 = scale_coef_bf16(__ldg(d.scales + b0));
+                        const uint32_t c1 = split < 8 ? scale_coef_bf16(__ldg(d.scales + b0 + 1)) : c0;
+                        __stcs(out + g, lossy_merge8<P>(e0, e1, hb_raw(s), c0, c1, split));
+                    } else {
+                        constexpr uint32_t W = P + 1;
+                        uint32_t bits;
+                        if constexpr (W == 4) bits = __byte_perm(hb_raw(s), 0, 0x0123);
+                        else if constexpr (W == 2) bits = __byte_perm(hb_raw(s), 0, 0x0144);
+                        else bits = hb_raw(s) << 24;
+                        const uint32_t B = d.block_size;
+                        const uint64_t gidx = sym0 + e;
+                        const uint64_t b0 = gidx / B;
+                        const float c0 = scale_coef(__ldg(d.scales + b0));
+                        const uint32_t split = (uint32_t)min((uint64_t)8, (b0 + 1) * B - gidx);
+                        const float c1 = split < 8 ? scale_coef(__ldg(d.scales + b0 + 1)) : c0;
+                        const uint32_t ew[2] = {e0, e1};
+                        uint32_t res[4];
+    #pragma unroll
+                        for (int qq = 0; qq < 8; ++qq) {
+                            const uint32_t ex = (ew[qq >> 2] >> (8 * (qq & 3))) & 0xFFu;
+                            const uint32_t item = (bits >> (32 - (qq + 1) * W)) & ((1u << W) - 1u);
+                            float c = qq < (int)split ? c0 : c1;
+                            if (B < 8 && qq >= (int)split) c = scale_coef(__ldg(d.scales + (gidx + qq) / B));
+                            const uint32_t h = lossy_rebuild(item, ex, P, c);
+                            if (qq & 1) res[qq >> 1] |= h << 16; else res[qq >> 1] = h;
+                        }
+                        __stcs(out + g, make_uint4(res[0], res[1], res[2], res[3]));
+                    }
+                }
+            };
+            auto merge_unit = [&](auto flavour) {
+                if (full) merge_groups(flavour, std::true_type{});
+                else merge_groups(flavour, std::false_type{});
+            };
+            if constexpr (P == 7) {
+                merge_unit(std::integral_constant<int, 0>{});
+            } else if (!fast_lossy) {
+                merge_unit(std::integral_constant<int, 3>{});
+            } else if (unit_scales >= 0) {
+                // scale bytes per unit: 32K / B = 2^(3 - unit_scales) (1 when B >= 32K)
+                if (unit_scales == 0) merge_unit(std::integral_constant<int, 4>{});
+                else if (unit_scales == 1) merge_unit(std::integral_constant<int, 5>{});
+                else if (unit_scales == 2) merge_unit(std::integral_constant<int, 6>{});
+                else merge_unit(std::integral_constant<int, 7>{});
+            } else if (d.log2_block != 0xFFFFFFFFu) {
+                merge_unit(std::integral_constant<int, 1>{});
+            } else {
+                merge_unit(std::integral_constant<int, 2>{});
+            }
+            for (uint32_t ii = (unit_syms & ~7u) + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
+                if ((int)((ii & (K - 1)) / KH) != h) continue;  // lies in the other half
+                const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (KH - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
+                const uint64_t gidx = sym0 + ii;
+                if constexpr (P == 7) {
+                    const uint32_t sm = __ldg(d.mant + gidx);
+                    d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
+                } else {
+                    d.out[gidx] = lossy_rebuild(packed_item(d.mant, gidx, P), ex, P,
+                                                scale_coef(__ldg(d.scales + gidx / d.block_size)));
+                }
+            }
+            __syncwarp();
+            }  // halves
         }
-        __syncwarp();
         cur = nxt;
         wa_cur = wa_nxt;
         u = un;
