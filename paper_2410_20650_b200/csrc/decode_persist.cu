@@ -33,6 +33,10 @@ namespace nzgpu {
 
 namespace {
 
+#ifndef NZ_HALVES_UNROLL
+#define NZ_HALVES_UNROLL 2
+#endif
+constexpr int kHalvesUnroll = NZ_HALVES_UNROLL;  // K = 128: unrolled halves (code size vs registers)
 constexpr int kPWarps = NZ_PWARPS;
 constexpr int kPUnroll = NZ_PUNROLL;
 constexpr int kPThreads = kPWarps * 32;
@@ -560,7 +564,8 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     #else
                     const uint32_t pos = q + (o8 & 0xFu);
     #endif
-                    if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
+                    NZ_CHECK(q + 8 <= winbuf0 + b * winstride + winstride && q >= winbuf0 + b * winstride);
+                if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
                 }
             }
             __syncwarp();
@@ -602,12 +607,14 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                     const uint32_t* er = erow + gi * ((256 >> LOG2K) * RW);
                     const uint32_t e0 = er[0], e1 = er[1];
                     if constexpr (M == 0) {
-                        __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                        NZ_CHECK(sym0 + 8ull * g + 8 <= d.n);
+                    __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
                     } else if constexpr (M >= 4) {
                         constexpr int NB = 8 >> (M - 4);
                         const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
                         const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
-                        __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
+                        NZ_CHECK(sym0 + 8ull * g + 8 <= d.n);
+                    __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
                     } else if constexpr (M == 1) {
                         // power-of-two B >= 8: an aligned 8-group never straddles a block
                         const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
@@ -668,6 +675,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
             for (uint32_t ii = groups * 8 + lane; ii < unit_syms; ii += 32) {  // tensor tail (n % 8)
                 const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (K - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
                 const uint64_t gidx = sym0 + ii;
+            NZ_CHECK(gidx < d.n);
                 if constexpr (P == 7) {
                     const uint32_t sm = __ldg(d.mant + gidx);
                     d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));
@@ -730,7 +738,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     #endif
                 }
             }
-    #pragma unroll
+#pragma unroll kHalvesUnroll
             for (int h = 0; h < HALVES; ++h) {
                 HB pre[G];
                 if (full) {
@@ -788,7 +796,8 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     #else
                         const uint32_t pos = q + (o8 & 0xFu);
     #endif
-                        if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
+                        NZ_CHECK(q + 8 <= winbuf0 + b * winstride + winstride && q >= winbuf0 + b * winstride);
+                if (x != cur.xe || pos != pend) err |= pos > pend ? kErrTruncated : kErrDesync;
                     }
                 }
                 __syncwarp();
@@ -831,12 +840,14 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                     const uint32_t* er = erow + gi * (4 * RW);
                     const uint32_t e0 = er[0], e1 = er[1];
                     if constexpr (M == 0) {
-                        __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
+                        NZ_CHECK(sym0 + 8ull * g + 8 <= d.n);
+                    __stcs(out + g, merge8(e0, hb_lo(s), e1, hb_hi(s)));
                     } else if constexpr (M >= 4) {
                         constexpr int NB = 8 >> (M - 4);
                         const uint32_t k = (uint32_t)(gi * NB / G);  // constant after unrolling
                         const uint32_t cp = __byte_perm(k < 4 ? sw0 : sw1, 0x3F3F3F3Fu, 0x4040u | (k & 3u) | ((k & 3u) << 8));
-                        __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
+                        NZ_CHECK(sym0 + 8ull * g + 8 <= d.n);
+                    __stcs(out + g, lossy_merge8_cp<P>(e0, e1, hb_raw(s), cp));
                     } else if constexpr (M == 1) {
                         // power-of-two B >= 8: an aligned 8-group never straddles a block
                         const uint32_t c = scale_coef_bf16(__ldg(d.scales + blk0 + ((rem0 + e) >> d.log2_block)));
@@ -898,6 +909,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                 if ((int)((ii & (K - 1)) / KH) != h) continue;  // lies in the other half
                 const uint32_t ex = (exps[(ii >> LOG2K) * RW + ((ii & (KH - 1)) >> 2)] >> (8 * (ii & 3))) & 0xFFu;
                 const uint64_t gidx = sym0 + ii;
+            NZ_CHECK(gidx < d.n);
                 if constexpr (P == 7) {
                     const uint32_t sm = __ldg(d.mant + gidx);
                     d.out[gidx] = (uint16_t)(((sm & 0x80u) << 8) | (ex << 7) | (sm & 0x7Fu));

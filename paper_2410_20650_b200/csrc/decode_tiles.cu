@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kDecodeThreads, NZ_MINBLOCKS) decode_tiles_ker
         const uint32_t* er = exps_s + (e >> LOG2K) * RW + ((e & (K - 1)) >> 2);
         const uint32_t e0 = er[0], e1 = er[1];
         if constexpr (P == 7) {
+            NZ_CHECK(sym0 + 8ull * g + 8 <= d.n);
             __stcs(out + g, merge8(e0, s.x, e1, s.y));
         } else if (fast_lossy) {
             const uint64_t gi = sym0 + e;

@@ -88,10 +88,12 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
             qhi = __funnelshift_r(qhi, x, 8 * nb);  // x & 0xFF first, then (x >> 8) & 0xFF
             qc += nb;
             if (qc >= 4) {  // the 4 oldest queued bytes, oldest at the highest address
+                NZ_CHECK(reinterpret_cast<uint8_t*>(wo - 1) >= slot_end - t.slot_bytes);
                 *--wo = __byte_perm(__funnelshift_rc(qlo, qhi, 64 - 8 * qc), 0, 0x0123);
                 qc -= 4;
             }
         } else {
+            NZ_CHECK(out - nb >= slot_end - t.slot_bytes);
             if (n1) out[-1] = (uint8_t)x;
             if (n2) out[-2] = (uint8_t)(x >> 8);
             out -= nb;

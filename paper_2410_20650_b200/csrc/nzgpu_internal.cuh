@@ -182,6 +182,24 @@ __device__ __forceinline__ uint16_t bf16_from_float(float f) {
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// Bounds assertions of the checked build (NZ_CHECKS=1, libnzgpu_checks.so;
+// tools/checked_suite.sh runs the GPU tests against it): a violated bound
+// traps the kernel, so the launch fails loudly instead of touching memory
+// it does not own.  Compiled out of the product library.
+#ifndef NZ_CHECKS
+#define NZ_CHECKS 0
+#endif
+#if NZ_CHECKS
+#define NZ_CHECK(cond)      \
+    do {                    \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define NZ_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 // Per-device, thread-safe record of the dynamic shared-memory opt-in of one
 // kernel: the attribute is per (device, function), so a process that drives
 // several GPUs (one host thread per device) must set it on each of them.
