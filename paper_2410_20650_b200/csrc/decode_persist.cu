@@ -395,22 +395,27 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
                                 ? min((int)d.log2_block - (LOG2K + 2), 3)
                                 : -1;
 
+    // Prologue: thread 0 arms the CTA's LUT copy; every warp's lane 0 inits
+    // the warp's own two window barriers, so each warp can load its first
+    // index records and issue its first window TMA before the CTA barrier
+    // (a lone launch -- a small tensor -- pays this latency once, unhidden).
     if (threadIdx.x == 0) {
         *reinterpret_cast<uint32_t*>(smem + 16) = ubeg + 2 * kPWarps;  // dynamic unit counter
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lut_bar));
-        for (int w = 0; w < kPWarps; ++w) {
-            const uint32_t r = sbase + kPHeader + kLutBytes + w * wregion;
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(r + 8));
-        }
         fence_mbar_init();
         if (!single) {
             p_expect_tx(lut_bar, kLutBytes);
             p_bulk(lut, d.lut, kLutBytes, lut_bar);
         }
     }
-    __syncthreads();
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(my_bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(my_bar0 + 8));
+        fence_mbar_init();
+    }
+    __syncwarp();
     if (ubeg >= uend) {
+        __syncthreads();
         if (!single) p_wait_token(lut_bar, 0);
         return;
     }
@@ -470,6 +475,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
         if (un < uend) raw_n = load_raw<LOG2K>(d, un * 32 + lane, nsub);
         cur = stage(u, 0, wa_cur, r0);
     }
+    __syncthreads();  // the LUT barrier is initialised (and the unit counter set)
     uint32_t tok = 0;
     if (!single) tok = p_wait_token(lut_bar, 0);
     const uint32_t lutt = lut + tok;
