@@ -113,8 +113,9 @@ int nzgpu_set_decode_kernel(int which);
 /* ---- device tier: device pointers, stream-ordered ---------------------- */
 /* Compress n bf16 values resident on the device (compress_lossless,
  * tensorstore.hpp:87-106, precision 7; compress_lossy, :141-208, k in
- * {0,1,3}).  chunk_symbols S (0 = 65536) and interval K (0 = 64, a power of
- * two in {64,128,256} dividing S).  Synchronises `stream` once (to size the
+ * {0,1,3}).  chunk_symbols S (0 = 65536) and interval K (0 = 64; 64 or 128,
+ * dividing S: the side index holds 16-bit offsets within a 32-sub-range
+ * unit, <= 31 (1.5 K + 2) bytes).  Synchronises `stream` once (to size the
  * exact stream allocation).  d_values must be 16-byte aligned. */
 int nzgpu_compress(const uint16_t* d_values, uint64_t n, int precision, uint32_t block_size,
                    uint32_t chunk_symbols, uint32_t interval, void* cuda_stream, nzgpu_blob* out);
@@ -227,6 +228,12 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
  * largest tensor it has staged) between calls; this frees the calling
  * thread's staging after its queued work completes. */
 int nzgpu_host_release(void);
+
+/* Blob sections live in a library-owned stream-ordered memory pool per
+ * device that keeps freed memory for the next blob (no cudaMalloc per
+ * compress).  This returns the current device's unused pool memory to the
+ * driver. */
+int nzgpu_trim_device_pool(void);
 
 /* ---- building blocks (device pointers, stream-ordered) ------------------ */
 /* K1: exponent plane, sign/mantissa plane and 256-bin u64 histogram
