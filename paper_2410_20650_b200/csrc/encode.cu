@@ -25,6 +25,10 @@
 
 #include "nzgpu_internal.cuh"
 
+#ifndef NZ_ENC_NOSTORE
+#define NZ_ENC_NOSTORE 0
+#endif
+
 namespace nzgpu {
 
 // Task of CTA `blk`: the last task whose first CTA is <= blk (tasks are in
@@ -94,8 +98,10 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
             }
         } else {
             NZ_CHECK(out - nb >= slot_end - t.slot_bytes);
+#if !NZ_ENC_NOSTORE  // timing experiment only: the chain without its byte stores
             if (n1) out[-1] = (uint8_t)x;
             if (n2) out[-2] = (uint8_t)(x >> 8);
+#endif
             out -= nb;
         }
         emitted += nb;
