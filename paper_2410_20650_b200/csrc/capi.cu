@@ -1815,21 +1815,9 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
               (wide ? kFlagWideScale : 0u);
     b.single_symbol = single != 0xFFFFFFFFu ? single : 0u;
 
-    // pinned staging: stream | mantissas | scales | index region | chunk table | table
-    Carve in;
-    const uint64_t i_stream = in.take(stream_len), i_mant = in.take(b.mant_len), i_scales = in.take(b.scales_len);
-    const uint64_t i_index = in.take(index_region_bytes(b.nsub)), i_info = in.take(b.nchunks * sizeof(uint4));
-    const uint64_t i_freqs = in.take(512);
-    if (int rc = hc.in.ensure(in.size)) return rc;
-    uint8_t* stage = static_cast<uint8_t*>(hc.in.p);
-    std::vector<uint4> info;
-    gather_stream(t, stage + i_stream, info);
-    par_memcpy(stage + i_mant, t->mantissas, b.mant_len);
-    if (b.scales_len) par_memcpy(stage + i_scales, t->scales, b.scales_len);
-    par_memcpy(stage + i_index, static_cast<const uint8_t*>(t->index) + sizeof(h), index_region_bytes(b.nsub));
-    std::memcpy(stage + i_info, info.data(), info.size() * sizeof(uint4));
-    std::memcpy(stage + i_freqs, t->freqs, 512);
-
+    // device buffers of the slot first, so each section's H2D can be issued
+    // as soon as the host workers have gathered it into pinned staging
+    // (gather of section k+1 overlaps the DMA of section k)
     Carve cv;
     const uint64_t o_freqs = cv.take(512), o_lut = cv.take(16384), o_mant = cv.take(b.mant_len + 16);
     const uint64_t o_scales = cv.take(std::max<uint64_t>(b.scales_len, 1));
@@ -1848,12 +1836,37 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     b.scratch_u32 = reinterpret_cast<uint32_t*>(m + o_scr);
     b.stream = static_cast<uint8_t*>(sl.stream.p);
     b.err = sl.err;
-    CK(cudaMemcpyAsync(b.stream, stage + i_stream, stream_len, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.mant, stage + i_mant, b.mant_len, cudaMemcpyHostToDevice, s));
-    if (b.scales_len) CK(cudaMemcpyAsync(b.scales, stage + i_scales, b.scales_len, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.index, stage + i_index, index_region_bytes(b.nsub), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.chunk_info, stage + i_info, b.nchunks * sizeof(uint4), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.freqs, stage + i_freqs, 512, cudaMemcpyHostToDevice, s));
+
+    // pinned staging: stream | mantissas | scales | index region | chunk table | table
+    Carve in;
+    const uint64_t i_stream = in.take(stream_len), i_mant = in.take(b.mant_len), i_scales = in.take(b.scales_len);
+    const uint64_t i_index = in.take(index_region_bytes(b.nsub)), i_info = in.take(b.nchunks * sizeof(uint4));
+    const uint64_t i_freqs = in.take(512);
+    if (int rc = hc.in.ensure(in.size)) return rc;
+    uint8_t* stage = static_cast<uint8_t*>(hc.in.p);
+    auto h2d = [&](void* dst, uint64_t at, uint64_t len) -> int {
+        if (len) CK(cudaMemcpyAsync(dst, stage + at, len, cudaMemcpyHostToDevice, s));
+        return NZGPU_OK;
+    };
+    std::vector<uint4> info;
+    gather_stream(t, stage + i_stream, info);
+    if (int rc = h2d(b.stream, i_stream, stream_len)) return rc;
+    constexpr uint64_t kInSlice = 32ull << 20;  // mantissa plane in slices: gather k+1 while k is in flight
+    for (uint64_t a0 = 0; a0 < b.mant_len; a0 += kInSlice) {
+        const uint64_t len = std::min(kInSlice, b.mant_len - a0);
+        par_memcpy(stage + i_mant + a0, t->mantissas + a0, len);
+        if (int rc = h2d(b.mant + a0, i_mant + a0, len)) return rc;
+    }
+    if (b.scales_len) {
+        par_memcpy(stage + i_scales, t->scales, b.scales_len);
+        if (int rc = h2d(b.scales, i_scales, b.scales_len)) return rc;
+    }
+    par_memcpy(stage + i_index, static_cast<const uint8_t*>(t->index) + sizeof(h), index_region_bytes(b.nsub));
+    if (int rc = h2d(b.index, i_index, index_region_bytes(b.nsub))) return rc;
+    std::memcpy(stage + i_info, info.data(), info.size() * sizeof(uint4));
+    std::memcpy(stage + i_freqs, t->freqs, 512);
+    if (int rc = h2d(b.chunk_info, i_info, b.nchunks * sizeof(uint4))) return rc;
+    if (int rc = h2d(b.freqs, i_freqs, 512)) return rc;
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
     if (!(b.flags & kFlagSingleSymbol)) {
