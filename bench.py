@@ -164,13 +164,23 @@ def run_gpu(args):
     import paper_2410_20650_b200 as nz
 
     world, rank, local = dist_setup()
+    # NZ_BENCH_BACKEND=gloo (test only): ranks may share a GPU (device =
+    # local rank mod visible GPUs) to exercise the N>1 harness on a 1-GPU box;
+    # the plumbing reductions then run on CPU tensors.  Default: NCCL, one GPU
+    # per rank.
+    backend = os.environ.get("NZ_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    red_dev = dev if backend == "nccl" else None  # where the timing reductions run
     stream = torch.cuda.current_stream()
 
     # ---- synthetic model: HF Llama init N(0, 0.02^2) weights, RMSNorm = 1.0.
@@ -354,7 +364,7 @@ def run_gpu(args):
 
     t_max, bytes_all = elapsed, bytes_algo  # bytes_all: algorithmic bytes of every rank's tensors
     if dist:
-        t_max, bytes_all = reduce_timing(dist, elapsed, bytes_algo, device=dev)
+        t_max, bytes_all = reduce_timing(dist, elapsed, bytes_algo, device=red_dev)
     value = bytes_all * args.steps / t_max / 1e9
     peak, peak_kind = load_peaks()
     achieved = bytes_algo * args.steps / kernel_time / 1e9  # per-launch bytes / launch time, aggregated
@@ -378,12 +388,12 @@ def run_gpu(args):
         verified, sample = verify_outputs(args, nz, torch, blobs, make_plan, run_plans, join, regen, stream, dev,
                                           rank)
         if dist:
-            vt = torch.tensor([verified], dtype=torch.int64, device=dev)
+            vt = torch.tensor([verified], dtype=torch.int64, device=red_dev)
             dist.all_reduce(vt, op=dist.ReduceOp.SUM)
             verified = int(vt.item())
 
     # ---- e2e through the reference-facing host API (host buffers in/out)
-    e2e = run_e2e(args, nz, blobs, torch, dist)
+    e2e = run_e2e(args, nz, blobs, torch, dist, red_dev)
     if dist:
         dist.barrier()
 
@@ -523,7 +533,7 @@ def verify_outputs(args, nz, torch, blobs, make_plan, run_plans, join, regen, st
     return checked, sample
 
 
-def run_e2e(args, nz, blobs, torch, dist=None):
+def run_e2e(args, nz, blobs, torch, dist=None, red_dev="cuda"):
     """Same metric through nzgpu_decompress_host_batch: compressed sections
     H2D from pinned host memory, GPU decode, bf16 D2H to pinned memory, every
     step.  Bounded to the first `--e2e-layers` layers to cap host memory."""
@@ -580,7 +590,7 @@ def run_e2e(args, nz, blobs, torch, dist=None):
     # every rank decodes its own tensors through its own PCIe link: whole-job
     # bytes over the slowest rank's time
     if dist:
-        t = torch.tensor([dt, float(algo), float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt, float(algo), float(h2d), float(d2h)], dtype=torch.float64, device=red_dev)
         dt_max = t[:1].clone()
         dist.all_reduce(dt_max, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)

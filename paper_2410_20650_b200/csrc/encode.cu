@@ -31,9 +31,6 @@
 #ifndef NZ_ENC_PF
 #define NZ_ENC_PF 1
 #endif
-#ifndef NZ_ENC_HI
-#define NZ_ENC_HI 1
-#endif
 
 namespace nzgpu {
 
@@ -111,26 +108,11 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
             out -= nb;
         }
         emitted += nb;
-#if NZ_ENC_HI
-        // ans.hpp:219 on the renormalised xr = x >> 8nb:
-        // (xr/f << 12) + xr%f + cum = xr + (xr/f)(4096 - f) + cum.  The
-        // quotient comes from the pre-renormalisation x, so its multiply starts
-        // in parallel with the compares: xr / f = x / (f 2^8nb), whose
-        // Granlund-Montgomery constants are f's multiplier m with l + 8nb, and
-        // for x < 2^31, (x m) >> (31 + l + 8nb) = umulhi(2x, m) >> (l + 8nb)
-        // -- a 32-bit high multiply and a 32-bit shift
-        // (tests/test_oracle.py::test_encoder_high_multiply_identity).
-        const uint32_t hi = __umulhi(x + x, e.rcp);
-        const uint32_t xr = x >> (8 * nb);
-        const uint32_t q = hi >> (e.pad - 31u + 8 * nb);
-        x = q * (kProbScale - e.freq) + (xr + e.cum);
-#else
         x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
         // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
         // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
         const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
         x = q * (kProbScale - e.freq) + (x + e.cum);
-#endif
         if (may_ckpt && ck_state && (i & kmask) == 0) {
             const uint64_t j = (begin + i) >> log2_interval;
             ck_state[j] = x;
