@@ -480,8 +480,8 @@ int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s, uint8_t*
 
 int compute_window(nzgpu_blob_s* b, cudaStream_t s) { return compute_windows(&b, 1, s); }
 
-// Persistent-kernel geometry of one tensor: one resident wave of CTAs (at
-// most one per unit), the units split evenly over them by the kernel.
+// Persistent-kernel geometry: 32-sub-range units, `upc` units per CTA so
+// that the grid is about one resident wave.
 struct PersistGeom {
     uint32_t ctas = 0, upc = 1;
 };
@@ -489,8 +489,8 @@ PersistGeom persist_geom(uint64_t units, int log2k, uint32_t win_cap) {
     PersistGeom g;
     if (!units) return g;
     const uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(log2k, win_cap));
-    g.ctas = (uint32_t)std::min<uint64_t>(units, resident);  // units split evenly over them in the kernel
-    g.upc = (uint32_t)ceil_div(units, g.ctas);
+    g.upc = (uint32_t)std::max<uint64_t>(1, ceil_div(units, resident));
+    g.ctas = (uint32_t)ceil_div(units, g.upc);
     return g;
 }
 
@@ -898,15 +898,11 @@ struct nzgpu_plan_s {
     }
 };
 
-// Persistent schedule of a plan: tensor t gets c_t CTAs and its units are
-// split evenly among them (the kernel gives CTA i units [i U/c, (i+1) U/c)),
-// so a CTA's load is floor or ceil of U_t / c_t.  The CTA budget is one
-// resident wave (a second wave of a few CTAs doubles the launch time); it is
-// handed out greedily to the tensor with the largest per-CTA load, which
-// minimises the largest load -- the launch's critical path.  A uniform
-// units-per-CTA split left the last CTA of every tensor short and the busiest
-// CTAs ~3 % above the average on a Llama-3-8B layer.  Returns the per-tensor
-// first-CTA prefix.
+// Persistent schedule of a plan: every CTA owns `upc` units of one tensor.
+// The per-tensor round-up must not push the CTA count past one resident wave
+// (a second wave of a few CTAs doubles the launch time), so upc is the
+// smallest value with sum_i ceil(units_i / upc) <= resident CTAs.  Returns
+// the per-tensor first-CTA prefix.
 std::vector<uint32_t> persist_geometry(nzgpu_plan_s* p) {
     std::vector<uint32_t> cta_prefix;
     uint64_t units = 0;
@@ -915,31 +911,40 @@ std::vector<uint32_t> persist_geometry(nzgpu_plan_s* p) {
     if (!units) return cta_prefix;
     uint64_t resident = std::max<uint32_t>(1, persist_resident_ctas(p->log2k, p->win_cap_unit));
     if (p->max_ctas) resident = std::min<uint64_t>(resident, p->max_ctas);
-    const size_t n = p->tunits.size();
-    // Tiny tensors (the trailing p->ntiny, e.g. a layer's norms) stay out of
-    // the one-wave budget: their few units run as extra CTAs that the SMs pick
-    // up in the launch's tail instead of each holding an SM for the whole
-    // launch.  Under an explicit cap (nzgpu_plan_set_max_ctas) every CTA
-    // counts: the caller promised the other SMs to concurrent work.
+    auto ctas_all = [&](uint64_t upc) {
+        uint64_t c = 0;
+        for (uint64_t u : p->tunits) c += ceil_div(u, upc);
+        return c;
+    };
+    // Tiny tensors (the trailing p->ntiny, e.g. a layer's norms) are left out
+    // of the one-wave budget: their few units run as extra CTAs that the SMs
+    // pick up in the launch's tail instead of each holding an SM for the
+    // whole launch.
+    const size_t nbig = p->tunits.size() - (size_t)p->ntiny;
+    auto ctas_big = [&](uint64_t upc) {
+        uint64_t c = 0;
+        for (size_t i = 0; i < nbig; ++i) c += ceil_div(p->tunits[i], upc);
+        return c;
+    };
+    // Under an explicit cap (nzgpu_plan_set_max_ctas) every CTA counts: the
+    // caller promised the other SMs to concurrent work.
     const bool tiny_outside = p->ntiny && !p->max_ctas;
-    const size_t nshare = tiny_outside ? n - (size_t)p->ntiny : n;
-    std::vector<uint64_t> c(n, 1);
-    auto load = [&](size_t i) { return ceil_div(p->tunits[i], c[i]); };
-    for (uint64_t used = nshare; used < resident; ++used) {
-        size_t best = n;
-        for (size_t i = 0; i < nshare; ++i)
-            if (c[i] < p->tunits[i] && (best == n || load(i) > load(best))) best = i;
-        if (best == n) break;  // every tensor has a CTA per unit
-        ++c[best];
+    auto ctas_for = [&](uint64_t upc) { return tiny_outside ? ctas_big(upc) : ctas_all(upc); };
+    uint64_t bunits = 0;
+    for (size_t i = 0; i < nbig; ++i) bunits += p->tunits[i];
+    const uint64_t umax = *std::max_element(p->tunits.begin(), p->tunits.end());
+    uint64_t lo = std::max<uint64_t>(1, ceil_div(tiny_outside ? bunits : units, resident)), hi = lo;
+    while (hi < umax && ctas_for(hi) > resident) hi *= 2;  // more tensors than CTAs: several waves
+    hi = std::max(lo, std::min(hi, umax));
+    while (lo < hi) {  // smallest upc in [lo, hi] that fits one wave
+        const uint64_t mid = (lo + hi) / 2;
+        if (ctas_for(mid) > resident) lo = mid + 1; else hi = mid;
     }
-    uint64_t max_load = 1;
-    for (size_t i = 0; i < nshare; ++i) max_load = std::max(max_load, load(i));
-    for (size_t i = nshare; i < n; ++i) c[i] = std::max<uint64_t>(1, ceil_div(p->tunits[i], max_load));
-    p->upc = (uint32_t)max_load;
+    p->upc = (uint32_t)lo;
     uint32_t ctas = 0;
-    for (size_t i = 0; i < n; ++i) {
+    for (uint64_t u : p->tunits) {
         cta_prefix.push_back(ctas);
-        ctas += (uint32_t)c[i];
+        ctas += (uint32_t)ceil_div(u, p->upc);
     }
     p->ctas = ctas;
     return cta_prefix;

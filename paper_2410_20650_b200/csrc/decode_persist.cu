@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     const uint32_t winstride = win_cap + 2 * K + 64;
 
     // ---- which tensor / unit range this CTA owns
-    uint32_t cta = blockIdx.x, nct = gridDim.x;  // this CTA's index among its tensor's nct CTAs
+    uint32_t cta = blockIdx.x;
     const DecodeDesc* dp = &one;
     if (descs) {
         int lo = 0, hi = ndesc - 1;
@@ -380,18 +380,12 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
             if (__ldg(cta_prefix + mid) <= cta) lo = mid; else hi = mid - 1;
         }
         dp = descs + lo;
-        const uint32_t first = __ldg(cta_prefix + lo);
-        nct = (lo + 1 < ndesc ? __ldg(cta_prefix + lo + 1) : gridDim.x) - first;
-        cta -= first;
+        cta -= __ldg(cta_prefix + lo);
     }
     const DecodeDesc d = *dp;
     const uint32_t nsub = (uint32_t)ceil_div(d.n, K);
     const uint32_t units = (nsub + 31) / 32;
-    // the tensor's units split evenly over its CTAs (persist_geometry); `upc`
-    // is the host's largest per-CTA load, kept for the launch signature
-    (void)upc;
-    const uint32_t ubeg = (uint32_t)((uint64_t)cta * units / nct);
-    const uint32_t uend = (uint32_t)((uint64_t)(cta + 1) * units / nct);
+    const uint32_t ubeg = cta * upc, uend = min(units, ubeg + upc);
     const bool single = d.flags & kFlagSingleSymbol;
     const bool fast_lossy = d.block_size >= 8 && !(d.flags & kFlagSlowLossy);
     // lossy, power-of-two B >= 32K/8: the unit's scale bytes come from one
