@@ -1268,7 +1268,12 @@ struct DevBuf {
 // H2D of tensor i+1, the decode of tensor i and the D2H of tensor i-1
 // overlap; buffers persist across calls (no per-call cudaMalloc).
 struct HostSlot {
-    cudaStream_t s = nullptr;
+    // s: table build, decode and D2H; s_in: the H2D of the compressed
+    // sections.  With one stream a slot's next H2D queued behind its previous
+    // D2H; now it waits only until the previous decode has read the inputs
+    // (in_free), and the decode waits for its own inputs (h2d_done).
+    cudaStream_t s = nullptr, s_in = nullptr;
+    cudaEvent_t in_free = nullptr, h2d_done = nullptr;
     DevBuf main, stream, out;
     uint32_t* err = nullptr;
     // Pinned staging for the host-built chunk table: a cudaMemcpyAsync from
@@ -1287,7 +1292,15 @@ struct HostSlot {
             if (info_h[i]) cudaFreeHost(info_h[i]);
             if (info_done[i]) cudaEventDestroy(info_done[i]);
         }
+        if (in_free) cudaEventDestroy(in_free);
+        if (h2d_done) cudaEventDestroy(h2d_done);
         if (s) cudaStreamDestroy(s);
+        if (s_in) cudaStreamDestroy(s_in);
+    }
+    int sync() {
+        if (s) CK(cudaStreamSynchronize(s));
+        if (s_in) CK(cudaStreamSynchronize(s_in));
+        return NZGPU_OK;
     }
     // Copy `info` into the next ring buffer; returns it (the caller issues the
     // H2D and then info_issued()).
@@ -1308,7 +1321,7 @@ struct HostSlot {
         return NZGPU_OK;
     }
     int info_issued() {
-        CK(cudaEventRecord(info_done[ring], s));
+        CK(cudaEventRecord(info_done[ring], s_in));
         info_pending[ring] = true;
         ring = (ring + 1) % kRing;
         return NZGPU_OK;
@@ -1456,6 +1469,12 @@ struct HostCtx {
     int init() {
         for (HostSlot& sl : slot) {
             if (!sl.s) CK(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking));
+            if (!sl.s_in) CK(cudaStreamCreateWithFlags(&sl.s_in, cudaStreamNonBlocking));
+            if (!sl.in_free) {
+                CK(cudaEventCreateWithFlags(&sl.in_free, cudaEventDisableTiming));
+                CK(cudaEventRecord(sl.in_free, sl.s));  // nothing to wait for yet
+            }
+            if (!sl.h2d_done) CK(cudaEventCreateWithFlags(&sl.h2d_done, cudaEventDisableTiming));
             if (!sl.err) CK(cudaMalloc(&sl.err, 64));
             for (auto& ev : sl.info_done)
                 if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1562,8 +1581,10 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     const uint64_t o_scales = cv.take(std::max<uint64_t>(b.scales_len, 1));
     const uint64_t o_info = cv.take(info.size() * sizeof(uint4));
     const uint64_t o_index = cv.take(index_region_bytes(b.nsub) + 16), o_scr = cv.take(64);
-    cudaStream_t s = sl.s;
+    cudaStream_t s = sl.s, si = sl.s_in;
     clk.lap(0);  // parse + validate
+    if (sl.main.cap < cv.size || sl.stream.cap < align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32)
+        if (int rc = sl.sync()) return rc;  // reallocation: both streams idle
     if (int rc = sl.main.ensure(cv.size, s)) return rc;
     if (int rc = sl.stream.ensure(align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32, s)) return rc;
     if (int rc = sl.out.ensure(align_up(t->n * 2, 16) + 16, s)) return rc;
@@ -1578,16 +1599,19 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     b.stream = static_cast<uint8_t*>(sl.stream.p);
     b.err = sl.err;
     clk.lap(1);  // buffers
-    CK(cudaMemcpyAsync(b.freqs, t->freqs, 512, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(b.stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
-    if (b.mant_len) CK(cudaMemcpyAsync(b.mant, t->mantissas, b.mant_len, cudaMemcpyHostToDevice, s));
-    if (b.scales_len) CK(cudaMemcpyAsync(b.scales, t->scales, b.scales_len, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamWaitEvent(si, sl.in_free, 0));  // the slot's previous decode has read its inputs
+    CK(cudaMemcpyAsync(b.freqs, t->freqs, 512, cudaMemcpyHostToDevice, si));
+    CK(cudaMemcpyAsync(b.stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, si));
+    if (b.mant_len) CK(cudaMemcpyAsync(b.mant, t->mantissas, b.mant_len, cudaMemcpyHostToDevice, si));
+    if (b.scales_len) CK(cudaMemcpyAsync(b.scales, t->scales, b.scales_len, cudaMemcpyHostToDevice, si));
     clk.lap(2);  // section copies
     uint4* info_pinned = nullptr;
     if (int rc = sl.stage_info(info, &info_pinned)) return rc;
-    CK(cudaMemcpyAsync(b.chunk_info, info_pinned, info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.chunk_info, info_pinned, info.size() * sizeof(uint4), cudaMemcpyHostToDevice, si));
     if (int rc = sl.info_issued()) return rc;
-    CK(cudaMemcpyAsync(b.index, ix, index_region_bytes(b.nsub), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(b.index, ix, index_region_bytes(b.nsub), cudaMemcpyHostToDevice, si));
+    CK(cudaEventRecord(sl.h2d_done, si));
+    CK(cudaStreamWaitEvent(s, sl.h2d_done, 0));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
     clk.lap(3);  // chunk table + index + LUT
@@ -1612,6 +1636,7 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
     }
     clk.lap(4);  // windows
     if (int rc = decode_blob(&b, static_cast<uint16_t*>(sl.out.p), s)) return rc;
+    CK(cudaEventRecord(sl.in_free, s));
     if (t->n) CK(cudaMemcpyAsync(host_out, sl.out.p, t->n * 2, cudaMemcpyDeviceToHost, s));
     clk.lap(5);  // decode + D2H issue
     return NZGPU_OK;
@@ -1653,13 +1678,14 @@ int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t
             if (!rc) CK(cudaStreamSynchronize(sl.s));  // b's buffers die here
         }
         if (rc) {
-            for (HostSlot& other : h.slot) cudaStreamSynchronize(other.s);
+            for (HostSlot& other : h.slot) other.sync();
             return rc;
         }
     }
     int rc = NZGPU_OK;
     const auto t1 = std::chrono::steady_clock::now();
     for (HostSlot& sl : h.slot) {
+        sl.sync();
         const int r = sync_status(sl.s, sl.err, true);
         if (!rc) rc = r;
     }
@@ -1791,7 +1817,7 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     if (int rc = hc.init()) return rc;
     HostSlot& sl = hc.slot[0];
     cudaStream_t s = sl.s;
-    CK(cudaStreamSynchronize(s));  // the slot's buffers and the pinned staging are free
+    if (int rc = sl.sync()) return rc;  // the slot's buffers and the pinned staging are free
     CK(cudaMemsetAsync(sl.err, 0, 64, s));
 
     nzgpu_blob_s& b = *new (std::nothrow) nzgpu_blob_s;  // descriptor over the slot's buffers
@@ -1917,8 +1943,7 @@ int nzgpu_trim_device_pool(void) {
 
 int nzgpu_host_release(void) {
     if (g_host) {
-        for (HostSlot& sl : g_host->slot)
-            if (sl.s) cudaStreamSynchronize(sl.s);
+        for (HostSlot& sl : g_host->slot) sl.sync();
         g_host.reset();
     }
     return NZGPU_OK;
