@@ -287,6 +287,10 @@ int nzgpu_blob_read_nzt(const uint8_t* data, uint64_t len, uint32_t interval, vo
  * sign[2] | exponent[256] | mantissa[128] (entropy.hpp:17-39). */
 int nzgpu_component_histogram(const uint16_t* d_values, uint64_t n, void* cuda_stream, uint64_t* counts);
 int nzgpu_component_histogram_host(const uint16_t* values, uint64_t n, uint64_t* counts);
+/* shannon_entropy (entropy.hpp:41-55): -sum p log2 p over the nonzero bins,
+ * summed in bin order (bit-identical to the reference); INVALID_ARGUMENT for
+ * an empty histogram. */
+int nzgpu_shannon_entropy(const uint64_t* counts, uint64_t bins, double* h);
 /* report_from_histogram (entropy.hpp:69-81): out5 = h_sign, h_exp, h_mant,
  * ideal_ratio, exponent_only_ratio. */
 int nzgpu_entropy_from_histogram(const uint64_t* counts, double* out5);

@@ -2397,6 +2397,16 @@ double shannon(const uint64_t* c, int bins) {
 }
 }  // namespace
 
+int nzgpu_shannon_entropy(const uint64_t* counts, uint64_t bins, double* h) {
+    if (!h || (bins && !counts)) return NZGPU_INVALID_ARGUMENT;
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < bins; ++i) total += counts[i];
+    if (bins == 0 || total == 0) return NZGPU_INVALID_ARGUMENT;  // "shannon_entropy: empty histogram"
+    if (bins > 0x7FFFFFFFull) return NZGPU_INVALID_ARGUMENT;
+    *h = shannon(counts, (int)bins);
+    return NZGPU_OK;
+}
+
 int nzgpu_entropy_from_histogram(const uint64_t* counts, double* out5) {
     if (!counts || !out5) return NZGPU_INVALID_ARGUMENT;
     if (counts[0] + counts[1] == 0) return NZGPU_INVALID_ARGUMENT;  // "entropy report: empty histogram"

@@ -204,6 +204,9 @@ __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a
 // kernel: the attribute is per (device, function), so a process that drives
 // several GPUs (one host thread per device) must set it on each of them.
 // Raising it concurrently from two threads is harmless (same call twice).
+#ifndef NZ_CARVEOUT
+#define NZ_CARVEOUT 0
+#endif
 struct SmemAttr {
     static constexpr int kMaxDevices = 64;
     std::atomic<uint32_t> configured[kMaxDevices] = {};
@@ -216,6 +219,11 @@ struct SmemAttr {
         if (smem <= configured[dev].load(std::memory_order_acquire)) return cudaSuccess;
         e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+#if NZ_CARVEOUT
+        // prefer the largest shared-memory carveout so a launch after a kernel
+        // that used the default split need not wait for the SMs to reconfigure
+        cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#endif
         uint32_t cur = configured[dev].load(std::memory_order_relaxed);
         while (cur < smem && !configured[dev].compare_exchange_weak(cur, smem, std::memory_order_acq_rel)) {
         }

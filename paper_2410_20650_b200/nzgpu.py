@@ -154,6 +154,7 @@ SIGNATURES = {
     "nzgpu_blob_decompress_host": (_i, [_vp, _vp]),
     "nzgpu_decompress_host_sections": (_i, [_p(HostSections), _vp]),
     "nzgpu_trim_device_pool": (_i, []),
+    "nzgpu_shannon_entropy": (_i, [_vp, _u64, _vp]),
     "nzgpu_plan_create": (_i, [_p(_vp), _p(_vp), _i, _p(_vp)]),
     "nzgpu_plan_launch": (_i, [_vp, _vp]),
     "nzgpu_plan_status": (_i, [_vp, _vp]),
