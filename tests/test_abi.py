@@ -73,3 +73,37 @@ def test_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 text = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert not re.search(r"import oracle|from oracle|liboracle|neuzip_oracle|libneuzip_ref", text), f
+
+
+def test_shannon_entropy_is_the_reference_sum():
+    """nzgpu_shannon_entropy (host math behind the drop-in's shannon_entropy,
+    entropy.hpp:41-55) sums -p log2 p over the nonzero bins in bin order with
+    p = c / total in double -- the reference's exact order, so the result is
+    bit-identical to the same loop in Python (both call libm's log2).  Empty
+    histograms are invalid_argument.  Host-only: runs without a GPU."""
+    import ctypes as C
+    import math
+
+    from paper_2410_20650_b200 import nzgpu as N
+
+    rng = np.random.default_rng(5)
+    for bins in (1, 2, 7, 128, 256, 1000):
+        for _ in range(5):
+            c = rng.integers(0, 1 << 40, size=bins).astype(np.uint64)
+            c[rng.random(bins) < 0.3] = 0
+            if c.sum() == 0:
+                c[0] = 1
+            h = C.c_double()
+            assert N.lib.nzgpu_shannon_entropy(c.ctypes.data, bins, C.byref(h)) == 0
+            n = float(int(c.sum()))
+            want = 0.0
+            for x in c.tolist():
+                if x:
+                    p = float(x) / n
+                    want -= p * math.log2(p)
+            want = 0.0 if want < 0.0 else want
+            assert h.value == want
+    h = C.c_double()
+    z = np.zeros(4, np.uint64)
+    assert N.lib.nzgpu_shannon_entropy(z.ctypes.data, 4, C.byref(h)) == N.INVALID_ARGUMENT
+    assert N.lib.nzgpu_shannon_entropy(None, 0, C.byref(h)) == N.INVALID_ARGUMENT
