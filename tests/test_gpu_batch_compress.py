@@ -135,3 +135,22 @@ def test_gpu_compress_batch_wide_launch_matches_oracle(nz, port):
         h = batch[i].to_host()
         assert h.stream == s and (h.freqs == f).all()
         assert torch.equal(batch[i].decompress().view(torch.int16), ts[i].view(torch.int16))
+
+
+def test_gpu_pool_reuse_and_trim(nz, port):
+    """Blob sections come from the library's stream-ordered pool: freed blob
+    memory is reused by the next compress (same results), and
+    nzgpu_trim_device_pool hands unused pool memory back to the driver."""
+    import torch
+
+    t = port.gaussian_bf16(31, 3 * 65536 + 5, 0.02)
+    d = torch.from_numpy(t.view(np.int16)).cuda()
+    first = nz.DeviceBlob.compress(d).to_host()
+    for _ in range(5):
+        b = nz.DeviceBlob.compress(d)
+        h = b.to_host()
+        assert h.stream == first.stream and h.index == first.index
+        b.free()
+    assert nz.nzgpu.lib.nzgpu_trim_device_pool() == 0
+    b = nz.DeviceBlob.compress(d)
+    assert (b.decompress().view(torch.int16).cpu().numpy().view(np.uint16) == t).all()
