@@ -222,13 +222,16 @@ cudaError_t pool_of(cudaMemPool_t* out) {
 // granules, which made a 10 GB model-batch arena cost ~0.7 s against
 // cudaMalloc's ~10 ms, while per-call cudaMalloc latency only matters for
 // the small blobs of per-tensor compresses.
+#ifndef NZ_POOL
+#define NZ_POOL 1
+#endif
 constexpr uint64_t kPoolMaxBytes = 256ull << 20;
 std::mutex g_pool_ptrs_mu;
 std::vector<void*> g_pool_ptrs;  // live pool allocations (small: one per pooled blob section)
 
 cudaError_t dev_alloc(void** p, uint64_t bytes, cudaStream_t s) {
     bytes = std::max<uint64_t>(bytes, 256);
-    if (bytes >= kPoolMaxBytes) return cudaMalloc(p, bytes);
+    if (!NZ_POOL || bytes >= kPoolMaxBytes) return cudaMalloc(p, bytes);
     cudaMemPool_t pool;
     cudaError_t e = pool_of(&pool);
     if (e != cudaSuccess) return e;
