@@ -36,15 +36,24 @@ namespace {
 #ifndef NZ_HALVES_UNROLL
 #define NZ_HALVES_UNROLL 2
 #endif
-constexpr int kHalvesUnroll = NZ_HALVES_UNROLL;  // K = 128: unrolled halves (code size vs registers)
+constexpr int kHalvesUnroll = NZ_HALVES_UNROLL;  // K = 128 in halves: unrolled halves (code size vs registers)
+#ifndef NZ_K128_SPLIT
+#define NZ_K128_SPLIT 0  // K = 128: 1 = two 64-symbol halves at NZ_PWARPS warps, 0 = one pass at NZ_K128_WARPS
+#endif
+#ifndef NZ_K128_WARPS
+#define NZ_K128_WARPS 24  // a K = 128 unit's exponent tile is twice K = 64's: fewer warps fit
+#endif
 constexpr int kPWarps = NZ_PWARPS;
+// warps per persistent CTA, and the log2 of the symbols per exponent-tile row
+__host__ __device__ constexpr int p_warps(int log2k) { return (log2k == 7 && !NZ_K128_SPLIT) ? NZ_K128_WARPS : NZ_PWARPS; }
+__host__ __device__ constexpr int tile_log2(int log2k) { return (log2k == 7 && NZ_K128_SPLIT) ? 6 : log2k; }
 constexpr int kPUnroll = NZ_PUNROLL;
 constexpr int kPThreads = kPWarps * 32;
 constexpr uint32_t kPHeader = 128;  // LUT mbarrier
 
 // exponent tile of a warp: 32 rows of (at most) 64 symbols (K = 128 is merged
 // in two halves through the same tile)
-__host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(log2k > 6 ? 6 : log2k); }
+__host__ __device__ constexpr uint32_t unit_words(int log2k) { return 32 * exps_row_words(tile_log2(log2k)); }
 
 // Per-warp region: its 2 mbarriers (16 B), the exponent tile (32 padded
 // rows) and 2 payload windows -- every per-warp address is the region base
@@ -56,7 +65,7 @@ __host__ __device__ constexpr uint32_t warp_region(int log2k, uint32_t win_cap) 
 }
 
 __host__ __device__ constexpr uint32_t persist_smem(int log2k, uint32_t win_cap) {
-    return kPHeader + kLutBytes + kPWarps * warp_region(log2k, win_cap);
+    return kPHeader + kLutBytes + p_warps(log2k) * warp_region(log2k, win_cap);
 }
 
 template <int P>
@@ -342,7 +351,7 @@ __device__ __forceinline__ LaneJob lane_job(const DecodeDesc& d, uint32_t j, uin
 }
 
 template <int LOG2K, int P>
-__global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(const DecodeDesc* __restrict__ descs,
+__global__ void __launch_bounds__(p_warps(LOG2K) * 32, NZ_PMINB) decode_persist_kernel(const DecodeDesc* __restrict__ descs,
                                                                       int ndesc,
                                                                       const uint32_t* __restrict__ cta_prefix,
                                                                       DecodeDesc one, uint32_t upc,
@@ -353,9 +362,10 @@ __global__ void __launch_bounds__(kPThreads, NZ_PMINB) decode_persist_kernel(con
     // ANS state carry over), so shared memory and the merge are those of K = 64
     // while the per-unit work (index records, window TMA, hand-out) is spread
     // over twice the symbols.
-    constexpr int KH = K > 64 ? 64 : K;
+    constexpr int KH = 1 << tile_log2(LOG2K);
     constexpr int HALVES = K / KH;
-    constexpr uint32_t RW = exps_row_words(LOG2K > 6 ? 6 : LOG2K);
+    constexpr int kPWarps = p_warps(LOG2K);  // shadows the default for this K
+    constexpr uint32_t RW = exps_row_words(tile_log2(LOG2K));
     constexpr int G = KH / 8;  // 8-element merge groups per lane per half
     using HB = typename HalfBits<P>::T;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -960,7 +970,8 @@ static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* 
     static SmemAttr attr;  // per device: one process may drive several GPUs
     if (cudaError_t e = attr.ensure((const void*)decode_persist_kernel<LOG2K, P>, smem)) return e;
     const MulConsts mc{1u};
-    decode_persist_kernel<LOG2K, P><<<ctas, kPThreads, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap, mc);
+    decode_persist_kernel<LOG2K, P><<<ctas, p_warps(LOG2K) * 32, smem, s>>>(descs, ndesc, cta_prefix, one, upc, win_cap,
+                                                                          mc);
     return cudaGetLastError();
 }
 
@@ -1006,7 +1017,7 @@ uint32_t persist_resident_ctas(int log2k, uint32_t win_cap) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     uint32_t per_sm = smem ? (uint32_t)per_sm_smem / (smem + 1024) : 1;
-    const uint32_t by_threads = 2048u / (uint32_t)kPThreads;
+    const uint32_t by_threads = 2048u / (uint32_t)(p_warps(log2k) * 32);
     if (per_sm > by_threads) per_sm = by_threads;
     if (per_sm < 1) per_sm = 1;
     return (uint32_t)sms * per_sm;
