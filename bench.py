@@ -756,7 +756,7 @@ def main():
     ap.add_argument("--block", type=int, default=512)
     ap.add_argument("--interval", type=int, default=0, help="checkpoint stride K (0 = auto)")
     ap.add_argument("--seed", type=int, default=42)
-    ap.add_argument("--e2e-layers", type=int, default=4)
+    ap.add_argument("--e2e-layers", type=int, default=8)
     ap.add_argument("--dropin", type=int, default=1, help="also time the C++ drop-in host API (rank 0, 8B lossless)")
     ap.add_argument("--cpu-tensors", type=int, default=7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
