@@ -85,11 +85,10 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     // x -> compare -> select -> IMAD.WIDE -> shift -> IMAD -> x; the byte
     // queue and the checkpoint record hang off it.
     auto step = [&](const EncSym& e, uint32_t i, bool may_ckpt) {
-        bad |= e.lim1 == 0;  // ans.hpp:210-212 (f == 0)
-        // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice;
-        // the second test, (x >> 8) >= f << 19, is x >= f << 27, precomputed
-        // (lim2) so both compares read x directly and leave the state chain
-        const bool n1 = x >= e.lim1, n2 = x >= e.lim2;
+        const uint32_t limit = e.freq << 19;
+        bad |= e.freq == 0;  // ans.hpp:210-212
+        // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
+        const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
         const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
         if constexpr (QUEUE) {
             qlo = __funnelshift_r(qlo, qhi, 8 * nb);
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
         // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
         // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
         const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
-        x = q * e.kmf + (x + e.cum);
+        x = q * (kProbScale - e.freq) + (x + e.cum);
         if (may_ckpt && ck_state && (i & kmask) == 0) {
             const uint64_t j = (begin + i) >> log2_interval;
             ck_state[j] = x;

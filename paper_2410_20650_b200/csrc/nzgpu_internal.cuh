@@ -64,12 +64,8 @@ constexpr uint32_t kFlagSlowLossy = kFlagHas255 | kFlagWideScale;
 struct EncSym {
     uint32_t freq;
     uint32_t cum;
-    uint32_t rcp;   // m = ceil(2^(31+l) / f), l = ceil(log2 f)
-    uint32_t pad;   // shift 31 + l: x / f = (x * m) >> shift for x < 2^31
-    uint32_t lim1;  // f << 19: the first renormalisation byte is due when x >= lim1
-    uint32_t lim2;  // f << 27 (f < 32; else never): the second one, compared with x directly
-    uint32_t kmf;   // 4096 - f
-    uint32_t spare;
+    uint32_t rcp;  // m = ceil(2^(31+l) / f), l = ceil(log2 f)
+    uint32_t pad;  // shift 31 + l: x / f = (x * m) >> shift for x < 2^31
 };
 
 // One tensor of a (batched) encode launch: K3 encodes its chunks into

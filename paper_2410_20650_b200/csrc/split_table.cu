@@ -329,10 +329,6 @@ __device__ __forceinline__ void build_table_body(const unsigned long long* __res
         while ((1u << l) < (uint32_t)f) ++l;
         e.rcp = f ? (uint32_t)(((1ull << (31 + l)) + (uint64_t)f - 1) / (uint64_t)f) : 0u;
         e.pad = 31 + l;
-        e.lim1 = (uint32_t)f << 19;
-        e.lim2 = f < 32 ? (uint32_t)f << 27 : 0xFFFFFFFFu;  // x < 2^31 never reaches it otherwise
-        e.kmf = kProbScale - (uint32_t)f;
-        e.spare = 0;
         enc[s] = e;
     }
     if (s == 255 && f > 0) atomicOr(info, kFlagHas255);
