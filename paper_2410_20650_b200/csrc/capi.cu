@@ -41,6 +41,8 @@ __global__ void gather_u32_kernel(const uint32_t* const*, uint32_t*, int);
 __global__ void stream_copy_kernel(const uint8_t*, uint64_t, const uint4*, uint8_t*);
 __global__ void lossy_normalize_kernel(const uint16_t*, uint64_t, int, uint32_t, uint8_t*, uint8_t*, uint8_t*,
                                        uint32_t*);
+cudaError_t launch_lossy_prep(const uint16_t*, uint64_t, int, uint32_t, uint8_t*, uint8_t*, uint8_t*, uint8_t*,
+                              uint64_t, unsigned long long*, uint32_t*, cudaStream_t);
 __global__ void pack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*, uint64_t);
 __global__ void lossy_roundtrip_kernel(const uint16_t*, const uint8_t*, uint64_t, int, uint16_t*);
 __global__ void unpack_items_kernel(const uint8_t*, uint64_t, int, uint8_t*);
@@ -778,10 +780,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
             CK(launch_split_hist(vs[i], n, exps, b->mant, counts, s));
         } else {
             uint8_t* items = tmp + L.to[i].items;
-            lossy_normalize_kernel<<<grid_for(ceil_div(n, block) * 32, 256), 256, 0, s>>>(
-                vs[i], n, precision, block, b->scales, exps, items, b->err);
-            byte_hist_kernel<<<grid_for(n / 16 + 1, 256), 256, 0, s>>>(exps, n, counts);
-            pack_items_kernel<<<grid_for(b->mant_len, 256), 256, 0, s>>>(items, n, precision, b->mant, b->mant_len);
+            CK(launch_lossy_prep(vs[i], n, precision, block, b->scales, exps, items, b->mant, b->mant_len, counts,
+                                 b->err, s));
         }
         tables[i] = TableTask{counts, b->freqs, enc, b->lut, b->scratch_u32};
         if (count == 1) build_table_kernel<<<1, 256, 0, s>>>(counts, nullptr, b->freqs, enc, b->lut, b->scratch_u32);

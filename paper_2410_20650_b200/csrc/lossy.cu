@@ -10,6 +10,8 @@
 // rounded to bf16 (RNE), its mantissa rounded to k bits (RNE with carry into
 // the exponent; exponent 254 truncates instead).  Exponents go to the ANS
 // coder, (sign, k-bit mantissa) items to the packer.
+#include <algorithm>
+
 #include "nzgpu_internal.cuh"
 
 namespace nzgpu {
@@ -110,6 +112,157 @@ __global__ void unpack_items_kernel(const uint8_t* __restrict__ packed, uint64_t
         const uint32_t shift = 8 - w - (uint32_t)(bit & 7);
         items[i] = (uint8_t)((packed[bit >> 3] >> shift) & ((1u << w) - 1u));
     }
+}
+
+// K6 fused: normalisation + exponent histogram + item packing for the full
+// blocks of a tensor whose block size is B = 32*E (E in {8, 16, 32, 64}).
+// One warp per block; lane l holds elements q*256 + 8l .. 8l+7 of the block
+// (q < E/8), so every load and store is warp-coalesced.  The bf16 block is
+// read once (the three-kernel path reads it twice and round-trips an item
+// plane through HBM).  Per element: 2 B read, 1 B exponent + (k+1)/8 B
+// packed written.  Exponents are counted in lane-private shared counters.
+constexpr int kFusedLoads = 8;  // uint4 loads in flight per lane
+
+template <int E, int K>
+__global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const uint16_t* __restrict__ v,
+                                                                          uint64_t nfull,
+                                                                          uint8_t* __restrict__ scales,
+                                                                          uint8_t* __restrict__ exps,
+                                                                          uint8_t* __restrict__ packed,
+                                                                          unsigned long long* __restrict__ counts,
+                                                                          uint32_t* __restrict__ err) {
+    constexpr int Q = E / 8;                                      // uint4 per lane per block
+    constexpr int U = kFusedLoads / Q > 0 ? kFusedLoads / Q : 1;  // blocks per warp iteration
+    constexpr uint64_t B = 32 * E;
+    constexpr uint32_t W = K + 1;
+    extern __shared__ uint32_t lh[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < (int)(kLaneHistSmem / 4); i += blockDim.x) lh[i] = 0;
+    __syncthreads();
+    uint16_t* h = reinterpret_cast<uint16_t*>(lh) + warp * 256 * 32 + lane;
+    const uint64_t nw = (uint64_t)gridDim.x * kLaneHistWarps;
+    for (uint64_t g = blockIdx.x * (uint64_t)kLaneHistWarps + warp; g * U < nfull; g += nw) {
+        uint4 w[U][Q];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t b = g * U + u;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (b < nfull) w[u][q] = __ldcs(reinterpret_cast<const uint4*>(v + b * B) + q * 32 + lane);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t b = g * U + u;
+            if (b >= nfull) break;
+            // argmax of magnitude bits, first index on ties (tensorstore.hpp:168-174)
+            uint32_t key = 0;
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const uint32_t in[4] = {w[u][q].x, w[u][q].y, w[u][q].z, w[u][q].w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t bits = (in[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+                    bad |= (bits & 0x7F80u) == 0x7F80u;
+                    const uint32_t idx = q * 256 + lane * 8 + j;
+                    key = max(key, ((bits & 0x7FFFu) << 16) | (0xFFFFu - idx));
+                }
+            }
+            key = __reduce_max_sync(0xFFFFFFFFu, key);
+            if (__any_sync(0xFFFFFFFFu, bad)) {
+                if (lane == 0) atomicOr(err, kErrNonFinite);
+                continue;
+            }
+            const uint32_t scale = (key >> 16) & 0x7Fu;
+            if (lane == 0) scales[b] = (uint8_t)scale;
+            const float c = lossy_coef(scale);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const uint32_t in[4] = {w[u][q].x, w[u][q].y, w[u][q].z, w[u][q].w};
+                uint32_t e8[2] = {0, 0}, acc = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t e, item;
+                    lossy_normalize((in[j >> 1] >> (16 * (j & 1))) & 0xFFFFu, c, K, e, item);
+                    h[e * 32] += 1;
+                    e8[j >> 2] |= e << (8 * (j & 3));
+                    acc = (acc << W) | item;  // pack_signed_mantissas: first item in the high bits
+                }
+                const uint64_t i0 = b * B + q * 256 + lane * 8;
+                __stcs(reinterpret_cast<uint2*>(exps + i0), make_uint2(e8[0], e8[1]));
+                if constexpr (K == 3) {
+                    __stcs(reinterpret_cast<uint32_t*>(packed + i0 / 2), __byte_perm(acc, 0, 0x0123));
+                } else if constexpr (K == 1) {
+                    *reinterpret_cast<uint16_t*>(packed + i0 / 4) = (uint16_t)__byte_perm(acc, 0, 0x0001);
+                } else {
+                    packed[i0 / 8] = (uint8_t)acc;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    lane_hist_flush(lh, counts);
+}
+
+template <int E, int K>
+static cudaError_t launch_fused(const uint16_t* v, uint64_t nfull, uint8_t* scales, uint8_t* exps, uint8_t* packed,
+                                unsigned long long* counts, uint32_t* err, cudaStream_t s) {
+    static SmemAttr attr;
+    if (cudaError_t e = attr.ensure((const void*)lossy_fused_kernel<E, K>, kLaneHistSmem)) return e;
+    constexpr uint64_t U = kFusedLoads / (E / 8) > 0 ? kFusedLoads / (E / 8) : 1;
+    const uint64_t per_warp = kLaneMax / E;  // blocks a warp may count (16-bit lane counters)
+    const uint64_t need = ceil_div(ceil_div(nfull, per_warp), kLaneHistWarps);
+    const uint64_t want = ceil_div(ceil_div(nfull, U), kLaneHistWarps);
+    const uint64_t grid = std::max<uint64_t>(need, std::min<uint64_t>(want, 148 * 3));
+    lossy_fused_kernel<E, K><<<(unsigned)grid, kLaneHistWarps * 32, kLaneHistSmem, s>>>(v, nfull, scales, exps, packed,
+                                                                                     counts, err);
+    return cudaGetLastError();
+}
+
+template <int E>
+static cudaError_t launch_fused_k(int k, const uint16_t* v, uint64_t nfull, uint8_t* scales, uint8_t* exps,
+                                  uint8_t* packed, unsigned long long* counts, uint32_t* err, cudaStream_t s) {
+    switch (k) {
+        case 0: return launch_fused<E, 0>(v, nfull, scales, exps, packed, counts, err, s);
+        case 1: return launch_fused<E, 1>(v, nfull, scales, exps, packed, counts, err, s);
+        default: return launch_fused<E, 3>(v, nfull, scales, exps, packed, counts, err, s);
+    }
+}
+
+__global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
+
+#ifndef NZ_LOSSY_FUSED
+#define NZ_LOSSY_FUSED 1
+#endif
+
+// K6 launcher: scales, exponent plane + histogram, packed (sign, mantissa)
+// items.  Full blocks of B in {256, 512, 1024, 2048} take the fused kernel;
+// the remaining blocks (a ragged last block, or every block of another B)
+// take normalise -> histogram -> pack through the `items` scratch plane.
+cudaError_t launch_lossy_prep(const uint16_t* v, uint64_t n, int k, uint32_t block, uint8_t* scales, uint8_t* exps,
+                              uint8_t* items, uint8_t* packed, uint64_t packed_len, unsigned long long* counts,
+                              uint32_t* err, cudaStream_t s) {
+    uint64_t nfull = 0;
+    if (NZ_LOSSY_FUSED && (block == 256 || block == 512 || block == 1024 || block == 2048) && (k == 0 || k == 1 || k == 3)) {
+        nfull = n / block;
+        if (nfull) {
+            const int E = (int)(block / 32);
+            cudaError_t e = E == 8    ? launch_fused_k<8>(k, v, nfull, scales, exps, packed, counts, err, s)
+                            : E == 16 ? launch_fused_k<16>(k, v, nfull, scales, exps, packed, counts, err, s)
+                            : E == 32 ? launch_fused_k<32>(k, v, nfull, scales, exps, packed, counts, err, s)
+                                      : launch_fused_k<64>(k, v, nfull, scales, exps, packed, counts, err, s);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    const uint64_t begin = nfull * block;  // a multiple of 256: byte- and 16-byte aligned planes
+    if (begin == n) return cudaSuccess;
+    const uint64_t rest = n - begin, pbegin = begin * (uint64_t)(k + 1) / 8;
+    auto grid = [](uint64_t work) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(work, 256), 148 * 16)); };
+    lossy_normalize_kernel<<<grid(ceil_div(rest, block) * 32), 256, 0, s>>>(v + begin, rest, k, block, scales + nfull,
+                                                                           exps + begin, items, err);
+    byte_hist_kernel<<<grid(rest / 16 + 1), 256, 0, s>>>(exps + begin, rest, counts);
+    pack_items_kernel<<<grid(packed_len - pbegin), 256, 0, s>>>(items, rest, k, packed + pbegin, packed_len - pbegin);
+    return cudaGetLastError();
 }
 
 // Elementwise lossy round trip under an explicit scale byte (the exhaustive

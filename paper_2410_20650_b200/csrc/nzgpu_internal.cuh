@@ -182,6 +182,30 @@ __device__ __forceinline__ uint16_t bf16_from_float(float f) {
 
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// Lane-private 16-bit exponent counters in shared memory (K1 and the fused
+// lossy kernel): counter (warp, bin, lane) at u16 index (warp*256 + bin)*32 +
+// lane, so a warp's 32 increments touch at most two lanes per bank and need
+// no match/atomic.  A lane counts at most kLaneMax elements (grids are sized
+// for it), so 16 bits cannot overflow.
+constexpr int kLaneHistWarps = 4;
+constexpr uint32_t kLaneHistSmem = kLaneHistWarps * 256 * 32 * 2;  // 64 KiB
+constexpr uint64_t kLaneMax = 65000;
+
+// Sum every warp's and lane's counters of the CTA into the global histogram
+// (call after a __syncthreads that follows the last increment).
+__device__ __forceinline__ void lane_hist_flush(const uint32_t* lh, unsigned long long* counts) {
+    for (int bin = threadIdx.x; bin < 256; bin += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int wp = 0; wp < kLaneHistWarps; ++wp) {
+            const uint32_t* row = lh + (wp * 256 + bin) * 16;  // 32 u16 counters = 16 words
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum += (row[(k + bin) & 15] & 0xFFFFu) + (row[(k + bin) & 15] >> 16);
+        }
+        if (sum) atomicAdd(counts + bin, (unsigned long long)sum);
+    }
+}
+
 // Bounds assertions of the checked build (NZ_CHECKS=1, libnzgpu_checks.so;
 // tools/checked_suite.sh runs the GPU tests against it): a violated bound
 // traps the kernel, so the launch fails loudly instead of touching memory

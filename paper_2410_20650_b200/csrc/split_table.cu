@@ -87,14 +87,7 @@ __global__ void __launch_bounds__(256) split_hist_kernel(const uint16_t* __restr
 }
 
 // K1 with per-lane private 16-bit counters in shared memory instead of
-// warp-aggregated atomics: counter (warp, bin, lane) at u16 index
-// (warp*256 + bin)*32 + lane, so a warp's 32 increments touch at most two
-// lanes per bank (<= 2-way conflicts) and need no match/atomic.  A lane
-// counts at most kLaneMax elements (the grid is sized for it), so 16 bits
-// cannot overflow.
-constexpr int kLaneHistWarps = 4;
-constexpr uint32_t kLaneHistSmem = kLaneHistWarps * 256 * 32 * 2;  // 64 KiB
-constexpr uint64_t kLaneMax = 65000;
+// warp-aggregated atomics (layout: kLaneHistWarps, nzgpu_internal.cuh).
 constexpr int kLaneUnroll = 8;
 
 __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(const uint16_t* __restrict__ v,
@@ -140,16 +133,7 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(co
         h[e * 32] += 1;
     }
     __syncthreads();
-    for (int bin = tid; bin < 256; bin += blockDim.x) {
-        uint32_t sum = 0;
-#pragma unroll
-        for (int wp = 0; wp < kLaneHistWarps; ++wp) {
-            const uint32_t* row = lh + (wp * 256 + bin) * 16;  // 32 u16 counters = 16 words
-#pragma unroll
-            for (int k = 0; k < 16; ++k) sum += (row[(k + bin) & 15] & 0xFFFFu) + (row[(k + bin) & 15] >> 16);
-        }
-        if (sum) atomicAdd(counts + bin, (unsigned long long)sum);
-    }
+    lane_hist_flush(lh, counts);
 }
 
 #ifndef NZ_HIST_LANE

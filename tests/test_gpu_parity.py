@@ -185,6 +185,37 @@ def test_gpu_lossy_pow2_blocks_match_oracle(nz, port, k, block):
         assert (nz.decompress_lossy(blob) == want).all()
 
 
+@pytest.mark.parametrize("block", [256, 512, 1024, 2048])
+@pytest.mark.parametrize("k", [0, 1, 3])
+def test_gpu_lossy_fused_blocks_random_patterns(nz, port, k, block):
+    """The fused normalise/histogram/pack kernel (full blocks of B = 256 ..
+    2048) on arbitrary finite bit patterns: subnormals, exponent-254 carries,
+    both signs, maxima anywhere in the block, plus a ragged last block that
+    takes the three-kernel path."""
+    rng = np.random.default_rng(1000 * k + block)
+    n = 4 * 2048 + 300
+    v = rng.integers(0, 1 << 16, n, dtype=np.uint32).astype(np.uint16)
+    v[(v & 0x7F80) == 0x7F80] ^= 0x0080  # exponent 255 -> 254
+    v[:block] = (v[:block] & 0x807F) | 0x7F00  # a block of exponent-254 values
+    blob = nz.compress_lossy(v, k, block)
+    f, sc, st, pk = port.compress_lossy(v, k, block)
+    assert (blob.scales == sc).all() and (blob.signmant == pk).all()
+    assert (blob.freqs == f).all() and blob.stream == st
+    assert (nz.decompress_lossy(blob) == port.decompress_lossy(f, sc, st, pk, k, block, n)).all()
+
+
+@pytest.mark.parametrize("block", [256, 2048])
+def test_gpu_lossy_fused_rejects_nonfinite(nz, port, block):
+    """A NaN or Inf inside a full block fails the whole call
+    (tensorstore.hpp:153-157), as it does in a ragged block."""
+    v = port.gaussian_bf16(5, 3 * block, 0.02)
+    for bad in (0x7FC1, 0xFF80, 0x7F80):
+        w = v.copy()
+        w[block + 77] = bad
+        with pytest.raises(nz.NonFiniteError):
+            nz.compress_lossy(w, 3, block)
+
+
 @pytest.mark.parametrize("k", [0, 1, 3])
 def test_gpu_lossy_elementwise_exhaustive(nz, port, k):
     """Every finite bf16 pattern x every scale byte (65,280 x 256 pairs)
