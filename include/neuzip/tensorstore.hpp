@@ -12,8 +12,10 @@
 // streams) decode too -- the GPU rebuilds it with a full sequential
 // validation first.
 
+#include <algorithm>
 #include <cstdint>
 #include <istream>
+#include <thread>
 #include <ostream>
 #include <span>
 #include <string>
@@ -25,7 +27,19 @@
 #include "neuzip/crc32.hpp"
 #include "neuzip/errors.hpp"
 
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
+
 namespace neuzip {
+
+#if defined(__linux__)
+#ifdef MADV_POPULATE_WRITE
+constexpr int kMadvPopulateWrite = MADV_POPULATE_WRITE;
+#else
+constexpr int kMadvPopulateWrite = 23;  // Linux 5.14+; older kernels return EINVAL
+#endif
+#endif
 
 constexpr std::uint32_t kDefaultBlockSize = 512;  // tensorstore.hpp:35
 constexpr int kLosslessPrecision = 7;             // tensorstore.hpp:36
@@ -142,14 +156,44 @@ inline void gpu_decompress_into(const TensorMeta& meta, const AnsStream& stream,
     check(nzgpu_decompress_host_sections(&t, reinterpret_cast<std::uint16_t*>(out)), "decompress");
 }
 
+// Fault the pages of a fresh output buffer in before it is value-initialised:
+// as transparent huge pages where the kernel allows it (MADV_HUGEPAGE), and
+// populated by several threads (MADV_POPULATE_WRITE) instead of one thread
+// taking a 4 KiB fault per page inside the vector's zero-fill.  Best effort:
+// any refusal leaves the ordinary fault path.
+inline void prefault_output(void* p, std::size_t bytes) {
+#if defined(__linux__)
+    constexpr std::size_t kHuge = 2u << 20;
+    if (bytes < 16 * kHuge) return;
+    const auto lo = reinterpret_cast<std::uintptr_t>(p), hi = lo + bytes;
+    const std::uintptr_t h0 = (lo + kHuge - 1) & ~(kHuge - 1), h1 = hi & ~(kHuge - 1);
+    if (h1 > h0) ::madvise(reinterpret_cast<void*>(h0), h1 - h0, MADV_HUGEPAGE);
+    const std::uintptr_t p0 = lo & ~std::uintptr_t(4095);
+    const unsigned workers = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const std::size_t step = (((hi - p0) + workers - 1) / workers + kHuge - 1) & ~(kHuge - 1);
+    std::vector<std::thread> ts;
+    for (unsigned w = 0; w < workers && p0 + w * step < hi; ++w) {
+        const std::uintptr_t a = p0 + w * step, b = std::min<std::uintptr_t>(hi, a + step);
+        ts.emplace_back([a, b] { ::madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite); });
+    }
+    for (std::thread& t : ts) t.join();
+#else
+    (void)p;
+    (void)bytes;
+#endif
+}
+
 inline std::vector<Bf16> gpu_decompress(const TensorMeta& meta, const AnsStream& stream,
                                         const std::vector<std::uint8_t>& mant, int precision, std::uint32_t block,
                                         const std::vector<std::uint8_t>* scales,
                                         const std::vector<std::uint8_t>& index) {
-    // A fresh vector is value-initialised (and its pages first touched) by
-    // one thread before the decode writes it: for large tensors that, not the
-    // GPU or PCIe, bounds this signature (the *_into overloads reuse memory).
-    std::vector<Bf16> out(meta.element_count());
+    // A fresh vector is value-initialised before the decode writes it; its
+    // pages are faulted in first, in parallel (prefault_output).  The
+    // *_into overloads reuse memory and skip both.
+    std::vector<Bf16> out;
+    out.reserve(meta.element_count());
+    prefault_output(out.data(), meta.element_count() * sizeof(Bf16));
+    out.resize(meta.element_count());
     gpu_decompress_into(meta, stream, mant, precision, block, scales, index, out.data());
     return out;
 }

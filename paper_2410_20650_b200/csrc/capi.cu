@@ -552,6 +552,33 @@ int decode_blob(nzgpu_blob_s* b, uint16_t* d_out, cudaStream_t s) {
     return NZGPU_OK;
 }
 
+// Decode elements [a, a + len) of a uniform-framing blob, a and len whole
+// chunks and warp units (and lossy blocks): the same kernels over a
+// descriptor whose index, chunk table, planes and output start at a.
+int decode_range(const nzgpu_blob_s* b, uint16_t* d_out, uint64_t a, uint64_t len, cudaStream_t s) {
+    if (len == 0) return NZGPU_OK;
+    DecodeDesc d = b->desc(d_out + a);
+    const uint64_t sub0 = a >> b->log2k, nsub = ceil_div(len, b->interval);
+    d.n = len;
+    d.ck_state += sub0;
+    d.ck_off += sub0;
+    d.ck_base += sub0 / 32;
+    d.chunk_info += a / b->chunk_syms;
+    if (b->precision == 7) {
+        d.mant += a;
+    } else {
+        d.mant += a * (uint64_t)(b->precision + 1) / 8;
+        d.scales += a / b->block;
+    }
+    if (use_persist() && persist_fits(b->log2k, b->max_window_unit)) {
+        const PersistGeom g = persist_geom(ceil_div(nsub, 32), b->log2k, b->max_window_unit);
+        CK(launch_decode_persist(b->log2k, b->precision, nullptr, 0, nullptr, d, g.ctas, g.upc, b->max_window_unit, s));
+    } else {
+        CK(launch_decode(b->log2k, b->precision, nullptr, 0, nullptr, d, decode_tiles_for(nsub), b->max_window, s));
+    }
+    return NZGPU_OK;
+}
+
 // Fill a blob from host sections (reference formats).
 int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, cudaStream_t s) {
     if (!t || !valid_precision(t->precision)) return NZGPU_INVALID_ARGUMENT;
@@ -1468,15 +1495,17 @@ private:
     bool stop_ = false;
 };
 
-// memcpy split over the host pool above ~4 MB.
+// memcpy split over the host pool above ~512 KB (pieces of >= 256 KB: the
+// pipelined host decode copies a few MB per slice, and one thread moves
+// only ~14 GB/s).
 void par_memcpy(void* dst, const void* src, uint64_t bytes) {
-    constexpr uint64_t kPiece = 2ull << 20;
+    constexpr uint64_t kPiece = 256ull << 10;
     if (bytes < 2 * kPiece) {
         std::memcpy(dst, src, bytes);
         return;
     }
     HostPool& pool = HostPool::get();
-    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 4, ceil_div(bytes, kPiece));
+    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 2, ceil_div(bytes, kPiece));
     const uint64_t step = align_up(ceil_div(bytes, (uint64_t)parts), 64);
     pool.run(parts, [&](int i) {
         const uint64_t a = (uint64_t)i * step;
@@ -1753,9 +1782,9 @@ int nzgpu_blob_decompress_host(nzgpu_blob b, uint16_t* out) {
 
 namespace {
 
-// Serialize chunk views (serialize_stream, ans.hpp:306-316) into `dst`,
-// chunk headers and payloads copied by the host pool; fills the chunk table.
-void gather_stream(const nzgpu_host_sections* t, uint8_t* dst, std::vector<uint4>& info) {
+// Chunk table of the serialized form of chunk views (serialize_stream,
+// ans.hpp:306-316): payload offset, length and symbol count per chunk.
+void stream_layout(const nzgpu_host_sections* t, std::vector<uint4>& info) {
     info.resize(t->nchunks);
     uint64_t pos = 4;
     for (uint64_t c = 0; c < t->nchunks; ++c) {
@@ -1763,19 +1792,59 @@ void gather_stream(const nzgpu_host_sections* t, uint8_t* dst, std::vector<uint4
         info[c] = make_uint4((uint32_t)pos, (uint32_t)(pos >> 32), t->chunks[c].len, t->chunks[c].nsym);
         pos += t->chunks[c].len;
     }
-    const uint32_t cnt = (uint32_t)t->nchunks;
-    std::memcpy(dst, &cnt, 4);
+}
+
+// Serialize chunks [c0, c1) into `dst` (the whole stream's buffer; chunk 0
+// also writes the leading chunk count), copied by the host pool.
+void gather_chunks(const nzgpu_host_sections* t, uint8_t* dst, const std::vector<uint4>& info, uint64_t c0,
+                   uint64_t c1) {
+    if (c0 == 0) {
+        const uint32_t cnt = (uint32_t)t->nchunks;
+        std::memcpy(dst, &cnt, 4);
+    }
     HostPool& pool = HostPool::get();
-    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 4, std::max<uint64_t>(1, t->nchunks / 16));
-    const uint64_t per = ceil_div(t->nchunks, (uint64_t)parts);
+    const uint64_t nc = c1 - c0;
+    const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 2, std::max<uint64_t>(1, nc));
+    const uint64_t per = ceil_div(nc, (uint64_t)parts);
     pool.run(parts, [&](int i) {
-        for (uint64_t c = i * per; c < std::min(t->nchunks, (i + 1) * per); ++c) {
+        for (uint64_t c = c0 + i * per; c < std::min(c1, c0 + (i + 1) * per); ++c) {
             const uint64_t at = ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32));
             std::memcpy(dst + at - 8, &info[c].w, 4);
             std::memcpy(dst + at - 4, &info[c].z, 4);
             if (info[c].z) std::memcpy(dst + at, t->chunks[c].payload, info[c].z);
         }
     });
+}
+
+void gather_stream(const nzgpu_host_sections* t, uint8_t* dst, std::vector<uint4>& info) {
+    stream_layout(t, info);
+    gather_chunks(t, dst, info, 0, t->nchunks);
+}
+
+// Slices of the pipelined host decode: a multiple of the chunk size, of the
+// warp unit (32 sub-ranges) and of the lossy block; 0 = do not slice.
+// (NZGPU_HOST_SLICE overrides the element count; 0 = one slice.)
+uint64_t slice_elems() {
+    static const uint64_t v = [] {
+        const char* e = std::getenv("NZGPU_HOST_SLICE");
+        return e ? std::strtoull(e, nullptr, 10) : 4ull << 20;
+    }();
+    return v;
+}
+uint64_t slice_grain(uint64_t S, uint64_t K, uint64_t B) {
+    auto lcm = [](uint64_t x, uint64_t y) -> uint64_t {
+        uint64_t a = x, c = y;
+        while (c) {
+            const uint64_t r = a % c;
+            a = c;
+            c = r;
+        }
+        const uint64_t l = x / a * y;
+        return l / y == x / a ? l : 0;
+    };
+    uint64_t g = lcm(S, 32 * K);
+    if (g && B) g = lcm(g, B);
+    return g;
 }
 
 // General path of the sections call: serialize, then the validating host tier.
@@ -1900,29 +1969,26 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     const uint64_t i_freqs = in.take(512);
     if (int rc = hc.in.ensure(in.size)) return rc;
     uint8_t* stage = static_cast<uint8_t*>(hc.in.p);
+    cudaStream_t si = sl.s_in;
     auto h2d = [&](void* dst, uint64_t at, uint64_t len) -> int {
-        if (len) CK(cudaMemcpyAsync(dst, stage + at, len, cudaMemcpyHostToDevice, s));
+        if (len) CK(cudaMemcpyAsync(dst, stage + at, len, cudaMemcpyHostToDevice, si));
         return NZGPU_OK;
     };
     std::vector<uint4> info;
-    gather_stream(t, stage + i_stream, info);
-    if (int rc = h2d(b.stream, i_stream, stream_len)) return rc;
-    constexpr uint64_t kInSlice = 32ull << 20;  // mantissa plane in slices: gather k+1 while k is in flight
-    for (uint64_t a0 = 0; a0 < b.mant_len; a0 += kInSlice) {
-        const uint64_t len = std::min(kInSlice, b.mant_len - a0);
-        par_memcpy(stage + i_mant + a0, t->mantissas + a0, len);
-        if (int rc = h2d(b.mant + a0, i_mant + a0, len)) return rc;
-    }
+    stream_layout(t, info);
+    // the small side tables first: every slice's decode needs them
+    par_memcpy(stage + i_index, static_cast<const uint8_t*>(t->index) + sizeof(h), index_region_bytes(b.nsub));
+    std::memcpy(stage + i_info, info.data(), info.size() * sizeof(uint4));
+    std::memcpy(stage + i_freqs, t->freqs, 512);
+    if (int rc = h2d(b.index, i_index, index_region_bytes(b.nsub))) return rc;
+    if (int rc = h2d(b.chunk_info, i_info, b.nchunks * sizeof(uint4))) return rc;
+    if (int rc = h2d(b.freqs, i_freqs, 512)) return rc;
     if (b.scales_len) {
         par_memcpy(stage + i_scales, t->scales, b.scales_len);
         if (int rc = h2d(b.scales, i_scales, b.scales_len)) return rc;
     }
-    par_memcpy(stage + i_index, static_cast<const uint8_t*>(t->index) + sizeof(h), index_region_bytes(b.nsub));
-    if (int rc = h2d(b.index, i_index, index_region_bytes(b.nsub))) return rc;
-    std::memcpy(stage + i_info, info.data(), info.size() * sizeof(uint4));
-    std::memcpy(stage + i_freqs, t->freqs, 512);
-    if (int rc = h2d(b.chunk_info, i_info, b.nchunks * sizeof(uint4))) return rc;
-    if (int rc = h2d(b.freqs, i_freqs, 512)) return rc;
+    CK(cudaEventRecord(sl.h2d_done, si));
+    CK(cudaStreamWaitEvent(s, sl.h2d_done, 0));
     build_table_kernel<<<1, 256, 0, s>>>(nullptr, b.freqs, nullptr, nullptr, b.lut, b.scratch_u32);
     CK(cudaGetLastError());
     if (!(b.flags & kFlagSingleSymbol)) {
@@ -1934,32 +2000,65 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
         if (!(use_persist() && persist_fits(log2k, b.max_window_unit)))
             b.max_window = host_max_window(info, base, b.nsub, S, log2k, decode_tile_subs());
     }
-    uint16_t* d_out = static_cast<uint16_t*>(sl.out.p);
-    if (int rc = decode_blob(&b, d_out, s)) return rc;
 
-    // bf16 back in slices through a pinned ring: the worker threads copy
-    // slice k into `out` while the DMA engine brings slice k + 1..
-    constexpr uint64_t kSlice = 32ull << 20;
-    const uint64_t bytes = t->n * 2, nslices = ceil_div(bytes, kSlice);
+    // Element slices, each a whole number of chunks, warp units and lossy
+    // blocks: the stream and mantissa bytes of slice p+1 are gathered and
+    // copied in while slice p decodes and its bf16 comes back through the
+    // pinned ring, so the two PCIe directions and the host copies overlap.
+    uint16_t* d_out = static_cast<uint16_t*>(sl.out.p);
+    const uint64_t n = t->n, grain = slice_grain(S, h.interval, t->precision == 7 ? 0 : t->block_size);
+    // at most slice_elems() per slice, and at least four slices when the grain allows
+    const uint64_t want = std::min(slice_elems(), n / 4);
+    const uint64_t slice = grain && grain <= want ? grain * (want / grain) : grain && slice_elems() ? std::min(n, grain) : n;
+    const uint64_t nslices = ceil_div(n, slice);
     for (int r = 0; r < HostCtx::kOutRing; ++r)
-        if (int rc = hc.ring[r].ensure(std::min(kSlice, bytes))) return rc;
-    auto issue = [&](uint64_t k) -> int {
-        const int r = (int)(k % HostCtx::kOutRing);
-        const uint64_t a = k * kSlice, len = std::min(kSlice, bytes - a);
-        CK(cudaMemcpyAsync(hc.ring[r].p, reinterpret_cast<uint8_t*>(d_out) + a, len, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(hc.ring_ev[r], s));
+        if (int rc = hc.ring[r].ensure(std::min(slice, n) * 2)) return rc;
+    auto mant_at = [&](uint64_t e) { return t->precision == 7 ? e : e * (uint64_t)(t->precision + 1) / 8; };
+    auto spos = [&](uint64_t c) { return c == b.nchunks ? stream_len : ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32)) - 8; };
+    static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
+    double us_gather = 0, us_wait = 0, us_out = 0;
+    auto since = [](std::chrono::steady_clock::time_point t0) {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const auto t_call = std::chrono::steady_clock::now();
+    // The host alternates: gather slice p, then copy slice p-1 out of the
+    // ring.  (A separate copy-out thread measured no faster: the gathers and
+    // copy-outs share the host's memory bandwidth.)
+    auto copy_out = [&](uint64_t p) -> int {
+        const int r = (int)(p % HostCtx::kOutRing);
+        auto t0 = std::chrono::steady_clock::now();
+        CK(cudaEventSynchronize(hc.ring_ev[r]));
+        us_wait += since(t0);
+        t0 = std::chrono::steady_clock::now();
+        const uint64_t a = p * slice;
+        par_memcpy(out + a, hc.ring[r].p, std::min(slice, n - a) * 2);
+        us_out += since(t0);
         return NZGPU_OK;
     };
-    for (uint64_t k = 0; k < std::min<uint64_t>(nslices, HostCtx::kOutRing); ++k)
-        if (int rc = issue(k)) return rc;
-    for (uint64_t k = 0; k < nslices; ++k) {
-        const int r = (int)(k % HostCtx::kOutRing);
-        CK(cudaEventSynchronize(hc.ring_ev[r]));
-        const uint64_t a = k * kSlice;
-        par_memcpy(reinterpret_cast<uint8_t*>(out) + a, hc.ring[r].p, std::min(kSlice, bytes - a));
-        if (k + HostCtx::kOutRing < nslices)
-            if (int rc = issue(k + HostCtx::kOutRing)) return rc;
+    for (uint64_t p = 0; p < nslices; ++p) {
+        const uint64_t a = p * slice, len = std::min(slice, n - a);
+        const uint64_t c0 = a / S, c1 = p + 1 == nslices ? b.nchunks : (a + len) / S;
+        const uint64_t s0 = p == 0 ? 0 : spos(c0), s1 = spos(c1);
+        const auto tg = std::chrono::steady_clock::now();
+        gather_chunks(t, stage + i_stream, info, c0, c1);
+        if (int rc = h2d(b.stream + s0, i_stream + s0, s1 - s0)) return rc;
+        const uint64_t m0 = mant_at(a), m1 = p + 1 == nslices ? b.mant_len : mant_at(a + len);
+        par_memcpy(stage + i_mant + m0, t->mantissas + m0, m1 - m0);
+        us_gather += since(tg);
+        if (int rc = h2d(b.mant + m0, i_mant + m0, m1 - m0)) return rc;
+        CK(cudaEventRecord(sl.h2d_done, si));
+        CK(cudaStreamWaitEvent(s, sl.h2d_done, 0));
+        if (int rc = decode_range(&b, d_out, a, len, s)) return rc;
+        const int r = (int)(p % HostCtx::kOutRing);  // its previous slice, p - R, was copied out below
+        CK(cudaMemcpyAsync(hc.ring[r].p, d_out + a, len * 2, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(hc.ring_ev[r], s));
+        if (p > 0)
+            if (int rc = copy_out(p - 1)) return rc;
     }
+    if (int rc = copy_out(nslices - 1)) return rc;
+    if (trace)
+        std::fprintf(stderr, "nzgpu sections: n=%llu slices=%llu gather %.0f us, wait %.0f us, copy-out %.0f us, call %.0f us\n",
+                     (unsigned long long)n, (unsigned long long)nslices, us_gather, us_wait, us_out, since(t_call));
     return sync_status(s, sl.err, true);
 }
 

@@ -63,6 +63,29 @@ static std::vector<std::uint64_t> counts_of(const std::vector<std::uint8_t>& xs)
     return c;
 }
 
+// The same lossy blob through the batched host entry (nzgpu_decompress_host,
+// whole-tensor staging): an independent route for the sliced pipeline of
+// decompress_lossy (nzgpu_decompress_host_sections).
+static std::vector<Bf16> via_batch_path(const LossyBlob& b) {
+    const auto stream = serialize_stream(b.exp_stream);
+    nzgpu_host_tensor t{};
+    t.n = b.meta.element_count();
+    t.precision = b.precision;
+    t.block_size = b.block_size;
+    t.freqs = b.exp_stream.table.frequencies().data();
+    t.stream = stream.data();
+    t.stream_len = stream.size();
+    t.mantissas = b.signmant.data();
+    t.mantissa_len = b.signmant.size();
+    t.scales = b.scales.data();
+    t.scales_len = b.scales.size();
+    t.index = b.gpu_index.data();
+    t.index_len = b.gpu_index.size();
+    std::vector<Bf16> out(t.n);
+    if (nzgpu_decompress_host(&t, reinterpret_cast<std::uint16_t*>(out.data())) != NZGPU_OK) out.clear();
+    return out;
+}
+
 int main() {
     // --- bitfloat (test_bitfloat.cpp) ------------------------------------
     {
@@ -187,6 +210,19 @@ int main() {
             std::vector<Bf16> lossy_into;
             decompress_lossy_into(lb3, lossy_into);
             CHECK(lossy_into == decompress_lossy(lb3));
+            // sliced host pipeline (4 Mi-element slices) against whole-tensor
+            // staging: slice-aligned blocks (B = 512, 64), and B = 1000 / 3,
+            // which no slice size divides (one slice)
+            const std::span<const Bf16> part = std::span(g).first(9'000'001);
+            for (int k : {0, 1, 3}) {
+                for (std::uint32_t B : {512u, 64u, 1000u, 3u}) {
+                    const LossyBlob lb = compress_lossy(part, k, B);
+                    const auto want = via_batch_path(lb);
+                    CHECK(want.size() == part.size() && decompress_lossy(lb) == want);
+                }
+            }
+            const LosslessBlob odd = compress_lossless(part);
+            CHECK(decompress_lossless(odd) == std::vector<Bf16>(part.begin(), part.end()));
         }
 
         LosslessBlob bad_meta = compress_lossless(std::span(g).first(1000));

@@ -6,6 +6,9 @@
 //       -L/usr/local/cuda/lib64 -lcudart -o build/hostpath_probe
 #include <cuda_runtime.h>
 
+#include <sys/mman.h>
+
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -36,6 +39,51 @@ int main(int argc, char** argv) {
     const size_t n = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 218112000ull;  // one Llama-3-8B layer
     const size_t bytes = n * 2;
     std::printf("n=%zu bytes=%zu hw_threads=%u\n", n, bytes, std::thread::hardware_concurrency());
+    for (const char* f : {"/sys/kernel/mm/transparent_hugepage/enabled", "/sys/kernel/mm/transparent_hugepage/defrag"}) {
+        if (FILE* fp = std::fopen(f, "r")) {
+            char buf[256] = {};
+            if (std::fgets(buf, sizeof buf, fp)) std::printf("%s: %s", f, buf);
+            std::fclose(fp);
+        }
+    }
+    // fresh-vector strategies: pre-populate the reserved pages (in parallel,
+    // optionally as huge pages), then value-initialise
+    for (int mode = 0; mode < 6; ++mode) {
+        const int threads = mode % 3 == 0 ? 1 : mode % 3 == 1 ? 8 : 16;
+        const bool huge = mode >= 3;
+        double t0 = now();
+        std::vector<Bf16> w;
+        w.reserve(n);
+        char* p = reinterpret_cast<char*>(w.data());
+        if (huge) {
+            char* a = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + (2u << 20) - 1) & ~uintptr_t((2u << 20) - 1));
+            if (a < p + bytes) madvise(a, (p + bytes - a) & ~size_t((2u << 20) - 1), MADV_HUGEPAGE);
+        }
+        double t1 = now();
+        int rc_pop = 0;
+        {
+            std::vector<std::thread> ts;
+            const size_t step = ((bytes + threads - 1) / threads + 4095) & ~size_t(4095);
+            char* base = reinterpret_cast<char*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(4095));
+            const size_t span = p + bytes - base;
+            std::atomic<int> bad{0};
+            for (int t = 0; t < threads; ++t) {
+                const size_t a = t * step, b = std::min(span, a + step);
+                if (a >= b) break;
+                ts.emplace_back([=, &bad] {
+                    if (madvise(base + a, b - a, 23 /* MADV_POPULATE_WRITE */)) bad = 1;
+                });
+            }
+            for (auto& t : ts) t.join();
+            rc_pop = bad;
+        }
+        double t2 = now();
+        w.resize(n);
+        double t3 = now();
+        std::printf("fresh vector: threads=%d huge=%d populate_rc=%d reserve+madvise %.1f ms populate %.1f ms "
+                    "value-init %.1f ms total %.1f ms (%.1f GB/s)\n", threads, huge, rc_pop, (t1 - t0) * 1e3,
+                    (t2 - t1) * 1e3, (t3 - t2) * 1e3, (t3 - t0) * 1e3, bytes / (t3 - t0) / 1e9);
+    }
     for (int rep = 0; rep < 3; ++rep) {
         double t0 = now();
         std::vector<Bf16> v(n);
