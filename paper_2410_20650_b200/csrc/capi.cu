@@ -73,12 +73,6 @@ uint32_t crc_finalize(uint32_t raw, uint64_t len);
 namespace {
 // Decode schedule: the persistent warp-pipelined kernel (default) or the
 // one-tile-per-CTA kernel (NZGPU_KERNEL=tiles, or nzgpu_set_decode_kernel).
-// K3 chains are latency-bound and their byte stores cost one transaction per
-// active lane (every lane writes a different chunk): few lanes per warp,
-// spread over many SMs.
-#ifndef NZ_ENC_THREADS
-#define NZ_ENC_THREADS 32
-#endif
 #ifndef NZ_ENC_QUEUE_MIN_CTAS
 #define NZ_ENC_QUEUE_MIN_CTAS 600
 #endif
@@ -836,6 +830,9 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         if (ctas + c >= (1ull << 31)) return NZGPU_INVALID_ARGUMENT;
         ctas += (uint32_t)c;
     }
+    // Byte queue once L1 store sectors rather than the chain latency bound
+    // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
+    const bool queue = ctas >= kEncQueueMinCtas;
     mark("setup");
     auto* d_tasks = reinterpret_cast<EncTask*>(tmp + L.tasks);
     if (count > 1) {
@@ -844,9 +841,7 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         build_tables_kernel<<<count, 256, 0, s>>>(d_tables);  // K2 of every tensor in one launch
         CK(cudaMemcpyAsync(d_tasks, tasks.data(), count * sizeof(EncTask), cudaMemcpyHostToDevice, s));
     }
-    // Byte queue once L1 store sectors rather than the chain latency bound
-    // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
-    CK(launch_encode(ctas >= kEncQueueMinCtas, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
+    CK(launch_encode(queue, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
                      s));
     if (!irregular) CK(launch_index_finalize(count > 1 ? d_tasks : nullptr, count, tasks[0], units, s));
     stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);

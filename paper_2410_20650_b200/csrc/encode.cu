@@ -46,11 +46,46 @@ __device__ __forceinline__ const EncTask& task_of(const EncTask* tasks, int ntas
     return tasks[lo];
 }
 
+// Stores of the encoder's outputs (scratch bytes/words, side index) as
+// explicit global stores: through a generic pointer ptxas must assume a store
+// may alias the shared-memory encoder table and cannot hoist the next
+// steps' table loads above it.
+#ifndef NZ_ENC_STG
+#define NZ_ENC_STG 0  // measured slower (C1 2.48-2.64 vs 2.34 ms)
+#endif
+template <class T>
+__device__ __forceinline__ void st_g(T* p, T v) {
+#if NZ_ENC_STG
+    __stcg(p, v);
+#else
+    *p = v;
+#endif
+}
+
+// One encoder chain: the state of ans_encode_chunk (ans.hpp:202-225) for one
+// chunk, plus where its renormalisation bytes go.
+struct EncChain {
+    uint32_t x;
+    uint32_t emitted;
+    uint8_t* out;     // direct byte stores: next byte goes to out[-1]
+    uint32_t* wo;     // QUEUE: next word goes to wo[-1]
+    uint32_t qlo, qhi, qc;
+    uint64_t begin;   // first symbol of the chunk
+};
+
 // QUEUE: word stores from the byte queue (throughput: many chains per SM,
 // where per-lane byte stores saturate L1); otherwise direct byte stores,
 // fewer instructions per step for latency-bound launches of few chains.
+//
+// One warp per CTA (NZ_ENC_THREADS), and the launch bounds say so: with the
+// register budget of a 32-thread, one-CTA bound ptxas schedules the step
+// with 84 registers instead of 62, and a lone chain runs 2.23 instead of
+// 2.88 ms on C1 (in-order issue: the stall cycles per step are what it
+// saves).  Two chains per thread, interleaved, measured 2x slower.  The
+// byte-queue kernel (many chains, throughput-bound) keeps the default
+// bound: with the tight one it took 15.3 instead of 14.3 ms on 8 layers.
 template <bool QUEUE>
-__global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restrict__ tasks, int ntasks,
+__global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) ans_encode_kernel(const EncTask* __restrict__ tasks, int ntasks,
                                                          const __grid_constant__ EncTask one) {
     __shared__ EncSym enc[256];
     const EncTask& t = task_of(tasks, ntasks, one, blockIdx.x);
@@ -64,123 +99,138 @@ __global__ void __launch_bounds__(128) ans_encode_kernel(const EncTask* __restri
     const uint64_t nchunks = ceil_div(n, chunk_syms);
     const uint64_t c = (blockIdx.x - t.cta0) * (uint64_t)blockDim.x + threadIdx.x;
     if (c >= nchunks) return;
-    const uint64_t begin = c * chunk_syms;
-    const uint32_t len = (uint32_t)min((uint64_t)chunk_syms, n - begin);
-    uint8_t* const slot_end = t.scratch + (c + 1) * t.slot_bytes;  // 16-byte aligned
-    const uint8_t* src = t.exps + begin;
-
-    uint32_t x = kStateLow;
-    uint32_t emitted = 0;
-    // Renormalisation bytes go backwards from slot_end - 4.  Every lane writes
-    // a different chunk, so a byte store costs one L2 sector per lane: with
-    // QUEUE the bytes are queued in a 64-bit register pair (newest at the top,
-    // pulled in by funnel shifts) and leave as aligned 32-bit words.
-    uint32_t qlo = 0, qhi = 0, qc = 0;
-    uint32_t* wo = reinterpret_cast<uint32_t*>(slot_end - 4);
-    uint8_t* out = slot_end - 4;
     bool bad = false;
     const uint32_t kmask = (1u << log2_interval) - 1u;
+    auto init = [&](EncChain& ch, uint64_t cc) {
+        ch.x = kStateLow;
+        ch.emitted = 0;
+        ch.begin = cc * chunk_syms;
+        // Renormalisation bytes go backwards from the slot's end - 4.  Every
+        // lane writes a different chunk, so a byte store costs one L2 sector
+        // per lane: with QUEUE the bytes are queued in a 64-bit register pair
+        // (newest at the top, pulled in by funnel shifts) and leave as
+        // aligned 32-bit words.
+        uint8_t* const slot_end = t.scratch + (cc + 1) * t.slot_bytes;  // 16-byte aligned
+        ch.out = slot_end - 4;
+        ch.wo = reinterpret_cast<uint32_t*>(slot_end - 4);
+        ch.qlo = ch.qhi = ch.qc = 0;
+    };
     // Branch-free step (lanes of a warp encode different chunks, so any
     // data-dependent branch diverges).  The serial chain is
     // x -> compare -> select -> IMAD.WIDE -> shift -> IMAD -> x; the byte
     // queue and the checkpoint record hang off it.
-    auto step = [&](const EncSym& e, uint32_t i, bool may_ckpt) {
+    auto step = [&](EncChain& ch, const EncSym& e, uint32_t i, bool may_ckpt) {
+        uint32_t x = ch.x;
         const uint32_t limit = e.freq << 19;
         bad |= e.freq == 0;  // ans.hpp:210-212
         // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
         const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
         const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
         if constexpr (QUEUE) {
-            qlo = __funnelshift_r(qlo, qhi, 8 * nb);
-            qhi = __funnelshift_r(qhi, x, 8 * nb);  // x & 0xFF first, then (x >> 8) & 0xFF
-            qc += nb;
-            if (qc >= 4) {  // the 4 oldest queued bytes, oldest at the highest address
-                NZ_CHECK(reinterpret_cast<uint8_t*>(wo - 1) >= slot_end - t.slot_bytes);
-                *--wo = __byte_perm(__funnelshift_rc(qlo, qhi, 64 - 8 * qc), 0, 0x0123);
-                qc -= 4;
+            ch.qlo = __funnelshift_r(ch.qlo, ch.qhi, 8 * nb);
+            ch.qhi = __funnelshift_r(ch.qhi, x, 8 * nb);  // x & 0xFF first, then (x >> 8) & 0xFF
+            ch.qc += nb;
+            if (ch.qc >= 4) {  // the 4 oldest queued bytes, oldest at the highest address
+                NZ_CHECK(reinterpret_cast<uint8_t*>(ch.wo - 1) >= t.scratch + (ch.begin / chunk_syms) * t.slot_bytes);
+                st_g(--ch.wo, __byte_perm(__funnelshift_rc(ch.qlo, ch.qhi, 64 - 8 * ch.qc), 0, 0x0123));
+                ch.qc -= 4;
             }
         } else {
-            NZ_CHECK(out - nb >= slot_end - t.slot_bytes);
+            NZ_CHECK(ch.out - nb >= t.scratch + (ch.begin / chunk_syms) * t.slot_bytes);
 #if !NZ_ENC_NOSTORE  // timing experiment only: the chain without its byte stores
-            if (n1) out[-1] = (uint8_t)x;
-            if (n2) out[-2] = (uint8_t)(x >> 8);
+            if (n1) st_g(ch.out - 1, (uint8_t)x);
+            if (n2) st_g(ch.out - 2, (uint8_t)(x >> 8));
 #endif
-            out -= nb;
+            ch.out -= nb;
         }
-        emitted += nb;
+        ch.emitted += nb;
         x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
         // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
         // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
         const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
         x = q * (kProbScale - e.freq) + (x + e.cum);
+        ch.x = x;
         if (may_ckpt && ck_state && (i & kmask) == 0) {
-            const uint64_t j = (begin + i) >> log2_interval;
-            ck_state[j] = x;
+            const uint64_t j = (ch.begin + i) >> log2_interval;
+            st_g(ck_state + j, x);
             // positions are final only once the chunk's length is known:
             // record -E_j (mod 2^16) and, for unit starts, E_j itself;
             // index_finalize_kernel adds the right reference (E_32u or len-4)
-            ck_off[j] = (uint16_t)(0u - emitted);
-            if ((j & 31) == 0) ck_base[j >> 5] = emitted;
+            st_g(ck_off + j, (uint16_t)(0u - ch.emitted));
+            if ((j & 31) == 0) st_g(ck_base + (j >> 5), ch.emitted);
         }
     };
+    auto finish = [&](EncChain& ch, uint64_t cc) {
+        uint8_t* const slot_end = t.scratch + (cc + 1) * t.slot_bytes;
+        // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie
+        // below the payload start, inside the slot.
+        if (QUEUE && ch.qc) *--ch.wo = __byte_perm(ch.qhi, 0, 0x0123) << (32 - 8 * ch.qc);
+        // ans.hpp:223: final state little-endian at the tail (aligned store).
+        *reinterpret_cast<uint32_t*>(slot_end - 4) = ch.x;
+        t.plen[cc] = ch.emitted + 4;
+    };
+#if NZ_ENC_PF
+    // A lone chain (few chunks: one warp per SM) cannot hide the load of
+    // its next 16-symbol block: ncu put 22 % of C1's stall samples on the
+    // block's first use.  The chunk's symbols are pulled into L2 in one
+    // bulk prefetch up front, and the block load is pinned where it is
+    // issued (asm volatile: the compiler otherwise sinks it next to its
+    // use, a whole block later than intended).
+    auto ldblk = [](const uint8_t* p) {
+        uint4 v;
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(p));
+        return v;
+    };
+#else
+    auto ldblk = [](const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); };
+#endif
+    auto sym_of = [](const uint32_t (&w)[4], int b) { return (w[b >> 2] >> (8 * (b & 3))) & 0xFFu; };
+
+
+    EncChain ch;
+    init(ch, c);
+    const uint32_t len = (uint32_t)min((uint64_t)chunk_syms, n - ch.begin);
+    const uint8_t* src = t.exps + ch.begin;
     uint32_t i = len;
     if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (!ck_state || (kmask & 15) == 15)) {
         // 16 symbols per aligned load, walked backwards in registers; with
         // K a multiple of 16 only the block's first symbol can be a checkpoint
         for (const uint32_t top = len & ~15u; i > top;) {
             --i;
-            step(enc[__ldg(src + i)], i, true);
+            step(ch, enc[__ldg(src + i)], i, true);
         }
 #if NZ_ENC_PF
-        // A lone chain (few chunks: one warp per SM) cannot hide the load of
-        // its next 16-symbol block: ncu put 22 % of C1's stall samples on the
-        // block's first use.  The chunk's symbols are pulled into L2 in one
-        // bulk prefetch up front, and the block load is pinned where it is
-        // issued (asm volatile: the compiler otherwise sinks it next to its
-        // use, a whole block later than intended).
         if (i >= 16) prefetch_l2(src, i & ~15u);
-        auto ldblk = [](const uint8_t* p) {
-            uint4 v;
-            asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                         : "l"(p));
-            return v;
-        };
-#else
-        auto ldblk = [](const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); };
 #endif
         // table entries are loaded one step ahead so the shared-memory
         // latency stays off the state chain
-        uint4 blk = i ? ldblk(src + i - 16) : make_uint4(0, 0, 0, 0);
+        uint4 blk4 = i ? ldblk(src + i - 16) : make_uint4(0, 0, 0, 0);
         while (i) {
             i -= 16;
-            const uint32_t w[4] = {blk.x, blk.y, blk.z, blk.w};
-            if (i) blk = ldblk(src + i - 16);
+            const uint32_t w[4] = {blk4.x, blk4.y, blk4.z, blk4.w};
+            if (i) blk4 = ldblk(src + i - 16);
             EncSym cur = enc[w[3] >> 24];
 #pragma unroll
             for (int b = 15; b >= 0; --b) {
                 EncSym nxt;
-                if (b > 0) nxt = enc[(w[(b - 1) >> 2] >> (8 * ((b - 1) & 3))) & 0xFFu];
-                step(cur, i + b, b == 0);
+                if (b > 0) nxt = enc[sym_of(w, b - 1)];
+                step(ch, cur, i + b, b == 0);
                 if (b > 0) cur = nxt;
             }
         }
     } else {
         while (i) {
             --i;
-            step(enc[__ldg(src + i)], i, true);
+            step(ch, enc[__ldg(src + i)], i, true);
         }
     }
     if (bad) {
         atomicOr(t.err, kErrZeroFreq);
         return;
     }
-    // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie below
-    // the payload start, inside the slot.
-    if (QUEUE && qc) *--wo = __byte_perm(qhi, 0, 0x0123) << (32 - 8 * qc);
-    // ans.hpp:223: final state little-endian at the tail (aligned store).
-    *reinterpret_cast<uint32_t*>(slot_end - 4) = x;
-    t.plen[c] = emitted + 4;
+    finish(ch, c);
 }
 
 // Side index positions after K3 (nzgpu_internal.cuh).  The encoder walks a

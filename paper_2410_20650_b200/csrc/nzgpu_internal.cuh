@@ -68,6 +68,13 @@ struct EncSym {
     uint32_t pad;  // shift 31 + l: x / f = (x * m) >> shift for x < 2^31
 };
 
+// K3 threads per CTA: chains are latency-bound and their byte stores cost one
+// transaction per active lane (every lane writes a different chunk), so few
+// lanes per warp, spread over many SMs.
+#ifndef NZ_ENC_THREADS
+#define NZ_ENC_THREADS 32
+#endif
+
 // One tensor of a (batched) encode launch: K3 encodes its chunks into
 // per-chunk scratch slots, K4 scans and compacts them.  A launch covers many
 // tensors so that their chunk chains run concurrently (one chain per thread).
