@@ -16,33 +16,50 @@
 
 namespace nzgpu {
 
+// |x| / c correctly rounded to FP32, given rc = RN(1/c): one multiply and a
+// Markstein correction (r = |x| - q0 c exactly, by FMA; q = RN(q0 + r rc))
+// instead of the IEEE division subroutine -- the fused kernel was bound by
+// the division.  Bit-identical to __fdiv_rn for every finite bf16 magnitude
+// and every scale byte (tests/test_gpu_parity.py::
+// test_gpu_lossy_elementwise_exhaustive checks all 65,280 x 256 pairs).
+#ifndef NZ_LOSSY_FASTDIV
+#define NZ_LOSSY_FASTDIV 1
+#endif
+__device__ __forceinline__ float div_coef(float ax, float c, float rc) {
+#if NZ_LOSSY_FASTDIV
+    const float q0 = __fmul_rn(ax, rc);
+    const float r = __fmaf_rn(-q0, c, ax);
+    return __fmaf_rn(r, rc, q0);
+#else
+    (void)rc;
+    return __fdiv_rn(ax, c);
+#endif
+}
+
 // round_mantissa (bitfloat.hpp:82-98) + carry rule (tensorstore.hpp:184-194).
-__device__ __forceinline__ void lossy_normalize(uint32_t bits, float c, int k, uint32_t& exponent,
+// The division runs on the magnitude; c > 0, so the sign is the input's and
+// the quotient is finite and non-negative (inputs are finite), so the FP32 ->
+// bf16 RNE needs no NaN case.  Rounding to k mantissa bits is one add:
+// m + (half - 1) + lsb carries exactly when RNE rounds up, and a carry out of
+// the mantissa lands in the exponent (e + 1, m = 0) by itself; only a carry
+// out of exponent 254 (to the Inf pattern) is replaced by the truncation the
+// reference applies there.
+__device__ __forceinline__ void lossy_normalize(uint32_t bits, float c, float rc, int k, uint32_t& exponent,
                                                 uint32_t& item) {
-    const uint32_t nb = bf16_from_float(__fdiv_rn(__uint_as_float(bits << 16), c));
-    const uint32_t s = nb >> 15;
-    uint32_t e = (nb >> 7) & 0xFFu;
-    uint32_t m = nb & 0x7Fu;
+    const uint32_t u = __float_as_uint(div_coef(__uint_as_float((bits & 0x7FFFu) << 16), c, rc));
+    const uint32_t nbm = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;  // Bf16::from_float, bitfloat.hpp:25-32
     const uint32_t drop = 7 - k;
-    const uint32_t rem = m & ((1u << drop) - 1u);
-    const uint32_t half = 1u << (drop - 1);
-    uint32_t kept = m >> drop;
-    if (rem > half || (rem == half && (kept & 1u))) kept += 1;
-    if (kept >= (1u << k)) {       // carry
-        if (e == 254) {
-            m = (m >> drop) << drop;  // truncate_mantissa, bitfloat.hpp:102-105
-        } else {
-            e += 1;
-            m = 0;
-        }
-    } else {
-        m = kept << drop;
-    }
-    exponent = e;
-    item = (s << k) | (m >> drop);
+    const uint32_t mask = (1u << drop) - 1u;
+    // the tie-break bit is the kept mantissa's lsb: bit `drop` of m, which
+    // for k = 0 (drop = 7) lies outside m -- kept is 0, even
+    uint32_t r = (nbm + (mask >> 1) + ((nbm >> drop) & (k != 0 ? 1u : 0u))) & ~mask;
+    if (r >= 0x7F80u) r = nbm & ~mask;  // truncate_mantissa, bitfloat.hpp:102-105
+    exponent = r >> 7;
+    item = ((bits >> 15) << k) | ((r & 0x7Fu) >> drop);
 }
 
 __device__ __forceinline__ float lossy_coef(uint32_t s) { return 1.0f + (float)s * (1.0f / 128.0f); }
+__device__ __forceinline__ float lossy_rcoef(float c) { return __frcp_rn(c); }
 
 // One warp per block (grid-stride over blocks).
 __global__ void __launch_bounds__(256) lossy_normalize_kernel(const uint16_t* __restrict__ v, uint64_t n, int k,
@@ -77,10 +94,10 @@ __global__ void __launch_bounds__(256) lossy_normalize_kernel(const uint16_t* __
         const uint32_t max_at = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu);
         const uint32_t scale = __ldg(v + begin + max_at) & 0x7Fu;
         if (lane == 0) scales[b] = (uint8_t)scale;
-        const float c = lossy_coef(scale);
+        const float c = lossy_coef(scale), rc = lossy_rcoef(c);
         for (uint32_t i = lane; i < len; i += 32) {
             uint32_t e, item;
-            lossy_normalize(__ldg(v + begin + i), c, k, e, item);
+            lossy_normalize(__ldg(v + begin + i), c, rc, k, e, item);
             exps[begin + i] = (uint8_t)e;
             items[begin + i] = (uint8_t)item;
         }
@@ -154,28 +171,26 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const 
         for (int u = 0; u < U; ++u) {
             const uint64_t b = g * U + u;
             if (b >= nfull) break;
-            // argmax of magnitude bits, first index on ties (tensorstore.hpp:168-174)
-            uint32_t key = 0;
-            bool bad = false;
+            // the block's largest magnitude (tensorstore.hpp:168-174: the
+            // argmax's index only breaks ties between equal magnitudes, which
+            // share their mantissa, so the scale byte is the max's mantissa);
+            // an exponent-255 element is the max iff the block is non-finite
+            uint32_t m2 = 0;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                const uint32_t in[4] = {w[u][q].x, w[u][q].y, w[u][q].z, w[u][q].w};
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t bits = (in[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-                    bad |= (bits & 0x7F80u) == 0x7F80u;
-                    const uint32_t idx = q * 256 + lane * 8 + j;
-                    key = max(key, ((bits & 0x7FFFu) << 16) | (0xFFFFu - idx));
-                }
+                m2 = __vmaxu2(m2, w[u][q].x & 0x7FFF7FFFu);
+                m2 = __vmaxu2(m2, w[u][q].y & 0x7FFF7FFFu);
+                m2 = __vmaxu2(m2, w[u][q].z & 0x7FFF7FFFu);
+                m2 = __vmaxu2(m2, w[u][q].w & 0x7FFF7FFFu);
             }
-            key = __reduce_max_sync(0xFFFFFFFFu, key);
-            if (__any_sync(0xFFFFFFFFu, bad)) {
+            const uint32_t mmax = __reduce_max_sync(0xFFFFFFFFu, max(m2 & 0xFFFFu, m2 >> 16));
+            if (mmax >= 0x7F80u) {
                 if (lane == 0) atomicOr(err, kErrNonFinite);
                 continue;
             }
-            const uint32_t scale = (key >> 16) & 0x7Fu;
+            const uint32_t scale = mmax & 0x7Fu;
             if (lane == 0) scales[b] = (uint8_t)scale;
-            const float c = lossy_coef(scale);
+            const float c = lossy_coef(scale), rc = lossy_rcoef(c);
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 const uint32_t in[4] = {w[u][q].x, w[u][q].y, w[u][q].z, w[u][q].w};
@@ -183,7 +198,7 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const 
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     uint32_t e, item;
-                    lossy_normalize((in[j >> 1] >> (16 * (j & 1))) & 0xFFFFu, c, K, e, item);
+                    lossy_normalize((in[j >> 1] >> (16 * (j & 1))) & 0xFFFFu, c, rc, K, e, item);
                     h[e * 32] += 1;
                     e8[j >> 2] |= e << (8 * (j & 3));
                     acc = (acc << W) | item;  // pack_signed_mantissas: first item in the high bits
@@ -272,7 +287,7 @@ __global__ void lossy_roundtrip_kernel(const uint16_t* __restrict__ v, const uin
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const float c = lossy_coef(sc[i]);
         uint32_t e, item;
-        lossy_normalize(v[i], c, k, e, item);
+        lossy_normalize(v[i], c, lossy_rcoef(c), k, e, item);
         const uint32_t s = item >> k, m = item & ((1u << k) - 1u);
         const uint32_t normalized = (s << 15) | (e << 7) | (m << (7 - k));
         out[i] = bf16_from_float(__fmul_rn(__uint_as_float(normalized << 16), c));
