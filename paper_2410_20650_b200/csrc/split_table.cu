@@ -104,12 +104,22 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(co
     const uint4* v4 = reinterpret_cast<const uint4*>(v);
     // Only 12 warps fit per SM (64 KiB of counters per CTA), so each thread
     // keeps kLaneUnroll 16-byte loads in flight to cover HBM latency.
+    // The next batch's loads are issued before this batch is processed, so a
+    // warp's loads stay in flight while it splits and counts.
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + tid; g0 < groups; g0 += kLaneUnroll * stride) {
+    uint4 nx[kLaneUnroll];
+    const uint64_t gfirst = blockIdx.x * (uint64_t)blockDim.x + tid;
+#pragma unroll
+    for (int k = 0; k < kLaneUnroll; ++k)
+        if (gfirst + k * stride < groups) nx[k] = __ldcs(v4 + gfirst + k * stride);
+    for (uint64_t g0 = gfirst; g0 < groups; g0 += kLaneUnroll * stride) {
         uint4 w[kLaneUnroll];
 #pragma unroll
+        for (int k = 0; k < kLaneUnroll; ++k) w[k] = nx[k];
+        const uint64_t gn = g0 + kLaneUnroll * stride;
+#pragma unroll
         for (int k = 0; k < kLaneUnroll; ++k)
-            if (g0 + k * stride < groups) w[k] = __ldcs(v4 + g0 + k * stride);
+            if (gn + k * stride < groups) nx[k] = __ldcs(v4 + gn + k * stride);
 #pragma unroll
         for (int k = 0; k < kLaneUnroll; ++k) {
             const uint64_t g = g0 + k * stride;
