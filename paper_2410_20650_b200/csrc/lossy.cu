@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const 
                     acc = (acc << W) | item;  // pack_signed_mantissas: first item in the high bits
                 }
                 const uint64_t i0 = b * B + q * 256 + lane * 8;
+                NZ_CHECK(i0 + 8 <= nfull * B);
                 __stcs(reinterpret_cast<uint2*>(exps + i0), make_uint2(e8[0], e8[1]));
                 if constexpr (K == 3) {
                     __stcs(reinterpret_cast<uint32_t*>(packed + i0 / 2), __byte_perm(acc, 0, 0x0123));
