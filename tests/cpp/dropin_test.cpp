@@ -3,6 +3,7 @@
 // test_ans.cpp, test_tensorstore.cpp, acceptance.cpp): same calls, same
 // expected values and exception types, run against the B200 implementation.
 // Exits 0 when every check passes.  Built and run by tests/test_cpp_dropin.py.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <sstream>
@@ -223,6 +224,21 @@ int main() {
             }
             const LosslessBlob odd = compress_lossless(part);
             CHECK(decompress_lossless(odd) == std::vector<Bf16>(part.begin(), part.end()));
+            // the sliced pipeline writes exactly n values: a guard band after
+            // them stays untouched (lossless and lossy k=0)
+            const LossyBlob lk0 = compress_lossy(part, 0, 512);
+            for (int lossy : {0, 1}) {
+                std::vector<Bf16> buf(part.size() + 4096, Bf16{0x5A5A});
+                if (lossy)
+                    detail::gpu_decompress_into(lk0.meta, lk0.exp_stream, lk0.signmant, lk0.precision, lk0.block_size,
+                                                &lk0.scales, lk0.gpu_index, buf.data());
+                else
+                    detail::gpu_decompress_into(odd.meta, odd.exp_stream, odd.signmant, kLosslessPrecision, 0, nullptr,
+                                                odd.gpu_index, buf.data());
+                const std::vector<Bf16> want = lossy ? decompress_lossy(lk0) : std::vector<Bf16>(part.begin(), part.end());
+                CHECK(std::equal(want.begin(), want.end(), buf.begin()));
+                CHECK(std::all_of(buf.begin() + part.size(), buf.end(), [](Bf16 x) { return x.bits == 0x5A5A; }));
+            }
         }
 
         LosslessBlob bad_meta = compress_lossless(std::span(g).first(1000));
