@@ -151,6 +151,17 @@ struct MulConsts {
 // shifts (the FMA pipe's IMAD.HI is not cheaper than the ALU shift), a
 // warp-uniform branch for the rare second byte (VOTE + reconvergence),
 // reloading both window words instead of rotating them (one more LDS).
+#ifndef NZ_EXP_LUTBANK
+#define NZ_EXP_LUTBANK 0  // timing experiment only (wrong output): every LUT gather conflict-free
+#endif
+#if NZ_EXP_LUTBANK
+#define NZP_TRANSITION(lut, x, v)                                                            \
+    do {                                                                                     \
+        uint32_t h_ = ((x) >> kProbBits) - kProbScale;                                       \
+        v = p_lds32(lut_lane + ((x) & 0xF80u) * 4u);                                         \
+        x = ((v) >> 20) * h_ + ((v) >> 8);                                                   \
+    } while (0)
+#else
 #define NZP_TRANSITION(lut, x, v)                                                            \
     do {                                                                                     \
         uint32_t a_, h_ = ((x) >> kProbBits) - kProbScale;                                   \
@@ -159,6 +170,7 @@ struct MulConsts {
         v = p_lds32(a_);                                                                     \
         x = ((v) >> 20) * h_ + ((v) >> 8);                                                   \
     } while (0)
+#endif
 
 #ifndef NZ_PBYTES
 #define NZ_PBYTES 0
@@ -210,6 +222,25 @@ struct MulConsts {
         asm("{\n\t.reg .b32 t, c;\n\t" NZP_RENORM_FLO "}"                                      \
             : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
     } while (0)
+#ifndef NZ_WSHIFT_MOV
+#define NZ_WSHIFT_MOV 0  // 1: measured no faster (182.3-184.3 us either way)
+#endif
+#if NZ_WSHIFT_MOV
+// Window shift as plain predicated moves/adds: the kernel is issue-bound
+// (a conflict-free LUT gather, timed with NZ_EXP_LUTBANK, is no faster), so
+// the instruction count per step is what matters, not the ALU/FMA balance.
+#define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
+    do {                                                                                     \
+        NZP_TRANSITION(lut, x, v);                                                           \
+        asm("{\n\t.reg .pred q;\n\t.reg .b32 t, c;\n\t" NZP_RENORM_FLO                        \
+            "setp.ge.u32 q, %2, 0x4000;\n\t"                                                 \
+            "@q mov.b32 %3, %4;\n\t"                                                         \
+            "@q add.u32 %1, %1, 4;\n\t"                                                      \
+            "@q sub.u32 %2, %2, 0x4400;\n\t"                                                 \
+            "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
+            : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2));                                \
+    } while (0)
+#else
 #define NZP_STEP(lut, x, q, o8, w, w2, v)                                                    \
     do {                                                                                     \
         NZP_TRANSITION(lut, x, v);                                                           \
@@ -221,6 +252,7 @@ struct MulConsts {
             "@q ld.shared.u32 %4, [%1+4];\n\t}"                                              \
             : "+r"(x), "+r"(q), "+r"(o8), "+r"(w), "+r"(w2) : "r"(mc.one));                  \
     } while (0)
+#endif
 #else
 // The window position is a PRMT selector sel = k | (k+1) << 4 (k = byte
 // offset into the 8-byte window w:w2) instead of a bit offset: one PRMT
@@ -491,6 +523,9 @@ __global__ void __launch_bounds__(p_warps(LOG2K) * 32, NZ_PMINB) decode_persist_
     const uint32_t lutt = lut + tok;
     const uint32_t lutm = lutt - (1u << 26);
     (void)lutm;
+#if NZ_EXP_LUTBANK
+    const uint32_t lut_lane = lutt + lane * 4u;  // (x & 0xF80) * 4 is a multiple of 128: bank = lane
+#endif
 
     for (uint32_t i = 0; u < uend; ++i) {
         const int b = i & 1;
@@ -943,6 +978,9 @@ __global__ void __launch_bounds__(p_warps(LOG2K) * 32, NZ_PMINB) decode_persist_
         un = unn;
     }
     err = __reduce_or_sync(0xFFFFFFFFu, err);
+#if NZ_EXP_LUTBANK
+    err = 0;
+#endif
     if (lane == 0 && err) atomicOr(d.err, err);
 }
 
