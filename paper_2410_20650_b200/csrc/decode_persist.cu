@@ -154,6 +154,7 @@ struct MulConsts {
 #ifndef NZ_EXP_LUTBANK
 #define NZ_EXP_LUTBANK 0  // timing experiment only (wrong output): every LUT gather conflict-free
 #endif
+
 #if NZ_EXP_LUTBANK
 #define NZP_TRANSITION(lut, x, v)                                                            \
     do {                                                                                     \
