@@ -612,10 +612,12 @@ def run_dropin_bench():
         out = subprocess.run([exe, "3"], capture_output=True, text=True, timeout=600)
         d = json.loads(out.stdout.strip().splitlines()[-1])
         return {"value": d["fresh_gbs"], "unit": "GB/s", "reused": d["reused_gbs"], "ok": d["ok"],
+                "compress": d.get("compress_gbs"),
                 "sample": "Llama-3-8B layer projections q,k,v,o,gate,up,down ("
                           f"{d['elements']} elements), C++ drop-in decompress_lossless per tensor, median of "
                           f"{d['reps']}; value = fresh std::vector per call (the reference signature), reused = "
-                          "decompress_lossless_into a kept vector"}
+                          "decompress_lossless_into a kept vector; compress = compress_lossless of the same tensors "
+                          "(host vector in, LosslessBlob out), same algorithmic bytes"}
     except Exception as e:  # reported, never required
         return {"value": None, "unit": "GB/s", "error": repr(e)[:200]}
 

@@ -13,6 +13,7 @@
 // validation first.
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <istream>
 #include <thread>
@@ -26,6 +27,7 @@
 #include "neuzip/bitfloat.hpp"
 #include "neuzip/crc32.hpp"
 #include "neuzip/errors.hpp"
+#include "neuzip/parallel.hpp"
 
 #if defined(__linux__)
 #include <sys/mman.h>
@@ -119,6 +121,77 @@ inline Sections export_blob(nzgpu_blob h) {
     return s;
 }
 
+// Fault the pages of a fresh output buffer in before it is value-initialised:
+// as transparent huge pages where the kernel allows it (MADV_HUGEPAGE), and
+// populated by several threads (MADV_POPULATE_WRITE) instead of one thread
+// taking a 4 KiB fault per page inside the vector's zero-fill.  Best effort:
+// any refusal leaves the ordinary fault path.
+inline void prefault_output(void* p, std::size_t bytes) {
+#if defined(__linux__)
+    constexpr std::size_t kHuge = 2u << 20;
+    if (bytes < 16 * kHuge) return;
+    const auto lo = reinterpret_cast<std::uintptr_t>(p), hi = lo + bytes;
+    const std::uintptr_t h0 = (lo + kHuge - 1) & ~(kHuge - 1), h1 = hi & ~(kHuge - 1);
+    if (h1 > h0) ::madvise(reinterpret_cast<void*>(h0), h1 - h0, MADV_HUGEPAGE);
+    const std::uintptr_t p0 = lo & ~std::uintptr_t(4095);
+    const unsigned workers = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const std::size_t step = (((hi - p0) + workers - 1) / workers + kHuge - 1) & ~(kHuge - 1);
+    std::vector<std::thread> ts;
+    for (unsigned w = 0; w < workers && p0 + w * step < hi; ++w) {
+        const std::uintptr_t a = p0 + w * step, b = std::min<std::uintptr_t>(hi, a + step);
+        ts.emplace_back([a, b] { ::madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite); });
+    }
+    for (std::thread& t : ts) t.join();
+#else
+    (void)p;
+    (void)bytes;
+#endif
+}
+
+// A freshly compressed blob's sections as the drop-in types: the exponent
+// stream straight into AnsChunk payload vectors (allocated by several
+// threads; no serialized copy, no deserialize_stream pass) and the planes
+// through the library's pinned staging (nzgpu_blob_export_chunks).
+struct Exported {
+    AnsStream stream;
+    std::vector<std::uint8_t> mantissas, scales, index;
+};
+
+// A fresh, value-initialised byte vector whose pages were faulted in first.
+inline std::vector<std::uint8_t> fresh_plane(std::size_t bytes) {
+    std::vector<std::uint8_t> v;
+    v.reserve(bytes);
+    prefault_output(v.data(), bytes);
+    v.resize(bytes);
+    return v;
+}
+
+// `mantissas` may come prepared (already info.mantissa_len bytes): the
+// compress calls build it on a helper thread while the GPU compresses.
+inline Exported export_chunked(nzgpu_blob h, std::vector<std::uint8_t> mantissas = {}) {
+    nzgpu_blob_info info{};
+    check(nzgpu_blob_info_get(h, &info), "blob info");
+    std::vector<std::uint32_t> lens(info.num_chunks), nsyms(info.num_chunks);
+    check(nzgpu_blob_chunks(h, lens.data(), nsyms.data()), "blob chunks");
+    Exported e;
+    e.stream.chunks.resize(info.num_chunks);
+    std::vector<std::uint8_t*> ptrs(info.num_chunks);
+    parallel_for(info.num_chunks, [&](std::size_t c) {
+        e.stream.chunks[c].symbol_count = nsyms[c];
+        e.stream.chunks[c].payload.resize(lens[c]);
+        ptrs[c] = e.stream.chunks[c].payload.data();
+    });
+    e.mantissas = mantissas.size() == info.mantissa_len ? std::move(mantissas) : fresh_plane(info.mantissa_len);
+    e.scales.resize(info.scales_len);
+    e.index.resize(info.index_len);
+    std::array<std::uint16_t, 256> freqs{};
+    check(nzgpu_blob_export_chunks(h, freqs.data(), ptrs.data(), e.mantissas.data(), e.scales.data(),
+                                   e.index.empty() ? nullptr : e.index.data()),
+          "blob export");
+    e.stream.table = FrequencyTable::from_frequencies(freqs);
+    return e;
+}
+
 inline FrequencyTable table_from(const std::vector<std::uint16_t>& f) {
     std::array<std::uint16_t, 256> a{};
     std::copy(f.begin(), f.end(), a.begin());
@@ -156,33 +229,6 @@ inline void gpu_decompress_into(const TensorMeta& meta, const AnsStream& stream,
     check(nzgpu_decompress_host_sections(&t, reinterpret_cast<std::uint16_t*>(out)), "decompress");
 }
 
-// Fault the pages of a fresh output buffer in before it is value-initialised:
-// as transparent huge pages where the kernel allows it (MADV_HUGEPAGE), and
-// populated by several threads (MADV_POPULATE_WRITE) instead of one thread
-// taking a 4 KiB fault per page inside the vector's zero-fill.  Best effort:
-// any refusal leaves the ordinary fault path.
-inline void prefault_output(void* p, std::size_t bytes) {
-#if defined(__linux__)
-    constexpr std::size_t kHuge = 2u << 20;
-    if (bytes < 16 * kHuge) return;
-    const auto lo = reinterpret_cast<std::uintptr_t>(p), hi = lo + bytes;
-    const std::uintptr_t h0 = (lo + kHuge - 1) & ~(kHuge - 1), h1 = hi & ~(kHuge - 1);
-    if (h1 > h0) ::madvise(reinterpret_cast<void*>(h0), h1 - h0, MADV_HUGEPAGE);
-    const std::uintptr_t p0 = lo & ~std::uintptr_t(4095);
-    const unsigned workers = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-    const std::size_t step = (((hi - p0) + workers - 1) / workers + kHuge - 1) & ~(kHuge - 1);
-    std::vector<std::thread> ts;
-    for (unsigned w = 0; w < workers && p0 + w * step < hi; ++w) {
-        const std::uintptr_t a = p0 + w * step, b = std::min<std::uintptr_t>(hi, a + step);
-        ts.emplace_back([a, b] { ::madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite); });
-    }
-    for (std::thread& t : ts) t.join();
-#else
-    (void)p;
-    (void)bytes;
-#endif
-}
-
 inline std::vector<Bf16> gpu_decompress(const TensorMeta& meta, const AnsStream& stream,
                                         const std::vector<std::uint8_t>& mant, int precision, std::uint32_t block,
                                         const std::vector<std::uint8_t>* scales,
@@ -205,12 +251,14 @@ inline LosslessBlob compress_lossless(std::span<const Bf16> values, TensorMeta m
     meta.validate();
     if (meta.element_count() != values.size()) throw std::invalid_argument("compress: shape does not match value count");
     detail::DeviceBlob b;
-    detail::check(nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(),
-                                      kLosslessPrecision, 0, 0, 0, &b.h),
-                  "compress_lossless");
-    detail::Sections s = detail::export_blob(b.h);
-    const FrequencyTable table = detail::table_from(s.freqs);
-    return LosslessBlob{std::move(meta), deserialize_stream(s.stream, table), std::move(s.mantissas), std::move(s.index)};
+    std::vector<std::uint8_t> mant;  // the n-byte plane, faulted in beside the GPU work
+    std::thread prep([&] { mant = detail::fresh_plane(values.size()); });
+    const int rc = nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(),
+                                       kLosslessPrecision, 0, 0, 0, &b.h);
+    prep.join();
+    detail::check(rc, "compress_lossless");
+    detail::Exported e = detail::export_chunked(b.h, std::move(mant));
+    return LosslessBlob{std::move(meta), std::move(e.stream), std::move(e.mantissas), std::move(e.index)};
 }
 
 // tensorstore.hpp:108-110
@@ -245,13 +293,15 @@ inline LossyBlob compress_lossy(std::span<const Bf16> values, int k, std::uint32
     meta.validate();
     if (meta.element_count() != values.size()) throw std::invalid_argument("compress: shape does not match value count");
     detail::DeviceBlob b;
-    detail::check(nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(), k,
-                                      block_size, 0, 0, &b.h),
-                  "compress_lossy");
-    detail::Sections s = detail::export_blob(b.h);
-    const FrequencyTable table = detail::table_from(s.freqs);
-    return LossyBlob{std::move(meta),   k, block_size, std::move(s.scales), deserialize_stream(s.stream, table),
-                     std::move(s.mantissas), std::move(s.index)};
+    std::vector<std::uint8_t> mant;  // the packed (k+1)-bit plane, faulted in beside the GPU work
+    std::thread prep([&] { mant = detail::fresh_plane((values.size() * static_cast<std::size_t>(k + 1) + 7) / 8); });
+    const int rc = nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(), k,
+                                       block_size, 0, 0, &b.h);
+    prep.join();
+    detail::check(rc, "compress_lossy");
+    detail::Exported e = detail::export_chunked(b.h, std::move(mant));
+    return LossyBlob{std::move(meta),       k, block_size, std::move(e.scales), std::move(e.stream),
+                     std::move(e.mantissas), std::move(e.index)};
 }
 
 // tensorstore.hpp:210-213

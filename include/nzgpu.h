@@ -147,6 +147,15 @@ int nzgpu_blob_free(nzgpu_blob blob);
  * info.scales_len; index: info.index_len bytes. */
 int nzgpu_blob_export(nzgpu_blob blob, uint16_t* freqs, uint8_t* stream, uint8_t* mantissas,
                       uint8_t* scales, void* index);
+/* Chunk table of a blob: payload bytes and symbol count of each of its
+ * info.num_chunks chunks (AnsChunk::payload.size(), ::symbol_count). */
+int nzgpu_blob_chunks(nzgpu_blob blob, uint32_t* lens, uint32_t* nsyms);
+/* nzgpu_blob_export with the exponent stream delivered as chunk payloads
+ * (chunk_payloads[c] receives lens[c] bytes of nzgpu_blob_chunks) -- the
+ * drop-in's AnsStream form, without a serialized copy.  Sections come back
+ * D2H through pinned staging, copied out by host worker threads. */
+int nzgpu_blob_export_chunks(nzgpu_blob blob, uint16_t* freqs, uint8_t* const* chunk_payloads, uint8_t* mantissas,
+                             uint8_t* scales, void* index);
 /* Upload a host tensor (reference formats) into a new device blob,
  * validating framing and table (deserialize_table / deserialize_stream,
  * ans.hpp:120-130, :318-347) and building the checkpoint index on the GPU
@@ -175,7 +184,9 @@ int nzgpu_plan_set_max_ctas(nzgpu_plan plan, uint32_t max_ctas);
 
 /* ---- host tier: the reference-facing calls (host buffers, synchronous) --- */
 /* Compress host values; returns a device blob (export its sections with
- * nzgpu_blob_export).  Equivalent to H2D + nzgpu_compress. */
+ * nzgpu_blob_export[_chunks]).  Equivalent to H2D + nzgpu_compress; the
+ * values go H2D in slices through pinned staging (host worker threads copy
+ * slice k+1 while slice k is in flight). */
 int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint32_t block_size,
                         uint32_t chunk_symbols, uint32_t interval, nzgpu_blob* out);
 /* Decompress a host tensor into host memory: H2D of the compressed sections,

@@ -1275,6 +1275,10 @@ int nzgpu_plan_kernel(nzgpu_plan p) {
 }
 
 // ---------------------------------------------------------------- host tier
+namespace {
+int h2d_staged(void* dst, const void* src, uint64_t bytes, cudaStream_t s);
+}
+
 int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint32_t block_size,
                         uint32_t chunk_symbols, uint32_t interval, nzgpu_blob* out) {
     if (!out) return NZGPU_INVALID_ARGUMENT;
@@ -1284,7 +1288,11 @@ int nzgpu_compress_host(const uint16_t* values, uint64_t n, int precision, uint3
     StreamGuard sg{StreamGuard::Own{}};
     uint16_t* d = nullptr;
     CK(cudaMallocAsync(&d, n * 2 + 16, sg.s));
-    CK(cudaMemcpyAsync(d, values, n * 2, cudaMemcpyHostToDevice, sg.s));
+    if (int rc = h2d_staged(d, values, n * 2, sg.s)) {
+        cudaFreeAsync(d, sg.s);
+        cudaStreamSynchronize(sg.s);
+        return rc;
+    }
     std::unique_ptr<nzgpu_blob_s> b(new (std::nothrow) nzgpu_blob_s);
     int rc = compress_into(b.get(), d, n, precision, block_size, chunk_symbols, interval, sg.s);
     cudaFreeAsync(d, sg.s);
@@ -1540,6 +1548,68 @@ struct HostCtx {
 };
 thread_local std::unique_ptr<HostCtx> g_host;
 
+constexpr uint64_t kStageSlice = 32ull << 20;  // pinned ring slice of the staged host copies
+
+// Pageable host -> device in slices through the calling thread's pinned ring:
+// host workers copy slice k+1 into its slot while slice k's DMA runs.  Returns
+// once every slice is queued on `s` (the last slots may still be in flight;
+// they are only reused after their events).
+int h2d_staged(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+    if (!bytes) return NZGPU_OK;
+    if (!g_host) g_host.reset(new HostCtx);
+    HostCtx& hc = *g_host;
+    if (int rc = hc.init()) return rc;
+    const uint64_t slice = std::min(kStageSlice, bytes);
+    for (int r = 0; r < HostCtx::kOutRing; ++r)
+        if (int rc = hc.ring[r].ensure(slice)) return rc;
+    // the ring may still feed a D2H/H2D of an earlier call on another stream
+    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
+    const uint64_t nslices = ceil_div(bytes, slice);
+    for (uint64_t k = 0; k < nslices; ++k) {
+        const int r = (int)(k % HostCtx::kOutRing);
+        if (k >= (uint64_t)HostCtx::kOutRing) CK(cudaEventSynchronize(hc.ring_ev[r]));
+        const uint64_t a = k * slice, len = std::min(slice, bytes - a);
+        par_memcpy(hc.ring[r].p, static_cast<const uint8_t*>(src) + a, len);
+        CK(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + a, hc.ring[r].p, len, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(hc.ring_ev[r], s));
+    }
+    return NZGPU_OK;
+}
+
+// Device -> host in slices through the pinned ring; `sink(offset, host, len)`
+// consumes each slice (on the calling thread, typically with the host pool)
+// while the next slices' DMA runs.  Synchronous.
+int d2h_staged(const void* src, uint64_t bytes, cudaStream_t s,
+               const std::function<void(uint64_t, const uint8_t*, uint64_t)>& sink) {
+    if (!bytes) return NZGPU_OK;
+    if (!g_host) g_host.reset(new HostCtx);
+    HostCtx& hc = *g_host;
+    if (int rc = hc.init()) return rc;
+    const uint64_t slice = std::min(kStageSlice, bytes);
+    for (int r = 0; r < HostCtx::kOutRing; ++r)
+        if (int rc = hc.ring[r].ensure(slice)) return rc;
+    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
+    const uint64_t nslices = ceil_div(bytes, slice);
+    auto issue = [&](uint64_t k) -> int {
+        const int r = (int)(k % HostCtx::kOutRing);
+        const uint64_t a = k * slice, len = std::min(slice, bytes - a);
+        CK(cudaMemcpyAsync(hc.ring[r].p, static_cast<const uint8_t*>(src) + a, len, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(hc.ring_ev[r], s));
+        return NZGPU_OK;
+    };
+    for (uint64_t k = 0; k < std::min<uint64_t>(nslices, HostCtx::kOutRing); ++k)
+        if (int rc = issue(k)) return rc;
+    for (uint64_t k = 0; k < nslices; ++k) {
+        const int r = (int)(k % HostCtx::kOutRing);
+        CK(cudaEventSynchronize(hc.ring_ev[r]));
+        const uint64_t a = k * slice;
+        sink(a, static_cast<const uint8_t*>(hc.ring[r].p), std::min(slice, bytes - a));
+        if (k + HostCtx::kOutRing < nslices)
+            if (int rc = issue(k + HostCtx::kOutRing)) return rc;
+    }
+    return NZGPU_OK;
+}
+
 // Host replica of tile_window() over the host copy of the index's unit
 // positions: the decode kernel's shared-memory window size without a device
 // round trip (ts = sub-ranges per tile/unit, a multiple of 32).
@@ -1697,6 +1767,68 @@ int stage_and_decode(HostSlot& sl, const nzgpu_host_tensor* t, uint16_t* host_ou
 }
 
 }  // namespace
+
+int nzgpu_blob_chunks(nzgpu_blob b, uint32_t* lens, uint32_t* nsyms) {
+    if (!b || (b->nchunks && (!lens || !nsyms))) return NZGPU_INVALID_ARGUMENT;
+    if (!b->nchunks) return NZGPU_OK;
+    std::vector<uint4> info(b->nchunks);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(info.data(), b->chunk_info, b->nchunks * sizeof(uint4), cudaMemcpyDeviceToHost));
+    for (uint64_t c = 0; c < b->nchunks; ++c) {
+        lens[c] = info[c].z;
+        nsyms[c] = info[c].w;
+    }
+    return NZGPU_OK;
+}
+
+int nzgpu_blob_export_chunks(nzgpu_blob b, uint16_t* freqs, uint8_t* const* chunk_payloads, uint8_t* mantissas,
+                             uint8_t* scales, void* index) {
+    if (!b || (b->nchunks && !chunk_payloads)) return NZGPU_INVALID_ARGUMENT;
+    StreamGuard sg{StreamGuard::Own{}};
+    CK(cudaDeviceSynchronize());  // the blob may have been produced on any stream
+    std::vector<uint4> info(b->nchunks);
+    if (b->nchunks) CK(cudaMemcpy(info.data(), b->chunk_info, b->nchunks * sizeof(uint4), cudaMemcpyDeviceToHost));
+    for (uint64_t c = 0; c < b->nchunks; ++c)
+        if (info[c].z && !chunk_payloads[c]) return NZGPU_INVALID_ARGUMENT;
+    if (freqs) CK(cudaMemcpy(freqs, b->freqs, 512, cudaMemcpyDeviceToHost));
+    // the stream's chunk payloads, scattered slice by slice (they are in
+    // stream order, so the chunks overlapping a slice are a contiguous run)
+    HostPool& pool = HostPool::get();
+    uint64_t first = 0;
+    auto scatter = [&](uint64_t a, const uint8_t* host, uint64_t len) {
+        auto pos = [&](uint64_t c) { return (uint64_t)info[c].x | ((uint64_t)info[c].y << 32); };
+        while (first < b->nchunks && pos(first) + info[first].z <= a) ++first;
+        uint64_t last = first;
+        while (last < b->nchunks && pos(last) < a + len) ++last;
+        const uint64_t nc = last - first;
+        if (!nc) return;
+        const int parts = (int)std::min<uint64_t>((uint64_t)pool.threads() * 2, nc);
+        const uint64_t per = ceil_div(nc, (uint64_t)parts);
+        pool.run(parts, [&](int i) {
+            for (uint64_t c = first + i * per; c < std::min(last, first + (i + 1) * per); ++c) {
+                const uint64_t p0 = std::max(pos(c), a), p1 = std::min(pos(c) + info[c].z, a + len);
+                if (p1 > p0) std::memcpy(chunk_payloads[c] + (p0 - pos(c)), host + (p0 - a), p1 - p0);
+            }
+        });
+    };
+    if (int rc = d2h_staged(b->stream, b->stream_len, sg.s, scatter)) return rc;
+    auto into = [](uint8_t* dst) {
+        return [dst](uint64_t a, const uint8_t* host, uint64_t len) { par_memcpy(dst + a, host, len); };
+    };
+    if (mantissas)
+        if (int rc = d2h_staged(b->mant, b->mant_len, sg.s, into(mantissas))) return rc;
+    if (scales && b->scales_len) CK(cudaMemcpy(scales, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
+    if (index && !(b->flags & kFlagIrregular)) {
+        IndexHeader h{kIndexMagic, kIndexVersion, b->chunk_syms, b->interval, b->n, b->nchunks, b->nsub, b->stream_len,
+                      b->max_window_unit, 0};
+        std::memcpy(index, &h, sizeof(h));
+        if (b->nsub)
+            if (int rc = d2h_staged(b->index, index_region_bytes(b->nsub), sg.s,
+                                    into(static_cast<uint8_t*>(index) + sizeof(h))))
+                return rc;
+    }
+    return NZGPU_OK;
+}
 
 int nzgpu_decompress_host_batch(const nzgpu_host_tensor* ts, int count, uint16_t* const* outs) {
     if (count < 0 || (count && (!ts || !outs))) return NZGPU_INVALID_ARGUMENT;

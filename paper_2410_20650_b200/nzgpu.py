@@ -150,6 +150,8 @@ SIGNATURES = {
     "nzgpu_blob_info_get": (_i, [_vp, _p(BlobInfo)]),
     "nzgpu_blob_free": (_i, [_vp]),
     "nzgpu_blob_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "nzgpu_blob_chunks": (_i, [_vp, _vp, _vp]),
+    "nzgpu_blob_export_chunks": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "nzgpu_blob_import": (_i, [_p(HostTensor), _u32, _vp, _p(_vp)]),
     "nzgpu_blob_decompress_host": (_i, [_vp, _vp]),
     "nzgpu_decompress_host_sections": (_i, [_p(HostSections), _vp]),
