@@ -1127,21 +1127,43 @@ int nzgpu_blob_free(nzgpu_blob blob) {
     return NZGPU_OK;
 }
 
+namespace {
+int d2h_staged(const void* src, uint64_t bytes, cudaStream_t s,
+               const std::function<void(uint64_t, const uint8_t*, uint64_t)>& sink);
+void par_memcpy(void* dst, const void* src, uint64_t bytes);
+// One section to host memory: large ones through the pinned ring and the
+// host workers (pageable destinations fault in parallel), small ones direct.
+int d2h_section(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+    if (!bytes) return NZGPU_OK;
+    if (bytes < (4ull << 20)) {
+        CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        return NZGPU_OK;
+    }
+    uint8_t* d = static_cast<uint8_t*>(dst);
+    return d2h_staged(src, bytes, s, [d](uint64_t a, const uint8_t* h, uint64_t len) { par_memcpy(d + a, h, len); });
+}
+}  // namespace
+
 int nzgpu_blob_export(nzgpu_blob b, uint16_t* freqs, uint8_t* stream, uint8_t* mantissas, uint8_t* scales,
                       void* index) {
     if (!b) return NZGPU_INVALID_ARGUMENT;
     CK(cudaDeviceSynchronize());
+    StreamGuard sg{StreamGuard::Own{}};
     if (freqs) CK(cudaMemcpy(freqs, b->freqs, 512, cudaMemcpyDeviceToHost));
-    if (stream && b->stream_len) CK(cudaMemcpy(stream, b->stream, b->stream_len, cudaMemcpyDeviceToHost));
-    if (mantissas && b->mant_len) CK(cudaMemcpy(mantissas, b->mant, b->mant_len, cudaMemcpyDeviceToHost));
-    if (scales && b->scales_len) CK(cudaMemcpy(scales, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
+    if (stream)
+        if (int rc = d2h_section(stream, b->stream, b->stream_len, sg.s)) return rc;
+    if (mantissas)
+        if (int rc = d2h_section(mantissas, b->mant, b->mant_len, sg.s)) return rc;
+    if (scales)
+        if (int rc = d2h_section(scales, b->scales, b->scales_len, sg.s)) return rc;
     if (index && !(b->flags & kFlagIrregular)) {
         IndexHeader h{kIndexMagic, kIndexVersion, b->chunk_syms, b->interval, b->n, b->nchunks, b->nsub, b->stream_len,
                       b->max_window_unit, 0};
         std::memcpy(index, &h, sizeof(h));
         if (b->nsub)
-            CK(cudaMemcpy(static_cast<uint8_t*>(index) + sizeof(h), b->index, index_region_bytes(b->nsub),
-                          cudaMemcpyDeviceToHost));
+            if (int rc = d2h_section(static_cast<uint8_t*>(index) + sizeof(h), b->index, index_region_bytes(b->nsub),
+                                     sg.s))
+                return rc;
     }
     return NZGPU_OK;
 }
