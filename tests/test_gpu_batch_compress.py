@@ -154,3 +154,49 @@ def test_gpu_pool_reuse_and_trim(nz, port):
     assert nz.nzgpu.lib.nzgpu_trim_device_pool() == 0
     b = nz.DeviceBlob.compress(d)
     assert (b.decompress().view(torch.int16).cpu().numpy().view(np.uint16) == t).all()
+
+
+def test_gpu_export_chunks_matches_serialized_export(nz, port):
+    """nzgpu_blob_export_chunks (the drop-in's AnsChunk export) hands out the
+    same bytes as nzgpu_blob_export: every chunk payload equals its slice of
+    the serialized stream (ans.hpp:306-316), and the planes and side index
+    are identical -- for tensors below and above the 4 MiB staging cutoff
+    and across 32 MiB staging slices (the chunk scatter crosses slices)."""
+    import ctypes as C
+
+    N = nz.nzgpu
+    for n, k in ((70001, 7), (1 << 22, 3), (40_000_000, 7)):
+        v = port.gaussian_bf16(port.derive(71, n), n, 0.02)
+        blob = nz.compress_lossless(v) if k == 7 else nz.compress_lossy(v, k, 512)
+        db = nz.DeviceBlob.from_host(blob)
+        try:
+            i = db.info
+            want = db.to_host()
+            nc = int(i.num_chunks)
+            lens = np.zeros(nc, np.uint32)
+            nsyms = np.zeros(nc, np.uint32)
+            assert N.lib.nzgpu_blob_chunks(db.handle, lens.ctypes.data, nsyms.ctypes.data) == 0
+            bufs = [np.zeros(max(int(x), 1), np.uint8) for x in lens]
+            ptrs = (C.c_void_p * nc)(*[b.ctypes.data for b in bufs])
+            freqs = np.zeros(256, np.uint16)
+            mant = np.zeros(max(int(i.mantissa_len), 1), np.uint8)
+            scales = np.zeros(max(int(i.scales_len), 1), np.uint8)
+            index = np.zeros(max(int(i.index_len), 1), np.uint8)
+            assert N.lib.nzgpu_blob_export_chunks(db.handle, freqs.ctypes.data, ptrs, mant.ctypes.data,
+                                                  scales.ctypes.data, index.ctypes.data) == 0
+            stream = want.stream
+            pos = 4
+            for c in range(nc):
+                assert int.from_bytes(stream[pos:pos + 4], "little") == nsyms[c]
+                assert int.from_bytes(stream[pos + 4:pos + 8], "little") == lens[c]
+                pos += 8
+                assert bufs[c][: lens[c]].tobytes() == stream[pos:pos + int(lens[c])], c
+                pos += int(lens[c])
+            assert pos == len(stream)
+            assert (freqs == want.freqs).all()
+            assert (mant[: i.mantissa_len] == want.signmant).all()
+            if k != 7:
+                assert (scales[: i.scales_len] == want.scales).all()
+            assert index[: i.index_len].tobytes() == want.index
+        finally:
+            db.free()
