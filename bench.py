@@ -449,12 +449,61 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if rank == 0:
+        if args.c1:
+            line["c1"] = run_c1(args, nz, torch, peak, dev)
         if args.dropin and args.model == "8b" and args.precision == 7:
             line["e2e_dropin"] = run_dropin_bench()
         line["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_c1(args, nz, torch, peak, dev):
+    """configs[0] beside the headline: one 4096x4096 N(0, 0.02^2) tensor
+    (rank 0, outside the timed region).  Decode latency with L2 flushed
+    before every repetition (a 256 MiB write), CUDA events on the launching
+    stream, median of 21; compress wall time (host-synchronised, median of 7).
+    The decoded tensor is checked against the source (lossless) or the
+    single-blob decode (lossy)."""
+    import numpy as np
+
+    g = torch.Generator(device=dev).manual_seed(args.seed + 1)
+    n = 4096 * 4096
+    w = (torch.randn(n, device=dev, generator=g) * 0.02).to(torch.bfloat16)
+    ts, blob = [], None
+    for i in range(7):
+        if blob is not None:
+            blob.free()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        blob = nz.DeviceBlob.compress_batch([w], precision=args.precision, block_size=args.block,
+                                            interval=args.interval)[0]
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    out = torch.empty_like(w)
+    scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    us = []
+    for i in range(24):
+        scrub.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        blob.decompress_into(out, stream)
+        b.record(stream)
+        b.synchronize()
+        if i >= 3:
+            us.append(a.elapsed_time(b) * 1e3)
+    blob.status(stream)
+    ok = bool(torch.equal(out.view(torch.int16), (w if args.precision == 7 else blob.decompress()).view(torch.int16)))
+    algo = int(blob.info.payload_bytes) + 2 * n
+    dec = float(np.median(us))
+    res = {"workload": "C1: one 4096x4096 tensor (configs[0])", "decode_us": round(dec, 2),
+           "decode_gbs": round(algo / dec / 1e3, 1), "decode_frac": round(algo / dec / 1e3 / peak, 4),
+           "compress_ms": round(float(np.median(ts)) * 1e3, 3), "verified": ok,
+           "note": "L2 flushed before each decode; events around the single launch (launch latency included)"}
+    blob.free()
+    return res
 
 
 def verify_outputs(args, nz, torch, blobs, make_plan, run_plans, join, regen, stream, dev, rank):
@@ -760,6 +809,7 @@ def main():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--e2e-layers", type=int, default=8)
     ap.add_argument("--dropin", type=int, default=1, help="also time the C++ drop-in host API (rank 0, 8B lossless)")
+    ap.add_argument("--c1", type=int, default=1, help="also time configs[0] (one 4096x4096 tensor), rank 0")
     ap.add_argument("--cpu-tensors", type=int, default=7)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--verify", type=int, default=1,

@@ -53,6 +53,9 @@ def test_b200_arm_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert "sm_mhz" in d["clocks"]
+    # configs[0] probe: one 4096x4096 tensor, decoded and verified
+    c1 = d["c1"]
+    assert c1["verified"] is True and c1["decode_us"] > 0 and 0 < c1["decode_frac"] < 1 and c1["compress_ms"] > 0
     # throughput = algorithmic bytes over the timed steps
     bytes_step = d["config"]["bytes_algo_per_step"]
     assert d["value"] == pytest.approx(bytes_step / (d["ms_per_step"] / 1e3) / 1e9, rel=0.01)
