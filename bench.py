@@ -597,7 +597,8 @@ def run_e2e(args, nz, blobs, torch, dist=None, red_dev="cuda"):
     pinned = []
 
     def pin(a):
-        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a if a.flags.writeable else a.copy()).pin_memory()
         pinned.append(t)
         return t
 
