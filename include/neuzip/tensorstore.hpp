@@ -15,11 +15,13 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <exception>
 #include <istream>
 #include <thread>
 #include <ostream>
 #include <span>
 #include <string>
+#include <system_error>
 #include <variant>
 #include <vector>
 
@@ -139,7 +141,12 @@ inline void prefault_output(void* p, std::size_t bytes) {
     std::vector<std::thread> ts;
     for (unsigned w = 0; w < workers && p0 + w * step < hi; ++w) {
         const std::uintptr_t a = p0 + w * step, b = std::min<std::uintptr_t>(hi, a + step);
-        ts.emplace_back([a, b] { ::madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite); });
+        auto populate = [a, b] { ::madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite); };
+        try {
+            ts.emplace_back(populate);
+        } catch (const std::system_error&) {  // no thread to spare: populate this range here
+            populate();
+        }
     }
     for (std::thread& t : ts) t.join();
 #else
@@ -165,6 +172,40 @@ inline std::vector<std::uint8_t> fresh_plane(std::size_t bytes) {
     v.resize(bytes);
     return v;
 }
+
+// fresh_plane(bytes) built on a helper thread while the caller works; get()
+// joins and hands it over (an allocation failure is rethrown there).
+class PlaneAsync {
+public:
+    explicit PlaneAsync(std::size_t bytes) : bytes_(bytes) {
+        try {
+            t_ = std::thread([this] { run(); });
+        } catch (const std::system_error&) {
+            run();  // no thread to spare: build it now
+        }
+    }
+    ~PlaneAsync() {
+        if (t_.joinable()) t_.join();
+    }
+    std::vector<std::uint8_t> get() {
+        if (t_.joinable()) t_.join();
+        if (err_) std::rethrow_exception(err_);
+        return std::move(v_);
+    }
+
+private:
+    void run() {
+        try {
+            v_ = fresh_plane(bytes_);
+        } catch (...) {
+            err_ = std::current_exception();
+        }
+    }
+    std::size_t bytes_;
+    std::vector<std::uint8_t> v_;
+    std::exception_ptr err_;
+    std::thread t_;
+};
 
 // `mantissas` may come prepared (already info.mantissa_len bytes): the
 // compress calls build it on a helper thread while the GPU compresses.
@@ -251,13 +292,12 @@ inline LosslessBlob compress_lossless(std::span<const Bf16> values, TensorMeta m
     meta.validate();
     if (meta.element_count() != values.size()) throw std::invalid_argument("compress: shape does not match value count");
     detail::DeviceBlob b;
-    std::vector<std::uint8_t> mant;  // the n-byte plane, faulted in beside the GPU work
-    std::thread prep([&] { mant = detail::fresh_plane(values.size()); });
+    detail::PlaneAsync mant(values.size());  // the n-byte plane, faulted in beside the GPU work
     const int rc = nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(),
                                        kLosslessPrecision, 0, 0, 0, &b.h);
-    prep.join();
+    std::vector<std::uint8_t> plane = mant.get();
     detail::check(rc, "compress_lossless");
-    detail::Exported e = detail::export_chunked(b.h, std::move(mant));
+    detail::Exported e = detail::export_chunked(b.h, std::move(plane));
     return LosslessBlob{std::move(meta), std::move(e.stream), std::move(e.mantissas), std::move(e.index)};
 }
 
@@ -293,13 +333,13 @@ inline LossyBlob compress_lossy(std::span<const Bf16> values, int k, std::uint32
     meta.validate();
     if (meta.element_count() != values.size()) throw std::invalid_argument("compress: shape does not match value count");
     detail::DeviceBlob b;
-    std::vector<std::uint8_t> mant;  // the packed (k+1)-bit plane, faulted in beside the GPU work
-    std::thread prep([&] { mant = detail::fresh_plane((values.size() * static_cast<std::size_t>(k + 1) + 7) / 8); });
+    // the packed (k+1)-bit plane, faulted in beside the GPU work
+    detail::PlaneAsync mant((values.size() * static_cast<std::size_t>(k + 1) + 7) / 8);
     const int rc = nzgpu_compress_host(reinterpret_cast<const std::uint16_t*>(values.data()), values.size(), k,
                                        block_size, 0, 0, &b.h);
-    prep.join();
+    std::vector<std::uint8_t> plane = mant.get();
     detail::check(rc, "compress_lossy");
-    detail::Exported e = detail::export_chunked(b.h, std::move(mant));
+    detail::Exported e = detail::export_chunked(b.h, std::move(plane));
     return LossyBlob{std::move(meta),       k, block_size, std::move(e.scales), std::move(e.stream),
                      std::move(e.mantissas), std::move(e.index)};
 }
