@@ -573,6 +573,19 @@ int decode_range(const nzgpu_blob_s* b, uint16_t* d_out, uint64_t a, uint64_t le
     return NZGPU_OK;
 }
 
+extern "C" int h2d_staged(void* dst, const void* src, uint64_t bytes, cudaStream_t s);  // host tier, below
+
+// One host section to the device: large ones through the pinned ring and the
+// host workers (10-16 GB/s from pageable memory otherwise), small ones direct.
+int h2d_section(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
+    if (!bytes) return NZGPU_OK;
+    if (bytes < (4ull << 20)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return NZGPU_OK;
+    }
+    return h2d_staged(dst, src, bytes, s);
+}
+
 // Fill a blob from host sections (reference formats).
 int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, cudaStream_t s) {
     if (!t || !valid_precision(t->precision)) return NZGPU_INVALID_ARGUMENT;
@@ -627,8 +640,8 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
     if (rc) return rc;
     CK(dev_alloc(reinterpret_cast<void**>(&b->stream), align_up(std::max<uint64_t>(t->stream_len, 1), 16) + 32, s));
     CK(cudaMemsetAsync(b->err, 0, 64, s));
-    if (t->stream_len) CK(cudaMemcpyAsync(b->stream, t->stream, t->stream_len, cudaMemcpyHostToDevice, s));
-    if (t->mantissa_len) CK(cudaMemcpyAsync(b->mant, t->mantissas, t->mantissa_len, cudaMemcpyHostToDevice, s));
+    if (int e = h2d_section(b->stream, t->stream, t->stream_len, s)) return e;
+    if (int e = h2d_section(b->mant, t->mantissas, t->mantissa_len, s)) return e;
     if (b->scales_len) CK(cudaMemcpyAsync(b->scales, t->scales, b->scales_len, cudaMemcpyHostToDevice, s));
     if (!info.empty())
         CK(cudaMemcpyAsync(b->chunk_info, info.data(), info.size() * sizeof(uint4), cudaMemcpyHostToDevice, s));
@@ -654,8 +667,9 @@ int import_into(nzgpu_blob_s* b, const nzgpu_host_tensor* t, uint32_t interval, 
                      h.interval == interval && h.n == t->n && h.nchunks == info.size() && h.nsub == b->nsub &&
                      h.stream_len == t->stream_len && t->index_len == sizeof(h) + index_region_bytes(h.nsub);
         if (have_index)
-            CK(cudaMemcpyAsync(b->index, static_cast<const uint8_t*>(t->index) + sizeof(h),
-                               index_region_bytes(b->nsub), cudaMemcpyHostToDevice, s));
+            if (int e = h2d_section(b->index, static_cast<const uint8_t*>(t->index) + sizeof(h),
+                                    index_region_bytes(b->nsub), s))
+                return e;
     }
     if (!have_index) {
         // K8: rebuild the checkpoint index by decoding every chunk once on
@@ -2581,13 +2595,13 @@ int nzgpu_blob_write_nzt(nzgpu_blob b, const uint64_t* shape, int ndim, uint8_t*
     CK(cudaMemcpy(p, b->freqs, 512, cudaMemcpyDeviceToHost));  // LE u16 table
     p += 512;
     p = put_le(p, b->scales_len, 4);
-    if (b->scales_len) CK(cudaMemcpy(p, b->scales, b->scales_len, cudaMemcpyDeviceToHost));
+    if (int rc = d2h_section(p, b->scales, b->scales_len, sg.s)) return rc;
     p += b->scales_len;
     p = put_le(p, b->stream_len, 8);
-    if (b->stream_len) CK(cudaMemcpy(p, b->stream, b->stream_len, cudaMemcpyDeviceToHost));
+    if (int rc = d2h_section(p, b->stream, b->stream_len, sg.s)) return rc;
     p += b->stream_len;
     p = put_le(p, b->mant_len, 8);
-    if (b->mant_len) CK(cudaMemcpy(p, b->mant, b->mant_len, cudaMemcpyDeviceToHost));
+    if (int rc = d2h_section(p, b->mant, b->mant_len, sg.s)) return rc;
     p += b->mant_len;
     p = put_le(p, crc, 4);
     if (written) *written = (uint64_t)(p - out);
