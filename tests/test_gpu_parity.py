@@ -395,6 +395,27 @@ def test_gpu_batch_host_decode(nz, port):
         nz.release_host_buffers()
 
 
+def test_gpu_host_tier_from_concurrent_threads(nz, port):
+    """The host tier from several threads at once: per-thread staging (pinned
+    ring, device slots), the shared host worker pool and the device pool.
+    Large tensors take the sliced pipeline (pageable outputs), compress the
+    staged H2D; every result must be exact."""
+    import concurrent.futures as cf
+
+    vs = [port.gaussian_bf16(500 + i, n, 0.02) for i, n in enumerate([5_000_000, 9_000_001, 70001, 4_194_304])]
+    blobs = [nz.compress_lossless(v) for v in vs]
+
+    def work(i):
+        for _ in range(3):
+            b = nz.compress_lossless(vs[i])
+            assert b.stream == blobs[i].stream and (b.signmant == blobs[i].signmant).all()
+            assert (nz.decompress_lossless(blobs[i]) == vs[i]).all()
+        return i
+
+    with cf.ThreadPoolExecutor(4) as ex:
+        assert sorted(ex.map(work, range(4))) == [0, 1, 2, 3]
+
+
 def test_gpu_index_window_hint_is_only_a_hint(nz, port):
     """The exported index carries the unit window size (header offset 48).
     A zeroed or implausible hint falls back to a scan and still decodes; an
