@@ -107,3 +107,20 @@ def test_shannon_entropy_is_the_reference_sum():
     z = np.zeros(4, np.uint64)
     assert N.lib.nzgpu_shannon_entropy(z.ctypes.data, 4, C.byref(h)) == N.INVALID_ARGUMENT
     assert N.lib.nzgpu_shannon_entropy(None, 0, C.byref(h)) == N.INVALID_ARGUMENT
+
+
+def test_host_tier_entry_points_reject_bad_arguments_without_a_device():
+    """The chunk-export and sections entry points validate their arguments
+    before any CUDA call (so these run on a GPU-less machine too)."""
+    import ctypes as C
+
+    from paper_2410_20650_b200 import nzgpu as N
+
+    lens = (C.c_uint32 * 4)()
+    assert N.lib.nzgpu_blob_chunks(None, lens, lens) == N.INVALID_ARGUMENT
+    assert N.lib.nzgpu_blob_export_chunks(None, None, None, None, None, None) == N.INVALID_ARGUMENT
+    assert N.lib.nzgpu_decompress_host_sections(None, None) == N.INVALID_ARGUMENT
+    t = N.HostSections() if hasattr(N, "HostSections") else None
+    if t is not None:
+        t.n, t.precision = 10, 5  # invalid precision
+        assert N.lib.nzgpu_decompress_host_sections(C.byref(t), None) == N.INVALID_ARGUMENT
