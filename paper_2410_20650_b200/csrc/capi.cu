@@ -2209,7 +2209,7 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     const uint64_t slice = grain && grain <= want ? grain * (want / grain) : grain && slice_elems() ? std::min(n, grain) : n;
     const uint64_t nslices = ceil_div(n, slice);
     for (int r = 0; r < HostCtx::kOutRing; ++r)
-        if (int rc = hc.ring[r].ensure(std::min(slice, n) * 2)) return rc;
+        if (int rc = hc.ring[r].ensure(std::min(std::min(slice, n) * 2, kStageSlice))) return rc;
     auto mant_at = [&](uint64_t e) { return t->precision == 7 ? e : e * (uint64_t)(t->precision + 1) / 8; };
     auto spos = [&](uint64_t c) { return c == b.nchunks ? stream_len : ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32)) - 8; };
     static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
@@ -2218,18 +2218,37 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
         return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     };
     const auto t_call = std::chrono::steady_clock::now();
-    // The host alternates: gather slice p, then copy slice p-1 out of the
-    // ring.  (A separate copy-out thread measured no faster: the gathers and
-    // copy-outs share the host's memory bandwidth.)
-    auto copy_out = [&](uint64_t p) -> int {
-        const int r = (int)(p % HostCtx::kOutRing);
+    // The host alternates: gather slice p, then copy the earlier slices'
+    // output out of the ring.  The output goes D2H in pieces of at most one
+    // ring slot (32 MB): one piece per slice normally; a slice larger than a
+    // slot (a lossy block size no slice size divides: one slice) streams its
+    // pieces through the 3-slot ring.  (A separate copy-out thread measured
+    // no faster: the gathers and copy-outs share the host's memory bandwidth.)
+    const uint64_t piece = std::min(std::min(slice, n) * 2, kStageSlice);
+    struct Piece {
+        uint64_t off, len;  // bytes of the bf16 output
+    };
+    std::vector<Piece> pieces;
+    uint64_t issued = 0, copied = 0;
+    auto copy_one = [&]() -> int {
+        const int r = (int)(copied % HostCtx::kOutRing);
         auto t0 = std::chrono::steady_clock::now();
         CK(cudaEventSynchronize(hc.ring_ev[r]));
         us_wait += since(t0);
         t0 = std::chrono::steady_clock::now();
-        const uint64_t a = p * slice;
-        par_memcpy(out + a, hc.ring[r].p, std::min(slice, n - a) * 2);
+        par_memcpy(reinterpret_cast<uint8_t*>(out) + pieces[copied].off, hc.ring[r].p, pieces[copied].len);
         us_out += since(t0);
+        ++copied;
+        return NZGPU_OK;
+    };
+    auto issue_one = [&]() -> int {
+        if (issued - copied == (uint64_t)HostCtx::kOutRing)  // its slot's previous piece is still to copy out
+            if (int rc = copy_one()) return rc;
+        const int r = (int)(issued % HostCtx::kOutRing);
+        CK(cudaMemcpyAsync(hc.ring[r].p, reinterpret_cast<const uint8_t*>(d_out) + pieces[issued].off,
+                           pieces[issued].len, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(hc.ring_ev[r], s));
+        ++issued;
         return NZGPU_OK;
     };
     for (uint64_t p = 0; p < nslices; ++p) {
@@ -2246,13 +2265,15 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
         CK(cudaEventRecord(sl.h2d_done, si));
         CK(cudaStreamWaitEvent(s, sl.h2d_done, 0));
         if (int rc = decode_range(&b, d_out, a, len, s)) return rc;
-        const int r = (int)(p % HostCtx::kOutRing);  // its previous slice, p - R, was copied out below
-        CK(cudaMemcpyAsync(hc.ring[r].p, d_out + a, len * 2, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(hc.ring_ev[r], s));
-        if (p > 0)
-            if (int rc = copy_out(p - 1)) return rc;
+        const uint64_t first_new = pieces.size();
+        for (uint64_t o = a * 2; o < (a + len) * 2; o += piece) pieces.push_back({o, std::min(piece, (a + len) * 2 - o)});
+        while (issued < pieces.size())
+            if (int rc = issue_one()) return rc;
+        while (copied < first_new)  // the earlier slices' pieces
+            if (int rc = copy_one()) return rc;
     }
-    if (int rc = copy_out(nslices - 1)) return rc;
+    while (copied < pieces.size())
+        if (int rc = copy_one()) return rc;
     if (trace)
         std::fprintf(stderr, "nzgpu sections: n=%llu slices=%llu gather %.0f us, wait %.0f us, copy-out %.0f us, call %.0f us\n",
                      (unsigned long long)n, (unsigned long long)nslices, us_gather, us_wait, us_out, since(t_call));

@@ -222,6 +222,10 @@ int main() {
                     CHECK(want.size() == part.size() && decompress_lossy(lb) == want);
                 }
             }
+            // one slice (no slice size divides B = 999) whose 33.5 MB output
+            // streams through the 32 MB ring slots in two pieces
+            const LossyBlob lbig = compress_lossy(g, 3, 999);
+            CHECK(decompress_lossy(lbig) == via_batch_path(lbig));
             const LosslessBlob odd = compress_lossless(part);
             CHECK(decompress_lossless(odd) == std::vector<Bf16>(part.begin(), part.end()));
             // the sliced pipeline writes exactly n values: a guard band after
