@@ -1558,10 +1558,12 @@ struct HostCtx {
     HostSlot slot[kHostSlots];
     // nzgpu_decompress_host_sections: gathered inputs and the D2H ring
     static constexpr int kOutRing = 3;
-    PinnedBuf in, ring[kOutRing];
-    cudaEvent_t ring_ev[kOutRing] = {};
+    PinnedBuf in, ring[kOutRing], in_ring[kOutRing];
+    cudaEvent_t ring_ev[kOutRing] = {}, in_ev[kOutRing] = {};
     ~HostCtx() {
         for (cudaEvent_t& e : ring_ev)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t& e : in_ev)
             if (e) cudaEventDestroy(e);
     }
     int init() {
@@ -1578,6 +1580,8 @@ struct HostCtx {
                 if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         }
         for (cudaEvent_t& e : ring_ev)
+            if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (cudaEvent_t& e : in_ev)
             if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         return NZGPU_OK;
     }
@@ -2159,9 +2163,11 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     b.stream = static_cast<uint8_t*>(sl.stream.p);
     b.err = sl.err;
 
-    // pinned staging: stream | mantissas | scales | index region | chunk table | table
+    // pinned staging of the side tables: scales | index region | chunk table
+    // | table (the stream and mantissa bytes go through a ring of slice-sized
+    // slots below, so pinned memory does not grow with the tensor)
     Carve in;
-    const uint64_t i_stream = in.take(stream_len), i_mant = in.take(b.mant_len), i_scales = in.take(b.scales_len);
+    const uint64_t i_scales = in.take(b.scales_len);
     const uint64_t i_index = in.take(index_region_bytes(b.nsub)), i_info = in.take(b.nchunks * sizeof(uint4));
     const uint64_t i_freqs = in.take(512);
     if (int rc = hc.in.ensure(in.size)) return rc;
@@ -2212,6 +2218,32 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
         if (int rc = hc.ring[r].ensure(std::min(std::min(slice, n) * 2, kStageSlice))) return rc;
     auto mant_at = [&](uint64_t e) { return t->precision == 7 ? e : e * (uint64_t)(t->precision + 1) / 8; };
     auto spos = [&](uint64_t c) { return c == b.nchunks ? stream_len : ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32)) - 8; };
+    // a slice's inputs: its stream bytes [s0, s1) and mantissa bytes [m0, m1)
+    struct SliceIn {
+        uint64_t a, len, c0, c1, s0, s1, m0, m1;
+    };
+    auto slice_in = [&](uint64_t p) {
+        SliceIn x;
+        x.a = p * slice;
+        x.len = std::min(slice, n - x.a);
+        x.c0 = x.a / S;
+        x.c1 = p + 1 == nslices ? b.nchunks : (x.a + x.len) / S;
+        x.s0 = p == 0 ? 0 : spos(x.c0);
+        x.s1 = spos(x.c1);
+        x.m0 = mant_at(x.a);
+        x.m1 = p + 1 == nslices ? b.mant_len : mant_at(x.a + x.len);
+        return x;
+    };
+    uint64_t slot_bytes = 0;
+    for (uint64_t p = 0; p < nslices; ++p) {
+        const SliceIn x = slice_in(p);
+        slot_bytes = std::max(slot_bytes, align_up(x.s1 - x.s0, 16) + (x.m1 - x.m0));
+    }
+    for (int r = 0; r < HostCtx::kOutRing; ++r) {
+        CK(cudaEventSynchronize(hc.in_ev[r]));  // an earlier call's H2D from this slot
+        if ((uint64_t)r < nslices)
+            if (int rc = hc.in_ring[r].ensure(slot_bytes)) return rc;
+    }
     static const bool trace = std::getenv("NZGPU_TRACE") != nullptr;
     double us_gather = 0, us_wait = 0, us_out = 0;
     auto since = [](std::chrono::steady_clock::time_point t0) {
@@ -2252,16 +2284,19 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
         return NZGPU_OK;
     };
     for (uint64_t p = 0; p < nslices; ++p) {
-        const uint64_t a = p * slice, len = std::min(slice, n - a);
-        const uint64_t c0 = a / S, c1 = p + 1 == nslices ? b.nchunks : (a + len) / S;
-        const uint64_t s0 = p == 0 ? 0 : spos(c0), s1 = spos(c1);
+        const SliceIn x = slice_in(p);
+        const uint64_t a = x.a, len = x.len;
+        const int ri = (int)(p % HostCtx::kOutRing);
+        if (p >= (uint64_t)HostCtx::kOutRing) CK(cudaEventSynchronize(hc.in_ev[ri]));  // slot's H2D of slice p-R
+        uint8_t* slot = static_cast<uint8_t*>(hc.in_ring[ri].p);
+        const uint64_t mat = align_up(x.s1 - x.s0, 16);
         const auto tg = std::chrono::steady_clock::now();
-        gather_chunks(t, stage + i_stream, info, c0, c1);
-        if (int rc = h2d(b.stream + s0, i_stream + s0, s1 - s0)) return rc;
-        const uint64_t m0 = mant_at(a), m1 = p + 1 == nslices ? b.mant_len : mant_at(a + len);
-        par_memcpy(stage + i_mant + m0, t->mantissas + m0, m1 - m0);
+        gather_chunks(t, slot - x.s0, info, x.c0, x.c1);  // writes stream bytes [s0, s1) at slot[0..)
+        par_memcpy(slot + mat, t->mantissas + x.m0, x.m1 - x.m0);
         us_gather += since(tg);
-        if (int rc = h2d(b.mant + m0, i_mant + m0, m1 - m0)) return rc;
+        if (x.s1 > x.s0) CK(cudaMemcpyAsync(b.stream + x.s0, slot, x.s1 - x.s0, cudaMemcpyHostToDevice, si));
+        if (x.m1 > x.m0) CK(cudaMemcpyAsync(b.mant + x.m0, slot + mat, x.m1 - x.m0, cudaMemcpyHostToDevice, si));
+        CK(cudaEventRecord(hc.in_ev[ri], si));
         CK(cudaEventRecord(sl.h2d_done, si));
         CK(cudaStreamWaitEvent(s, sl.h2d_done, 0));
         if (int rc = decode_range(&b, d_out, a, len, s)) return rc;
