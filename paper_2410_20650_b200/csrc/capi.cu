@@ -33,7 +33,7 @@ __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, u
                                    uint32_t*);
 cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTask& one, uint64_t total_units,
                                   cudaStream_t s);
-cudaError_t launch_encode(bool queue, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
+cudaError_t launch_encode(bool queue, bool check, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
                           const EncTask& one, cudaStream_t s);
 __global__ void stream_scan_kernel(const EncTask*, const __grid_constant__ EncTask);
 __global__ void build_tables_kernel(const TableTask*);
@@ -77,6 +77,9 @@ namespace {
 #define NZ_ENC_QUEUE_MIN_CTAS 600
 #endif
 constexpr uint32_t kEncQueueMinCtas = NZ_ENC_QUEUE_MIN_CTAS;
+#ifndef NZ_ENC_CHECK_OWN
+#define NZ_ENC_CHECK_OWN false  // compress: the frequency check is redundant with the histogram's table
+#endif
 
 int g_kernel = -1;  // -1: from the environment
 bool use_persist() {
@@ -855,7 +858,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         build_tables_kernel<<<count, 256, 0, s>>>(d_tables);  // K2 of every tensor in one launch
         CK(cudaMemcpyAsync(d_tasks, tasks.data(), count * sizeof(EncTask), cudaMemcpyHostToDevice, s));
     }
-    CK(launch_encode(queue, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
+    // the tables come from the tensors' own histograms: no zero frequency
+    CK(launch_encode(queue, NZ_ENC_CHECK_OWN, ctas, NZ_ENC_THREADS, count > 1 ? d_tasks : nullptr, count, tasks[0],
                      s));
     if (!irregular) CK(launch_index_finalize(count > 1 ? d_tasks : nullptr, count, tasks[0], units, s));
     stream_scan_kernel<<<count, 1024, 0, s>>>(count > 1 ? d_tasks : nullptr, tasks[0]);
@@ -2419,7 +2423,7 @@ int nzgpu_ans_encode_host(const uint8_t* symbols, uint64_t n, const uint16_t* fr
     t.n = n;
     t.slot_bytes = slot;
     t.chunk_syms = chunk_symbols;
-    CK(launch_encode(false, grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, nullptr, 1, t, s));
+    CK(launch_encode(false, true, grid_for(nchunks, NZ_ENC_THREADS, 1u << 30), NZ_ENC_THREADS, nullptr, 1, t, s));
     stream_scan_kernel<<<1, 1024, 0, s>>>(nullptr, t);
     CK(cudaGetLastError());
     uint32_t m[8];

@@ -87,7 +87,10 @@ struct EncChain {
 // saves).  Two chains per thread, interleaved, measured 2x slower.  The
 // byte-queue kernel (many chains, throughput-bound) keeps the default
 // bound: with the tight one it took 15.3 instead of 14.3 ms on 8 layers.
-template <bool QUEUE>
+// CHECK: test every symbol's frequency (ans.hpp:210-212) -- needed for a
+// caller's table (nzgpu_ans_encode); a table built from the data's own
+// histogram gives every present symbol a nonzero frequency (ans.hpp:71-90).
+template <bool QUEUE, bool CHECK>
 __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) ans_encode_kernel(const EncTask* __restrict__ tasks, int ntasks,
                                                          const __grid_constant__ EncTask one) {
     __shared__ EncSym enc[256];
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
     auto step = [&](EncChain& ch, const EncSym& e, uint32_t i, bool may_ckpt) {
         uint32_t x = ch.x;
         const uint32_t limit = e.freq << 19;
-        bad |= e.freq == 0;  // ans.hpp:210-212
+        if constexpr (CHECK) bad |= e.freq == 0;  // ans.hpp:210-212
         // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
         const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
         const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
@@ -390,12 +393,16 @@ cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTas
 }
 
 // K3 launcher (the template kernels stay in this translation unit).
-cudaError_t launch_encode(bool queue, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
+cudaError_t launch_encode(bool queue, bool check, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
                           const EncTask& one, cudaStream_t s) {
-    if (queue)
-        ans_encode_kernel<true><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+    if (queue && check)
+        ans_encode_kernel<true, true><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+    else if (queue)
+        ans_encode_kernel<true, false><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+    else if (check)
+        ans_encode_kernel<false, true><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
     else
-        ans_encode_kernel<false><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
+        ans_encode_kernel<false, false><<<ctas, threads, 0, s>>>(tasks, ntasks, one);
     return cudaGetLastError();
 }
 
