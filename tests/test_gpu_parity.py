@@ -67,6 +67,22 @@ def test_gpu_checkpoint_intervals(nz, port, interval):
     assert (len(blob.index) - 56) / v.size < (0.0959 if interval == 64 else 0.0480)
 
 
+@pytest.mark.parametrize("interval", [64, 128])
+@pytest.mark.parametrize("k", [7, 3])
+def test_gpu_sliced_host_decode_intervals(nz, port, interval, k):
+    """The sliced host pipeline (pageable output, >= 4 Mi elements) at both
+    checkpoint strides, lossless and lossy: slices are whole chunks, warp
+    units (32 K symbols) and lossy blocks."""
+    v = port.gaussian_bf16(321 + interval, 5_000_003, 0.02)
+    if k == 7:
+        blob = nz.compress_lossless(v, interval=interval)
+        assert (nz.decompress_lossless(blob) == v).all()
+    else:
+        blob = nz.compress_lossy(v, k, 512, interval=interval)
+        f, sc, st, pk = port.compress_lossy(v, k, 512)
+        assert (nz.decompress_lossy(blob) == port.decompress_lossy(f, sc, st, pk, k, 512, v.size)).all()
+
+
 def test_gpu_interval_256_rejected(nz, port):
     """The decoder's checkpoint strides are 64 and 128 symbols (a unit of
     32 sub-ranges then spans <= 31 * (1.5 K + 2) bytes: 16-bit offsets)."""
