@@ -1604,10 +1604,11 @@ int h2d_staged(void* dst, const void* src, uint64_t bytes, cudaStream_t s) {
     HostCtx& hc = *g_host;
     if (int rc = hc.init()) return rc;
     const uint64_t slice = std::min(kStageSlice, bytes);
+    // copies still reading the ring (an earlier section of the same call)
+    // finish before a slot is reused or reallocated
+    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
     for (int r = 0; r < HostCtx::kOutRing; ++r)
         if (int rc = hc.ring[r].ensure(slice)) return rc;
-    // the ring may still feed a D2H/H2D of an earlier call on another stream
-    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
     const uint64_t nslices = ceil_div(bytes, slice);
     for (uint64_t k = 0; k < nslices; ++k) {
         const int r = (int)(k % HostCtx::kOutRing);
@@ -1630,9 +1631,9 @@ int d2h_staged(const void* src, uint64_t bytes, cudaStream_t s,
     HostCtx& hc = *g_host;
     if (int rc = hc.init()) return rc;
     const uint64_t slice = std::min(kStageSlice, bytes);
+    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
     for (int r = 0; r < HostCtx::kOutRing; ++r)
         if (int rc = hc.ring[r].ensure(slice)) return rc;
-    for (int r = 0; r < HostCtx::kOutRing; ++r) CK(cudaEventSynchronize(hc.ring_ev[r]));
     const uint64_t nslices = ceil_div(bytes, slice);
     auto issue = [&](uint64_t k) -> int {
         const int r = (int)(k % HostCtx::kOutRing);
@@ -2218,8 +2219,10 @@ int nzgpu_decompress_host_sections(const nzgpu_host_sections* t, uint16_t* out) 
     const uint64_t want = std::min(slice_elems(), n / 4);
     const uint64_t slice = grain && grain <= want ? grain * (want / grain) : grain && slice_elems() ? std::min(n, grain) : n;
     const uint64_t nslices = ceil_div(n, slice);
-    for (int r = 0; r < HostCtx::kOutRing; ++r)
+    for (int r = 0; r < HostCtx::kOutRing; ++r) {
+        CK(cudaEventSynchronize(hc.ring_ev[r]));  // nothing in flight reads or writes a slot it may reallocate
         if (int rc = hc.ring[r].ensure(std::min(std::min(slice, n) * 2, kStageSlice))) return rc;
+    }
     auto mant_at = [&](uint64_t e) { return t->precision == 7 ? e : e * (uint64_t)(t->precision + 1) / 8; };
     auto spos = [&](uint64_t c) { return c == b.nchunks ? stream_len : ((uint64_t)info[c].x | ((uint64_t)info[c].y << 32)) - 8; };
     // a slice's inputs: its stream bytes [s0, s1) and mantissa bytes [m0, m1)
