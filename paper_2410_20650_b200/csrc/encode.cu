@@ -31,6 +31,9 @@
 #ifndef NZ_ENC_PF
 #define NZ_ENC_PF 1
 #endif
+#ifndef NZ_ENC_PTXSTORE
+#define NZ_ENC_PTXSTORE 1
+#endif
 #ifndef NZ_ENC_PF_WIN
 #define NZ_ENC_PF_WIN 4096  // symbols per L2 prefetch step (power of two, multiple of 16)
 #endif
@@ -143,11 +146,27 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
             }
         } else {
             NZ_CHECK(ch.out - nb >= t.scratch + (ch.begin / chunk_syms) * t.slot_bytes);
+#if NZ_ENC_PTXSTORE
+            // both predicated byte stores at immediate offsets from the
+            // pointer and its decrement as one IMAD.WIDE (ptxas otherwise
+            // rebuilds each store address in 64-bit arithmetic)
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t"
+                "setp.ne.u32 p, %2, 0;\n\t"
+                "setp.ne.u32 q, %3, 0;\n\t"
+                "@p st.u8 [%0+-1], %1;\n\t"
+                "@q st.u8 [%0+-2], %4;\n\t"
+                "mad.wide.s32 %0, %5, -1, %0;\n\t}"
+                : "+l"(ch.out)
+                : "r"(x), "r"((uint32_t)n1), "r"((uint32_t)n2), "r"(x >> 8), "r"(nb)
+                : "memory");
+#else
 #if !NZ_ENC_NOSTORE  // timing experiment only: the chain without its byte stores
             if (n1) st_g(ch.out - 1, (uint8_t)x);
             if (n2) st_g(ch.out - 2, (uint8_t)(x >> 8));
 #endif
             ch.out -= nb;
+#endif
         }
         ch.emitted += nb;
         x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
