@@ -34,6 +34,9 @@
 #ifndef NZ_ENC_PTXSTORE
 #define NZ_ENC_PTXSTORE 1
 #endif
+#ifndef NZ_ENC_PTXRENORM
+#define NZ_ENC_PTXRENORM 1
+#endif
 #ifndef NZ_ENC_PF_WIN
 #define NZ_ENC_PF_WIN 4096  // symbols per L2 prefetch step (power of two, multiple of 16)
 #endif
@@ -132,6 +135,33 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
         uint32_t x = ch.x;
         const uint32_t limit = e.freq << 19;
         if constexpr (CHECK) bad |= e.freq == 0;  // ans.hpp:210-212
+#if NZ_ENC_PTXRENORM
+        if constexpr (!QUEUE) {
+            // ans.hpp:214-218 as one PTX block: emit x & 0xFF while
+            // x >= f << 19 (at most twice) -- compares, predicated byte stores
+            // at immediate offsets, the renormalised state, the byte count
+            // and the pointer decrement (one IMAD.WIDE)
+            uint32_t nb;
+            NZ_CHECK(ch.out - 2 >= t.scratch + (ch.begin / chunk_syms) * t.slot_bytes);
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+                "shr.u32 t, %1, 8;\n\t"
+                "setp.ge.u32 p, %1, %3;\n\t"
+                "setp.ge.u32 q, t, %3;\n\t"
+                "@p st.u8 [%0+-1], %1;\n\t"
+                "@q st.u8 [%0+-2], t;\n\t"
+                "selp.u32 %2, 1, 0, p;\n\t"
+                "@p mov.b32 %1, t;\n\t"
+                "@q shr.u32 %1, t, 8;\n\t"
+                "@q add.u32 %2, %2, 1;\n\t"
+                "mad.wide.s32 %0, %2, -1, %0;\n\t}"
+                : "+l"(ch.out), "+r"(x), "=r"(nb)
+                : "r"(limit)
+                : "memory");
+            ch.emitted += nb;
+        } else
+#endif
+        {
         // ans.hpp:214-218: emit x & 0xFF while x >= f << 19 -- at most twice.
         const bool n1 = x >= limit, n2 = (x >> 8) >= limit;
         const uint32_t nb = (uint32_t)n1 + (uint32_t)n2;
@@ -170,6 +200,7 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
         }
         ch.emitted += nb;
         x = n2 ? x >> 16 : (n1 ? x >> 8 : x);
+        }
         // ans.hpp:219: (x/f << 12) + x%f + cum = x + (x/f)(4096 - f) + cum,
         // with x/f exact from one 64-bit multiply and shift (x < 2^31 here)
         const uint32_t q = (uint32_t)(((uint64_t)x * e.rcp) >> e.pad);
