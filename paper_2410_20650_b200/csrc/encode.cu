@@ -37,6 +37,9 @@
 #ifndef NZ_ENC_PTXRENORM
 #define NZ_ENC_PTXRENORM 1
 #endif
+#ifndef NZ_ENC_PTXOFF
+#define NZ_ENC_PTXOFF 1
+#endif
 #ifndef NZ_ENC_PF_WIN
 #define NZ_ENC_PF_WIN 4096  // symbols per L2 prefetch step (power of two, multiple of 16)
 #endif
@@ -77,6 +80,8 @@ struct EncChain {
     uint32_t x;
     uint32_t emitted;
     uint8_t* out;     // direct byte stores: next byte goes to out[-1]
+    uint8_t* base;    // slot start; with off: out = base + off (the PTX step's form)
+    uint32_t off;
     uint32_t* wo;     // QUEUE: next word goes to wo[-1]
     uint32_t qlo, qhi, qc;
     uint64_t begin;   // first symbol of the chunk
@@ -124,6 +129,8 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
         // aligned 32-bit words.
         uint8_t* const slot_end = t.scratch + (cc + 1) * t.slot_bytes;  // 16-byte aligned
         ch.out = slot_end - 4;
+        ch.base = slot_end - t.slot_bytes;
+        ch.off = (uint32_t)t.slot_bytes - 4;
         ch.wo = reinterpret_cast<uint32_t*>(slot_end - 4);
         ch.qlo = ch.qhi = ch.qc = 0;
     };
@@ -142,6 +149,27 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
             // at immediate offsets, the renormalised state, the byte count
             // and the pointer decrement (one IMAD.WIDE)
             uint32_t nb;
+#if NZ_ENC_PTXOFF
+            // the store address as slot base + 32-bit offset: one unsigned
+            // IMAD.WIDE, where a 64-bit pointer decrement costs four
+            NZ_CHECK(ch.off >= 2);
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t.reg .b64 a;\n\t"
+                "mad.wide.u32 a, %0, 1, %4;\n\t"
+                "shr.u32 t, %1, 8;\n\t"
+                "setp.ge.u32 p, %1, %3;\n\t"
+                "setp.ge.u32 q, t, %3;\n\t"
+                "@p st.u8 [a+-1], %1;\n\t"
+                "@q st.u8 [a+-2], t;\n\t"
+                "selp.u32 %2, 1, 0, p;\n\t"
+                "@p mov.b32 %1, t;\n\t"
+                "@q shr.u32 %1, t, 8;\n\t"
+                "@q add.u32 %2, %2, 1;\n\t"
+                "sub.u32 %0, %0, %2;\n\t}"
+                : "+r"(ch.off), "+r"(x), "=r"(nb)
+                : "r"(limit), "l"(ch.base)
+                : "memory");
+#else
             NZ_CHECK(ch.out - 2 >= t.scratch + (ch.begin / chunk_syms) * t.slot_bytes);
             asm volatile(
                 "{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
@@ -158,6 +186,7 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
                 : "+l"(ch.out), "+r"(x), "=r"(nb)
                 : "r"(limit)
                 : "memory");
+#endif
             ch.emitted += nb;
         } else
 #endif
