@@ -31,6 +31,11 @@ cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, uns
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
+cudaError_t launch_stream_copy_batch(const void* jobs, int njobs, uint64_t total_chunks, uint64_t slot_bytes,
+                                     cudaStream_t s);
+size_t stream_copy_job_bytes();
+void stream_copy_job_fill(void* at, const uint8_t* scratch, const uint4* chunk_info, uint8_t* stream,
+                          const uint8_t* hdr, uint64_t chunk0);
 cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTask& one, uint64_t total_units,
                                   cudaStream_t s);
 cudaError_t launch_encode(bool queue, bool check, unsigned ctas, unsigned threads, const EncTask* tasks, int ntasks,
@@ -901,6 +906,11 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         if (int rc = arena_alloc(stotal, stream_arena, s)) return rc;
     }
     mark("str arena");
+    // K4 copies: one launch for every chunk of the batch (the job table goes
+    // where the encode tasks were: every kernel reading those is queued before)
+    const size_t jb = stream_copy_job_bytes();
+    std::vector<uint8_t> jobs(count > 1 ? count * jb : 0);
+    uint64_t chunks_total = 0;
     for (int i = 0; i < count; ++i) {
         nzgpu_blob_s* b = bs[i];
         if (stream_arena) {
@@ -909,9 +919,20 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         } else {
             CK(dev_alloc(reinterpret_cast<void**>(&b->stream), align_up(b->stream_len, 16) + 32, s));
         }
-        CK(cudaMemcpyAsync(b->stream, tasks[i].hdr, 4, cudaMemcpyDeviceToDevice, s));
-        stream_copy_kernel<<<(unsigned)b->nchunks, 256, 0, s>>>(tasks[i].scratch, slot, b->chunk_info, b->stream);
-        CK(cudaGetLastError());
+        if (count > 1) {
+            stream_copy_job_fill(jobs.data() + i * jb, tasks[i].scratch, b->chunk_info, b->stream, tasks[i].hdr,
+                                 chunks_total);
+            chunks_total += b->nchunks;
+        } else {
+            CK(cudaMemcpyAsync(b->stream, tasks[i].hdr, 4, cudaMemcpyDeviceToDevice, s));
+            stream_copy_kernel<<<(unsigned)b->nchunks, 256, 0, s>>>(tasks[i].scratch, slot, b->chunk_info, b->stream);
+            CK(cudaGetLastError());
+        }
+    }
+    if (count > 1) {
+        static_assert(sizeof(EncTask) >= 40, "the job table reuses the task table's space");
+        CK(cudaMemcpyAsync(tmp + L.tasks, jobs.data(), jobs.size(), cudaMemcpyHostToDevice, s));
+        CK(launch_stream_copy_batch(tmp + L.tasks, count, chunks_total, slot, s));
     }
     mark("streams");
     // the readback arrays (6 pointers and 6 words per blob) are free again

@@ -14,6 +14,7 @@
 //    sub-range), writes exponents into the warp's padded smem tile, and the
 //    same warp then merges the unit with coalesced 16-byte stores -- so
 //    decode (ALU/shared) of some warps overlaps merge (HBM) of others.
+#include <algorithm>
 #include <type_traits>
 
 #include "decode_common.cuh"

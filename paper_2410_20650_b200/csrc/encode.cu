@@ -463,6 +463,66 @@ __global__ void __launch_bounds__(256) stream_copy_kernel(const uint8_t* __restr
     for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
 }
 
+// K4 copy of many tensors in one launch: block b copies chunk b - chunk0 of
+// the job whose chunk range holds it (binary search); a tensor's first block
+// also writes its stream's leading u32 chunk count.
+struct StreamCopyJob {
+    const uint8_t* scratch;
+    const uint4* chunk_info;
+    uint8_t* stream;
+    const uint8_t* hdr;
+    uint64_t chunk0;
+};
+
+__global__ void __launch_bounds__(256) stream_copy_batch_kernel(const StreamCopyJob* __restrict__ jobs, int njobs,
+                                                                uint64_t slot_bytes) {
+    int lo = 0, hi = njobs - 1;
+    const uint64_t blk = blockIdx.x;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (jobs[mid].chunk0 <= blk) lo = mid; else hi = mid - 1;
+    }
+    const StreamCopyJob j = jobs[lo];
+    const uint64_t c = blk - j.chunk0;
+    if (c == 0 && threadIdx.x < 4) j.stream[threadIdx.x] = j.hdr[threadIdx.x];
+    const uint4 ci = j.chunk_info[c];
+    const uint64_t off = (uint64_t)ci.x | ((uint64_t)ci.y << 32);
+    const uint32_t len = ci.z;
+    const uint8_t* src = j.scratch + (c + 1) * slot_bytes - len;
+    uint8_t* dst = j.stream + off;
+    if (threadIdx.x < 8) {
+        const uint32_t v = threadIdx.x < 4 ? ci.w : len;
+        dst[-8 + (int)threadIdx.x] = (uint8_t)(v >> (8 * (threadIdx.x & 3)));
+    }
+    const uint32_t head = (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3);
+    for (uint32_t i = threadIdx.x; i < min(head, len); i += blockDim.x) dst[i] = src[i];
+    if (len <= head) return;
+    const uint32_t body = (len - head) / 4;
+    const uint8_t* sb = src + head;
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst + head);
+    const uint32_t mis = (uint32_t)((uintptr_t)sb & 3);
+    const uint32_t* sa = reinterpret_cast<const uint32_t*>(sb - mis);
+    for (uint32_t w = threadIdx.x; w < body; w += blockDim.x) {
+        const uint32_t lo32 = __ldg(sa + w);
+        const uint32_t hi32 = mis ? __ldg(sa + w + 1) : 0u;
+        d[w] = mis ? __funnelshift_r(lo32, hi32, 8 * mis) : lo32;
+    }
+    for (uint32_t i = head + body * 4 + threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_stream_copy_batch(const void* jobs, int njobs, uint64_t total_chunks, uint64_t slot_bytes,
+                                     cudaStream_t s) {
+    if (!total_chunks) return cudaSuccess;
+    stream_copy_batch_kernel<<<(unsigned)total_chunks, 256, 0, s>>>(static_cast<const StreamCopyJob*>(jobs), njobs,
+                                                                   slot_bytes);
+    return cudaGetLastError();
+}
+size_t stream_copy_job_bytes() { return sizeof(StreamCopyJob); }
+void stream_copy_job_fill(void* at, const uint8_t* scratch, const uint4* chunk_info, uint8_t* stream,
+                          const uint8_t* hdr, uint64_t chunk0) {
+    *static_cast<StreamCopyJob*>(at) = StreamCopyJob{scratch, chunk_info, stream, hdr, chunk0};
+}
+
 cudaError_t launch_index_finalize(const EncTask* tasks, int ntasks, const EncTask& one, uint64_t total_units,
                                   cudaStream_t s) {
     if (!total_units) return cudaSuccess;
