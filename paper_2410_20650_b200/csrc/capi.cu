@@ -67,6 +67,8 @@ cudaError_t launch_decode_persist(int log2k, int precision, const DecodeDesc* de
 uint32_t persist_resident_ctas(int log2k, uint32_t win_cap);
 bool persist_fits(int log2k, uint32_t win_cap);
 cudaError_t launch_unit_window_max(int log2k, const DecodeDesc& d, uint32_t* out, cudaStream_t s);
+cudaError_t launch_windows_batch(int log2k, const DecodeDesc* descs, int count, uint32_t tile_subs, uint64_t max_units,
+                                 uint32_t* out, cudaStream_t s);
 // entropy.cu
 __global__ void component_hist_kernel(const uint16_t*, uint64_t, unsigned long long*);
 // crc32.cu
@@ -452,7 +454,43 @@ int install_table(nzgpu_blob_s* b, const uint16_t* h_freqs, cudaStream_t s) {
 // decoders' shared-memory windows): the window kernels of every blob, then one
 // readback.
 int compute_windows(nzgpu_blob_s* const* bs, int count, cudaStream_t s, uint8_t* scratch_ptrs = nullptr,
-                    uint32_t* scratch_res = nullptr) {
+                    uint32_t* scratch_res = nullptr, uint8_t* scratch_descs = nullptr) {
+    // A compress batch (device scratch for a descriptor table given): one
+    // launch for every window maximum of one stride, where the per-tensor
+    // form costs a memset and two launches per tensor
+    if (scratch_descs && scratch_res && count > 1) {
+        std::vector<DecodeDesc> ds;
+        std::vector<int> idx;
+        int log2k = -1;
+        bool same = true;
+        uint64_t max_units = 0;
+        for (int i = 0; i < count; ++i) {
+            nzgpu_blob_s* b = bs[i];
+            b->max_window = b->max_window_unit = 0;
+            if ((b->flags & kFlagIrregular) || b->nsub == 0 || (b->flags & kFlagSingleSymbol)) continue;
+            if (log2k >= 0 && b->log2k != log2k) same = false;
+            log2k = b->log2k;
+            ds.push_back(b->desc(nullptr));
+            idx.push_back(i);
+            max_units = std::max<uint64_t>(max_units, ceil_div(b->nsub, 32));
+        }
+        if (ds.empty()) return NZGPU_OK;
+        if (same) {
+            auto* d_descs = reinterpret_cast<DecodeDesc*>(scratch_descs);
+            CK(cudaMemcpyAsync(d_descs, ds.data(), ds.size() * sizeof(DecodeDesc), cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(scratch_res, 0, ds.size() * 8, s));
+            CK(launch_windows_batch(log2k, d_descs, (int)ds.size(), (uint32_t)decode_tile_subs(), max_units,
+                                    scratch_res, s));
+            std::vector<uint32_t> w(ds.size() * 2);
+            CK(cudaMemcpyAsync(w.data(), scratch_res, w.size() * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));  // w is a host stack vector
+            for (size_t j = 0; j < idx.size(); ++j) {
+                bs[idx[j]]->max_window_unit = w[2 * j];
+                bs[idx[j]]->max_window = w[2 * j + 1];
+            }
+            return NZGPU_OK;
+        }
+    }
     std::vector<const uint32_t*> ptrs;
     std::vector<int> who;
     for (int i = 0; i < count; ++i) {
@@ -936,7 +974,8 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     }
     mark("streams");
     // the readback arrays (6 pointers and 6 words per blob) are free again
-    const int rc = compute_windows(bs, count, s, tmp + L.ptrs, reinterpret_cast<uint32_t*>(tmp + L.res));
+    static_assert(sizeof(EncTask) >= sizeof(DecodeDesc), "the descriptor table reuses the task table's space");
+    const int rc = compute_windows(bs, count, s, tmp + L.ptrs, reinterpret_cast<uint32_t*>(tmp + L.res), tmp + L.tasks);
     // a caller's workspace must be free to reuse when this returns
     if (ws) CK(cudaStreamSynchronize(s));
     mark("windows");

@@ -1002,6 +1002,51 @@ __global__ void unit_window_max_kernel(DecodeDesc d, uint32_t* __restrict__ out)
     atomicMax(out, best);
 }
 
+// Both window maxima (per 32-sub-range unit for the persistent kernel, per
+// `tile_subs`-sub-range tile for the tiles kernel) of many tensors in one
+// launch: blockIdx.y picks the tensor, out[2y] / out[2y + 1] receive them
+// (zeroed by the caller).
+template <int LOG2K>
+__global__ void windows_batch_kernel(const DecodeDesc* __restrict__ descs, uint32_t tile_subs,
+                                     uint32_t* __restrict__ out) {
+    const DecodeDesc d = descs[blockIdx.y];
+    const uint32_t nsub = (uint32_t)ceil_div(d.n, 1u << LOG2K);
+    const uint32_t units = (nsub + 31) / 32, tiles = (nsub + tile_subs - 1) / tile_subs;
+    uint32_t bu = 0, bt = 0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < units; t += stride) {
+        uint64_t a, b;
+        tile_window(d, t * 32, min(32u, nsub - t * 32), LOG2K, nsub, a, b);
+        bu = max(bu, (uint32_t)min((uint64_t)(((b + 15) & ~15ull) - (a & ~15ull)), (uint64_t)0xFFFFFFFFu));
+    }
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += stride) {
+        uint64_t a, b;
+        tile_window(d, t * tile_subs, min(tile_subs, nsub - t * tile_subs), LOG2K, nsub, a, b);
+        bt = max(bt, (uint32_t)min((uint64_t)(((b + 15) & ~15ull) - (a & ~15ull)), (uint64_t)0xFFFFFFFFu));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        bu = max(bu, __shfl_xor_sync(0xFFFFFFFFu, bu, o));
+        bt = max(bt, __shfl_xor_sync(0xFFFFFFFFu, bt, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bu) atomicMax(out + 2 * blockIdx.y, bu);
+        if (bt) atomicMax(out + 2 * blockIdx.y + 1, bt);
+    }
+}
+
+cudaError_t launch_windows_batch(int log2k, const DecodeDesc* descs, int count, uint32_t tile_subs, uint64_t max_units,
+                                 uint32_t* out, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(max_units, 256), 148)), (unsigned)count);
+    switch (log2k) {
+        case 6: windows_batch_kernel<6><<<grid, 256, 0, s>>>(descs, tile_subs, out); break;
+        case 7: windows_batch_kernel<7><<<grid, 256, 0, s>>>(descs, tile_subs, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ launchers --
 template <int LOG2K, int P>
 static cudaError_t launch_p(const DecodeDesc* descs, int ndesc, const uint32_t* cta_prefix, const DecodeDesc& one,
