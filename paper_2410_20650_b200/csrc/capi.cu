@@ -31,6 +31,10 @@ cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, uns
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
+size_t split_task_bytes();
+void split_task_fill(void* at, const uint16_t* v, uint64_t n, uint8_t* exps, uint8_t* signmant,
+                     unsigned long long* counts, uint32_t* err);
+cudaError_t launch_split_hist_batch(const void* tasks, int count, uint64_t max_n, cudaStream_t s);
 cudaError_t launch_stream_copy_batch(const void* jobs, int njobs, uint64_t total_chunks, uint64_t slot_bytes,
                                      cudaStream_t s);
 size_t stream_copy_job_bytes();
@@ -84,6 +88,9 @@ namespace {
 #define NZ_ENC_QUEUE_MIN_CTAS 600
 #endif
 constexpr uint32_t kEncQueueMinCtas = NZ_ENC_QUEUE_MIN_CTAS;
+#ifndef NZ_K1_BATCH
+#define NZ_K1_BATCH 1
+#endif
 #ifndef NZ_ENC_CHECK_OWN
 #define NZ_ENC_CHECK_OWN false  // compress: the frequency check is redundant with the histogram's table
 #endif
@@ -841,6 +848,12 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     mark("blob alloc");
     std::vector<EncTask> tasks(count);
     std::vector<TableTask> tables(count);
+    // lossless batches: K1 (and the zeroing of histograms and error words)
+    // for every tensor in one launch; its task table uses the encode task
+    // table's space, which is only written after it
+    const bool batched_k1 = precision == 7 && count > 1 && NZ_K1_BATCH;
+    std::vector<uint8_t> split_tasks(batched_k1 ? count * split_task_bytes() : 0);
+    uint64_t max_n = 0;
     uint32_t ctas = 0;
     uint64_t units = 0;  // warp units of every tensor's side index (index_finalize_kernel)
     for (int i = 0; i < count; ++i) {
@@ -855,9 +868,15 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         uint8_t* exps = tmp + L.to[i].exps;
         auto* counts = reinterpret_cast<unsigned long long*>(tmp + L.to[i].counts);
         auto* enc = reinterpret_cast<EncSym*>(tmp + L.to[i].enc);
-        CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
-        CK(cudaMemsetAsync(b->err, 0, 64, s));
-        if (precision == 7) {
+        if (batched_k1) {  // K1 of the whole batch in one launch after this loop
+            split_task_fill(split_tasks.data() + i * split_task_bytes(), vs[i], n, exps, b->mant, counts, b->err);
+            max_n = std::max<uint64_t>(max_n, n);
+        } else {
+            CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
+            CK(cudaMemsetAsync(b->err, 0, 64, s));
+        }
+        if (batched_k1) {
+        } else if (precision == 7) {
             CK(launch_split_hist(vs[i], n, exps, b->mant, counts, s));
         } else {
             uint8_t* items = tmp + L.to[i].items;
@@ -893,8 +912,13 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     // Byte queue once L1 store sectors rather than the chain latency bound
     // the launch: >= ~4 chains per SM (crossover measured at 416-832 chains).
     const bool queue = ctas >= kEncQueueMinCtas;
-    mark("setup");
     auto* d_tasks = reinterpret_cast<EncTask*>(tmp + L.tasks);
+    if (batched_k1) {
+        static_assert(sizeof(EncTask) >= 48, "the K1 task table reuses the encode task table's space");
+        CK(cudaMemcpyAsync(d_tasks, split_tasks.data(), split_tasks.size(), cudaMemcpyHostToDevice, s));
+        CK(launch_split_hist_batch(d_tasks, count, max_n, s));
+    }
+    mark("setup");
     if (count > 1) {
         auto* d_tables = reinterpret_cast<TableTask*>(tmp + L.tables);
         CK(cudaMemcpyAsync(d_tables, tables.data(), count * sizeof(TableTask), cudaMemcpyHostToDevice, s));

@@ -90,11 +90,12 @@ __global__ void __launch_bounds__(256) split_hist_kernel(const uint16_t* __restr
 // warp-aggregated atomics (layout: kLaneHistWarps, nzgpu_internal.cuh).
 constexpr int kLaneUnroll = 8;
 
-__global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(const uint16_t* __restrict__ v,
-                                                                              uint64_t n,
-                                                                              uint8_t* __restrict__ exps,
-                                                                              uint8_t* __restrict__ signmant,
-                                                                              unsigned long long* __restrict__ counts) {
+// K1 body over one tensor for CTA `bx` of `gx` (the single-tensor launch and
+// the batched launch below share it).
+__device__ __forceinline__ void split_hist_lane_body(const uint16_t* __restrict__ v, uint64_t n,
+                                                     uint8_t* __restrict__ exps, uint8_t* __restrict__ signmant,
+                                                     unsigned long long* __restrict__ counts, uint32_t bx,
+                                                     uint32_t gx) {
     extern __shared__ uint32_t lh[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < (int)(kLaneHistSmem / 4); i += blockDim.x) lh[i] = 0;
@@ -106,9 +107,9 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(co
     // keeps kLaneUnroll 16-byte loads in flight to cover HBM latency.
     // The next batch's loads are issued before this batch is processed, so a
     // warp's loads stay in flight while it splits and counts.
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t stride = (uint64_t)gx * blockDim.x;
     uint4 nx[kLaneUnroll];
-    const uint64_t gfirst = blockIdx.x * (uint64_t)blockDim.x + tid;
+    const uint64_t gfirst = bx * (uint64_t)blockDim.x + tid;
 #pragma unroll
     for (int k = 0; k < kLaneUnroll; ++k)
         if (gfirst + k * stride < groups) nx[k] = __ldcs(v4 + gfirst + k * stride);
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(co
             for (int b = 0; b < 4; ++b) h[((e8.y >> (8 * b)) & 0xFFu) * 32] += 1;
         }
     }
-    if (blockIdx.x == 0 && tid < (n & 7)) {  // tail (n % 8 elements)
+    if (bx == 0 && tid < (n & 7)) {  // tail (n % 8 elements)
         const uint64_t i = groups * 8 + tid;
         const uint32_t b = v[i];
         const uint32_t e = (b >> 7) & 0xFFu;
@@ -144,6 +145,57 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(co
     }
     __syncthreads();
     lane_hist_flush(lh, counts);
+}
+
+__global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_kernel(const uint16_t* __restrict__ v,
+                                                                              uint64_t n,
+                                                                              uint8_t* __restrict__ exps,
+                                                                              uint8_t* __restrict__ signmant,
+                                                                              unsigned long long* __restrict__ counts) {
+    split_hist_lane_body(v, n, exps, signmant, counts, blockIdx.x, gridDim.x);
+}
+
+// K1 of a whole compress batch in one launch (blockIdx.y = tensor): the
+// small tensors (norms, the k/v projections) no longer cost a launch each.
+struct SplitTask {
+    const uint16_t* v;
+    uint64_t n;
+    uint8_t* exps;
+    uint8_t* signmant;
+    unsigned long long* counts;
+    uint32_t* err;
+};
+
+__global__ void __launch_bounds__(kLaneHistWarps * 32) split_hist_lane_batch_kernel(const SplitTask* __restrict__ tasks) {
+    const SplitTask t = tasks[blockIdx.y];
+    split_hist_lane_body(t.v, t.n, t.exps, t.signmant, t.counts, blockIdx.x, gridDim.x);
+}
+
+// The batch's histograms and error words zeroed in one launch (block = task).
+__global__ void zero_split_tasks_kernel(const SplitTask* __restrict__ tasks) {
+    const SplitTask t = tasks[blockIdx.x];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) t.counts[i] = 0ull;
+    if (threadIdx.x < 16) t.err[threadIdx.x] = 0u;
+}
+
+size_t split_task_bytes() { return sizeof(SplitTask); }
+void split_task_fill(void* at, const uint16_t* v, uint64_t n, uint8_t* exps, uint8_t* signmant,
+                     unsigned long long* counts, uint32_t* err) {
+    *static_cast<SplitTask*>(at) = SplitTask{v, n, exps, signmant, counts, err};
+}
+
+cudaError_t launch_split_hist_batch(const void* tasks, int count, uint64_t max_n, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    static SmemAttr attr;
+    if (cudaError_t e = attr.ensure((const void*)split_hist_lane_batch_kernel, kLaneHistSmem)) return e;
+    const auto* t = static_cast<const SplitTask*>(tasks);
+    zero_split_tasks_kernel<<<count, 256, 0, s>>>(t);
+    const uint64_t threads = kLaneHistWarps * 32;
+    const uint64_t want = ceil_div(max_n / 8 + 1, threads);
+    const uint64_t need = ceil_div(max_n, threads * kLaneMax);  // 16-bit counters
+    const uint64_t gx = std::max<uint64_t>(need, std::min<uint64_t>(want, 148 * 3));
+    split_hist_lane_batch_kernel<<<dim3((unsigned)gx, (unsigned)count), (unsigned)threads, kLaneHistSmem, s>>>(t);
+    return cudaGetLastError();
 }
 
 #ifndef NZ_HIST_LANE
