@@ -40,6 +40,9 @@
 #ifndef NZ_ENC_PTXOFF
 #define NZ_ENC_PTXOFF 1
 #endif
+#ifndef NZ_ENC_PTXQUEUE
+#define NZ_ENC_PTXQUEUE 1
+#endif
 #ifndef NZ_ENC_PF_WIN
 #define NZ_ENC_PF_WIN 4096  // symbols per L2 prefetch step (power of two, multiple of 16)
 #endif
@@ -142,6 +145,42 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
         uint32_t x = ch.x;
         const uint32_t limit = e.freq << 19;
         if constexpr (CHECK) bad |= e.freq == 0;  // ans.hpp:210-212
+#if NZ_ENC_PTXQUEUE
+        if constexpr (QUEUE) {
+            // The byte queue as one branch-free PTX block: the renormalising
+            // compares, the queue shift (two wrap funnel shifts), and -- when
+            // four bytes are queued -- the word store at slot base + 32-bit
+            // offset, all predicated (the C++ form branched per lane)
+            uint32_t nb;
+            NZ_CHECK(ch.off >= 4);
+            asm volatile(
+                "{\n\t.reg .pred p, q, w;\n\t.reg .b32 t, s8, sh, wd;\n\t.reg .b64 a;\n\t"
+                "shr.u32 t, %1, 8;\n\t"
+                "setp.ge.u32 p, %1, %6;\n\t"
+                "setp.ge.u32 q, t, %6;\n\t"
+                "selp.u32 %5, 1, 0, p;\n\t"
+                "@q add.u32 %5, %5, 1;\n\t"
+                "shl.b32 s8, %5, 3;\n\t"
+                "shf.r.wrap.b32 %2, %2, %3, s8;\n\t"
+                "shf.r.wrap.b32 %3, %3, %1, s8;\n\t"
+                "add.u32 %4, %4, %5;\n\t"
+                "setp.ge.u32 w, %4, 4;\n\t"
+                "shl.b32 sh, %4, 3;\n\t"
+                "sub.u32 sh, 64, sh;\n\t"
+                "shf.r.clamp.b32 wd, %2, %3, sh;\n\t"
+                "prmt.b32 wd, wd, 0, 0x0123;\n\t"
+                "mad.wide.u32 a, %0, 1, %7;\n\t"
+                "@w st.u32 [a+-4], wd;\n\t"
+                "@w sub.u32 %0, %0, 4;\n\t"
+                "@w sub.u32 %4, %4, 4;\n\t"
+                "@p mov.b32 %1, t;\n\t"
+                "@q shr.u32 %1, t, 8;\n\t}"
+                : "+r"(ch.off), "+r"(x), "+r"(ch.qlo), "+r"(ch.qhi), "+r"(ch.qc), "=r"(nb)
+                : "r"(limit), "l"(ch.base)
+                : "memory");
+            ch.emitted += nb;
+        } else
+#endif
 #if NZ_ENC_PTXRENORM
         if constexpr (!QUEUE) {
             // ans.hpp:214-218 as one PTX block: emit x & 0xFF while
@@ -249,6 +288,9 @@ __global__ void __launch_bounds__(QUEUE ? 128 : NZ_ENC_THREADS, QUEUE ? 0 : 1) a
         uint8_t* const slot_end = t.scratch + (cc + 1) * t.slot_bytes;
         // The last 1-3 queued bytes: one word whose low (4 - qc) bytes lie
         // below the payload start, inside the slot.
+#if NZ_ENC_PTXQUEUE
+        if (QUEUE) ch.wo = reinterpret_cast<uint32_t*>(ch.base + ch.off);  // the PTX queue step's position
+#endif
         if (QUEUE && ch.qc) *--ch.wo = __byte_perm(ch.qhi, 0, 0x0123) << (32 - 8 * ch.qc);
         // ans.hpp:223: final state little-endian at the tail (aligned store).
         *reinterpret_cast<uint32_t*>(slot_end - 4) = ch.x;
