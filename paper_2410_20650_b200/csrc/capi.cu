@@ -31,6 +31,12 @@ cudaError_t launch_split_hist(const uint16_t*, uint64_t, uint8_t*, uint8_t*, uns
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 __global__ void build_table_kernel(const unsigned long long*, const uint16_t*, uint16_t*, EncSym*, uint32_t*,
                                    uint32_t*);
+size_t lossy_task_bytes();
+void lossy_task_fill(void* at, const uint16_t* v, uint64_t nfull, uint8_t* scales, uint8_t* exps, uint8_t* packed,
+                     unsigned long long* counts, uint32_t* err);
+bool lossy_batchable(uint64_t n, int k, uint32_t block);
+cudaError_t launch_lossy_prep_batch(const void* tasks, int count, int k, uint32_t block, uint64_t max_nfull,
+                                    cudaStream_t s);
 size_t split_task_bytes();
 void split_task_fill(void* at, const uint16_t* v, uint64_t n, uint8_t* exps, uint8_t* signmant,
                      unsigned long long* counts, uint32_t* err);
@@ -854,6 +860,10 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
     const bool batched_k1 = precision == 7 && count > 1 && NZ_K1_BATCH;
     std::vector<uint8_t> split_tasks(batched_k1 ? count * split_task_bytes() : 0);
     uint64_t max_n = 0;
+    // lossy batches whose every tensor is whole fused blocks: K6 likewise
+    bool batched_k6 = precision != 7 && count > 1 && NZ_K1_BATCH;
+    for (int i = 0; batched_k6 && i < count; ++i) batched_k6 = lossy_batchable(ns[i], precision, block);
+    std::vector<uint8_t> lossy_tasks(batched_k6 ? count * lossy_task_bytes() : 0);
     uint32_t ctas = 0;
     uint64_t units = 0;  // warp units of every tensor's side index (index_finalize_kernel)
     for (int i = 0; i < count; ++i) {
@@ -871,11 +881,15 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         if (batched_k1) {  // K1 of the whole batch in one launch after this loop
             split_task_fill(split_tasks.data() + i * split_task_bytes(), vs[i], n, exps, b->mant, counts, b->err);
             max_n = std::max<uint64_t>(max_n, n);
+        } else if (batched_k6) {
+            lossy_task_fill(lossy_tasks.data() + i * lossy_task_bytes(), vs[i], n / block, b->scales, exps, b->mant,
+                            counts, b->err);
+            max_n = std::max<uint64_t>(max_n, n / block);
         } else {
             CK(cudaMemsetAsync(counts, 0, 256 * 8, s));
             CK(cudaMemsetAsync(b->err, 0, 64, s));
         }
-        if (batched_k1) {
+        if (batched_k1 || batched_k6) {
         } else if (precision == 7) {
             CK(launch_split_hist(vs[i], n, exps, b->mant, counts, s));
         } else {
@@ -917,6 +931,10 @@ int compress_many(nzgpu_blob_s* const* bs, const uint16_t* const* vs, const uint
         static_assert(sizeof(EncTask) >= 48, "the K1 task table reuses the encode task table's space");
         CK(cudaMemcpyAsync(d_tasks, split_tasks.data(), split_tasks.size(), cudaMemcpyHostToDevice, s));
         CK(launch_split_hist_batch(d_tasks, count, max_n, s));
+    } else if (batched_k6) {
+        static_assert(sizeof(EncTask) >= 56, "the K6 task table reuses the encode task table's space");
+        CK(cudaMemcpyAsync(d_tasks, lossy_tasks.data(), lossy_tasks.size(), cudaMemcpyHostToDevice, s));
+        CK(launch_lossy_prep_batch(d_tasks, count, precision, block, max_n, s));
     }
     mark("setup");
     if (count > 1) {

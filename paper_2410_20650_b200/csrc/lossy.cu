@@ -36,6 +36,10 @@ __device__ __forceinline__ float div_coef(float ax, float c, float rc) {
 #endif
 }
 
+#ifndef NZ_LOSSY_FUSED
+#define NZ_LOSSY_FUSED 1
+#endif
+
 // round_mantissa (bitfloat.hpp:82-98) + carry rule (tensorstore.hpp:184-194).
 // The division runs on the magnitude; c > 0, so the sign is the input's and
 // the quotient is finite and non-negative (inputs are finite), so the FP32 ->
@@ -140,14 +144,22 @@ __global__ void unpack_items_kernel(const uint8_t* __restrict__ packed, uint64_t
 // packed written.  Exponents are counted in lane-private shared counters.
 constexpr int kFusedLoads = 8;  // uint4 loads in flight per lane
 
+// One tensor's share of K6 (the single launch and the batched one below).
+struct LossyTask {
+    const uint16_t* v;
+    uint64_t nfull;
+    uint8_t* scales;
+    uint8_t* exps;
+    uint8_t* packed;
+    unsigned long long* counts;
+    uint32_t* err;
+};
+
 template <int E, int K>
-__global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const uint16_t* __restrict__ v,
-                                                                          uint64_t nfull,
-                                                                          uint8_t* __restrict__ scales,
-                                                                          uint8_t* __restrict__ exps,
-                                                                          uint8_t* __restrict__ packed,
-                                                                          unsigned long long* __restrict__ counts,
-                                                                          uint32_t* __restrict__ err) {
+__device__ __forceinline__ void lossy_fused_body(const uint16_t* __restrict__ v, uint64_t nfull,
+                                                 uint8_t* __restrict__ scales, uint8_t* __restrict__ exps,
+                                                 uint8_t* __restrict__ packed, unsigned long long* __restrict__ counts,
+                                                 uint32_t* __restrict__ err, uint32_t bx, uint32_t gx) {
     constexpr int Q = E / 8;                                      // uint4 per lane per block
     constexpr int U = kFusedLoads / Q > 0 ? kFusedLoads / Q : 1;  // blocks per warp iteration
     constexpr uint64_t B = 32 * E;
@@ -157,8 +169,8 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const 
     for (int i = tid; i < (int)(kLaneHistSmem / 4); i += blockDim.x) lh[i] = 0;
     __syncthreads();
     uint16_t* h = reinterpret_cast<uint16_t*>(lh) + warp * 256 * 32 + lane;
-    const uint64_t nw = (uint64_t)gridDim.x * kLaneHistWarps;
-    for (uint64_t g = blockIdx.x * (uint64_t)kLaneHistWarps + warp; g * U < nfull; g += nw) {
+    const uint64_t nw = (uint64_t)gx * kLaneHistWarps;
+    for (uint64_t g = bx * (uint64_t)kLaneHistWarps + warp; g * U < nfull; g += nw) {
         uint4 w[U][Q];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -221,6 +233,30 @@ __global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const 
 }
 
 template <int E, int K>
+__global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_kernel(const uint16_t* __restrict__ v,
+                                                                          uint64_t nfull,
+                                                                          uint8_t* __restrict__ scales,
+                                                                          uint8_t* __restrict__ exps,
+                                                                          uint8_t* __restrict__ packed,
+                                                                          unsigned long long* __restrict__ counts,
+                                                                          uint32_t* __restrict__ err) {
+    lossy_fused_body<E, K>(v, nfull, scales, exps, packed, counts, err, blockIdx.x, gridDim.x);
+}
+
+// K6 of a whole compress batch in one launch (blockIdx.y = tensor).
+template <int E, int K>
+__global__ void __launch_bounds__(kLaneHistWarps * 32) lossy_fused_batch_kernel(const LossyTask* __restrict__ tasks) {
+    const LossyTask t = tasks[blockIdx.y];
+    lossy_fused_body<E, K>(t.v, t.nfull, t.scales, t.exps, t.packed, t.counts, t.err, blockIdx.x, gridDim.x);
+}
+
+__global__ void zero_lossy_tasks_kernel(const LossyTask* __restrict__ tasks) {
+    const LossyTask t = tasks[blockIdx.x];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) t.counts[i] = 0ull;
+    if (threadIdx.x < 16) t.err[threadIdx.x] = 0u;
+}
+
+template <int E, int K>
 static cudaError_t launch_fused(const uint16_t* v, uint64_t nfull, uint8_t* scales, uint8_t* exps, uint8_t* packed,
                                 unsigned long long* counts, uint32_t* err, cudaStream_t s) {
     static SmemAttr attr;
@@ -245,11 +281,53 @@ static cudaError_t launch_fused_k(int k, const uint16_t* v, uint64_t nfull, uint
     }
 }
 
+template <int E, int K>
+static cudaError_t launch_fused_batch(const LossyTask* tasks, int count, uint64_t max_nfull, cudaStream_t s) {
+    static SmemAttr attr;
+    if (cudaError_t e = attr.ensure((const void*)lossy_fused_batch_kernel<E, K>, kLaneHistSmem)) return e;
+    constexpr uint64_t U = kFusedLoads / (E / 8) > 0 ? kFusedLoads / (E / 8) : 1;
+    const uint64_t per_warp = kLaneMax / E;
+    const uint64_t need = ceil_div(ceil_div(max_nfull, per_warp), kLaneHistWarps);
+    const uint64_t want = ceil_div(ceil_div(max_nfull, U), kLaneHistWarps);
+    const uint64_t gx = std::max<uint64_t>(need, std::min<uint64_t>(want, 148 * 3));
+    zero_lossy_tasks_kernel<<<count, 256, 0, s>>>(tasks);
+    lossy_fused_batch_kernel<E, K><<<dim3((unsigned)gx, (unsigned)count), kLaneHistWarps * 32, kLaneHistSmem, s>>>(tasks);
+    return cudaGetLastError();
+}
+
+template <int E>
+static cudaError_t launch_fused_batch_k(int k, const LossyTask* tasks, int count, uint64_t max_nfull, cudaStream_t s) {
+    switch (k) {
+        case 0: return launch_fused_batch<E, 0>(tasks, count, max_nfull, s);
+        case 1: return launch_fused_batch<E, 1>(tasks, count, max_nfull, s);
+        default: return launch_fused_batch<E, 3>(tasks, count, max_nfull, s);
+    }
+}
+
+size_t lossy_task_bytes() { return sizeof(LossyTask); }
+void lossy_task_fill(void* at, const uint16_t* v, uint64_t nfull, uint8_t* scales, uint8_t* exps, uint8_t* packed,
+                     unsigned long long* counts, uint32_t* err) {
+    *static_cast<LossyTask*>(at) = LossyTask{v, nfull, scales, exps, packed, counts, err};
+}
+bool lossy_batchable(uint64_t n, int k, uint32_t block) {
+    return NZ_LOSSY_FUSED && (block == 256 || block == 512 || block == 1024 || block == 2048) &&
+           (k == 0 || k == 1 || k == 3) && n % block == 0;
+}
+// K6 (with the histograms and error words zeroed) of every tensor of a
+// lossy batch in one launch; every tensor must be lossy_batchable.
+cudaError_t launch_lossy_prep_batch(const void* tasks, int count, int k, uint32_t block, uint64_t max_nfull,
+                                    cudaStream_t s) {
+    const auto* t = static_cast<const LossyTask*>(tasks);
+    switch (block) {
+        case 256: return launch_fused_batch_k<8>(k, t, count, max_nfull, s);
+        case 512: return launch_fused_batch_k<16>(k, t, count, max_nfull, s);
+        case 1024: return launch_fused_batch_k<32>(k, t, count, max_nfull, s);
+        default: return launch_fused_batch_k<64>(k, t, count, max_nfull, s);
+    }
+}
+
 __global__ void byte_hist_kernel(const uint8_t*, uint64_t, unsigned long long*);
 
-#ifndef NZ_LOSSY_FUSED
-#define NZ_LOSSY_FUSED 1
-#endif
 
 // K6 launcher: scales, exponent plane + histogram, packed (sign, mantissa)
 // items.  Full blocks of B in {256, 512, 1024, 2048} take the fused kernel;
