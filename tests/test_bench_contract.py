@@ -56,6 +56,8 @@ def test_b200_arm_line():
     # configs[0] probe: one 4096x4096 tensor, decoded and verified
     c1 = d["c1"]
     assert c1["verified"] is True and c1["decode_us"] > 0 and 0 < c1["decode_frac"] < 1 and c1["compress_ms"] > 0
+    c3 = d["c3"]  # configs[2] probe: a lossy layer, decoded and checked
+    assert c3["verified"] is True and 0 < c3["decode_frac"] < 1 and c3["ratio"] > 2
     # throughput = algorithmic bytes over the timed steps
     bytes_step = d["config"]["bytes_algo_per_step"]
     assert d["value"] == pytest.approx(bytes_step / (d["ms_per_step"] / 1e3) / 1e9, rel=0.01)
